@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: mixed-precision preconditioned BiCGStab on the operational-size grid.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5]
+
+One STEP = one pass of every SURVEY.md §8(a) row over the resident synthetic problem:
+    eg_solver_set_operator (a1: diagonal scaling of the 7 fp64 bands)  +
+    eg_solve(b, x0 = 0, tol = 0, maxit = 8)  (a2 entry, 8 x a3-a10, a11 true-residual verification)
+value = BiCGStab iterations per second of the whole job = 8 * K / (device time of K steps),
+max over ranks.  For N > 1 (torchrun) the grid is split into latitude bands (strong scaling).
+
+Timing: CUDA events on the solver's stream, barrier + synchronize on both sides.  Inputs are far
+larger than L2 (46.8 GB of algorithmic traffic per iteration at C5), so no L2 flush is needed.
+The `--impl reference` arm times the CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BiCGStab iters/s & time-to-solve, 2560×1920×70 fp32; achieved HBM GB/s"
+ITERS_PER_STEP = 8
+# algorithmic HBM bytes per grid point per BiCGStab iteration:
+# 18 vector + 12 band + 2 x accesses: MIXED 136, FP64 256, FP32 128
+B_ALG = {"mixed": 136, "fp64": 256, "fp32": 128}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [t.strip() for t in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def oracle_sample(prob, precision, target_s=12.0):
+    """Time the CPU oracle on a bounded latitude sample of the workload (same nx, nz, recipe).
+    Returns dict(value = iters/s scaled to the full grid, ...)."""
+    import gen
+    import oracle
+    rows = 8
+    g = (prob.nx, rows, prob.nz)
+    sub = prob.with_(ny=rows)
+    bands, b = gen.host(sub)
+    ahat, diag = oracle.scale(g, bands, precision)
+    t0 = time.perf_counter()
+    oracle.solve(g, precision, ahat, diag, b, tol=0.0, maxit=1)
+    t1 = time.perf_counter() - t0
+    # choose rows (multiple of 8, <= ny) and iterations so the run is ~target_s
+    rows = int(max(8, min(prob.ny, 8 * round(rows * target_s / max(t1, 1e-3) / ITERS_PER_STEP / 8))))
+    g = (prob.nx, rows, prob.nz)
+    sub = prob.with_(ny=rows)
+    bands, b = gen.host(sub)
+    t0 = time.perf_counter()
+    ahat, diag = oracle.scale(g, bands, precision)
+    x, hist, info = oracle.solve(g, precision, ahat, diag, b, tol=0.0, maxit=ITERS_PER_STEP)
+    dt = time.perf_counter() - t0
+    frac = (prob.nx * rows * prob.nz) / prob.n
+    return {
+        "value": info.iters / dt * frac, "unit": "iter/s", "cores": oracle.threads(), "kind": "oracle",
+        "sample": (f"oracle_scale + oracle_solve({precision}, tol=0, maxit={ITERS_PER_STEP}) on a "
+                   f"{prob.nx}x{rows}x{prob.nz} latitude sample ({frac:.4f} of the grid) generated "
+                   f"with the same recipe; {dt:.2f} s wall; iters/s scaled by the point ratio"),
+        "seconds": dt,
+    }
+
+
+def run_reference(args, prob, ws, rank):
+    if rank != 0:
+        return
+    import oracle  # noqa: F401  (the reference arm is the CPU oracle)
+    for _ in range(args.warmup):
+        oracle_sample(prob, args.precision, target_s=1.0)
+    vals, secs = [], 0.0
+    last = None
+    for _ in range(args.steps):
+        last = oracle_sample(prob, args.precision, target_s=args.ref_seconds)
+        vals.append(last["value"])
+        secs += last["seconds"]
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * ITERS_PER_STEP / v,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision],
+        "data": "synthetic", "config": config_dict(args, prob, ws),
+        "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+DTYPE = {"mixed": "f32 (x, global sums f64)", "fp64": "f64", "fp32": "f32"}
+
+
+def config_dict(args, prob, ws):
+    return {
+        "workload": (f"{args.config}: {prob.nx}x{prob.ny}x{prob.nz} seed {prob.seed}, "
+                     f"c_v~U({prob.cv[0]:g},{prob.cv[1]:g}), {args.precision}, step = set_operator + "
+                     f"solve(tol=0, maxit={ITERS_PER_STEP})"),
+        "grid": [prob.nx, prob.ny, prob.nz], "precision": args.precision,
+        "iters_per_step": ITERS_PER_STEP, "parallelism": f"latitude-bands x{ws}",
+        "l2": "inputs larger than L2 (no flush needed)", "data": "synthetic (seeded generator, gen/)",
+    }
+
+
+def run_ours(args, prob, ws, rank, local):
+    import numpy as np
+    import torch
+
+    import gen
+    import paper_1811_03852_b200 as egs
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    group = None
+    if ws > 1:
+        import torch.distributed as dist
+        group = dist.group.WORLD
+    j0, j1 = egs.band_rows(prob.ny, rank, ws) if ws > 1 else (0, prob.ny)
+    nloc = (j1 - j0) * prob.nx * prob.nz
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        bands = torch.empty((7, nloc), dtype=torch.float64, device=dev)
+        b = torch.empty(nloc, dtype=torch.float64, device=dev)
+        gen.device(prob, bands, b, j0, j1, stream=stream)
+        x = torch.empty(nloc, dtype=torch.float64, device=dev)
+        s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, args.precision, group=group, stream=stream)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def step(flags, bb=b, xx=x):
+        s.set_operator(bands)
+        _, info, _ = s.solve(bb, tol=0.0, maxit=ITERS_PER_STEP, flags=flags, out=xx)
+        return info
+
+    def timed(nsteps, flags, bb=b, xx=x):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        infos = [step(flags, bb, xx) for _ in range(nsteps)]
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        if ws > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, infos
+
+    # warm-up (also captures the CUDA graph), then the timed region with per-kernel events
+    for _ in range(args.warmup):
+        step(egs.EG_SOLVE_PROFILE)
+    s.profile_reset()
+    with Clocks(local) as clk:
+        ms, infos = timed(args.steps, egs.EG_SOLVE_PROFILE)
+    prof = s.profile()
+    iters = sum(i.iters for i in infos)
+    value = iters / (ms / 1000.0)
+    launches = sum(v[1] for v in prof.values())
+
+    # dominant kernel roofline (algorithmic bytes / average CUDA-event duration)
+    peak, peak_src = peaks()
+    kname, (kms, kn, kbytes) = max(((k, v) for k, v in prof.items() if v[1] > 0), key=lambda kv: kv[1][0])
+    achieved = kbytes / (kms / kn / 1000.0) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.precision, {}).get(kname)
+        except Exception:
+            traffic = None
+    kernels = {k: {"avg_ms": v[0] / v[1], "launches": v[1], "alg_GBps": v[2] / (v[0] / v[1] / 1e3) / 1e9,
+                   "share": v[0] / sum(w[0] for w in prof.values())} for k, v in prof.items() if v[1] > 0}
+
+    # graph-replay timing (no per-kernel events) for comparison
+    ms_graph, infos_g = timed(args.steps, 0)
+    iters_g = sum(i.iters for i in infos_g)
+
+    # end to end through the public API with HOST buffers: b in (pinned), x out (pinned)
+    hb = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
+    hb.copy_(b)
+    hx = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
+    step(0, hb.numpy(), hx.numpy())
+    ms_e2e, infos_e = timed(args.steps, 0, hb.numpy(), hx.numpy())
+    iters_e = sum(i.iters for i in infos_e)
+
+    # time-to-solution at the operational tolerance, one solve, device events
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    barrier()
+    ev0.record(stream)
+    s.set_operator(bands)
+    _, tinfo, thist = s.solve(b, tol=1e-4, maxit=200, out=x)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    tts = ev0.elapsed_time(ev1)
+
+    if rank != 0:
+        return
+    n = prob.n
+    line = {
+        "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic",
+        "config": config_dict(args, prob, ws),
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "alg_bytes_per_launch": kbytes},
+        "iteration_roofline": {"alg_bytes_per_point": B_ALG[args.precision],
+                               "achieved_GBps": B_ALG[args.precision] * n * value / 1e9,
+                               "frac": B_ALG[args.precision] * n * value / 1e9 / peak,
+                               "note": "whole step incl. a1/a2/a11 and control, per iteration"},
+        "kernels": kernels,
+        "graph_replay": {"value": iters_g / (ms_graph / 1000.0), "ms_per_step": ms_graph / args.steps},
+        "e2e": {"value": iters_e / (ms_e2e / 1000.0), "unit": "iter/s",
+                "h2d_bytes_per_step": 8 * nloc, "d2h_bytes_per_step": 8 * nloc + 8 * (ITERS_PER_STEP + 1),
+                "ms_per_step": ms_e2e / args.steps},
+        "time_to_solution": {"tol": 1e-4, "ms": tts, "iters": tinfo.iters, "converged": tinfo.converged,
+                             "true_R": tinfo.true_R, "history": [float(v) for v in thist],
+                             "includes": "set_operator + solve (a1-a11)"},
+        "gpu_launches": int(launches),
+        "restarts_in_timed_region": int(sum(i.restarts for i in infos)),
+        "clocks": clk.summary(),
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        cb = oracle_sample(prob, args.precision, target_s=args.ref_seconds)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--precision", default="mixed", choices=["mixed", "fp64", "fp32"])
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    subprocess.check_call(["make", "-s", "all"], cwd=ROOT, stdout=subprocess.DEVNULL)
+    import gen
+    prob = gen.CONFIGS[args.config]
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, prob, ws, rank)
+    else:
+        run_ours(args, prob, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * egsolve.h — C ABI of the B200-native mixed-precision BiCGStab Helmholtz solver.
+ *
+ * Implements the hot path of Maynard & Walters, "Precision of the ENDGame: Mixed-precision
+ * arithmetic in the iterative solver of the Unified Model" (arXiv 1811.03852).  Citations "P:L"
+ * are lines of the paper's text; "A-n" are the readings listed in DESIGN.md §Readings.
+ *
+ *   A x = b                                (Eq. 1)  pressure-correction / Helmholtz system
+ *   D_g^-1 A C C^-1 x = D_g^-1 b           (Eq. 5) diagonal scaling outside the solver,
+ *                                           right ("post-") preconditioned BiCGStab
+ *   C^-1 = T^-1, T the vertical tridiagonal of Ahat (Eq. 6; reading A-3)
+ *   halt when R = ||r|| / ||b|| < R_c      (Eq. 8-9)
+ *   MIXED: x 64-bit, matrix / vectors / arithmetic / halos 32-bit, global sums 64-bit
+ *          (P:151-154); mandatory restart every 150 iterations.
+ *
+ * Every step runs in this library's sm_100a kernels; there is no CPU fallback.  No torch or CUDA
+ * types cross this boundary: device buffers are plain pointers, streams are `void*`
+ * (a cudaStream_t), sizes are int64_t / size_t.
+ *
+ * GRID AND LAYOUT.  nx longitudes (periodic, nx >= 3), ny latitudes (zero-flux at j = 0 and
+ * j = ny-1), nz levels (zero-flux at k = 0 and k = nz-1).  Every field — bands, b, x, vectors —
+ * is stored longitude-fastest ("IKJ"):  q = i + nx*(k + nz*j_local),  j_local = j - j_begin.
+ * A latitude row is one contiguous block of nx*nz values, so a latitude band is one contiguous
+ * chunk.  (The paper fixes no layout; DESIGN.md §Layout explains the choice.)
+ *
+ * BANDS.  Seven unscaled fp64 coefficient arrays in the order C (diagonal), E (i+1), W (i-1),
+ * N (j+1), S (j-1), U (k+1), D (k-1); band d at point q multiplies x at neighbour d of q.
+ * A band at an absent neighbour (N at j = ny-1, S at j = 0, U at k = nz-1, D at k = 0) must be 0.
+ *
+ * THREADING.  One handle is not thread-safe; separate handles are independent.  All device work
+ * is ordered on the stream given to eg_solver_create.
+ */
+#ifndef EGSOLVE_H
+#define EGSOLVE_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (returned by every int function; 0 = success) ---- */
+#define EG_OK 0
+#define EG_ERR_ARG 1             /* invalid argument / grid / decomposition / layout            */
+#define EG_ERR_SINGULAR_DIAG 2   /* some a_C is 0 or non-finite                         */
+#define EG_ERR_DEGENERATE_RHS 3  /* ||D_g^-1 b|| = 0                                    */
+#define EG_ERR_BREAKDOWN 4       /* two consecutive BiCGStab breakdowns without progress (A-12) */
+#define EG_ERR_NONFINITE 5       /* non-finite value in the iteration               */
+#define EG_ERR_CUDA 6            /* CUDA runtime error (see eg_last_error)                      */
+#define EG_ERR_NCCL 7            /* NCCL error (see eg_last_error)                              */
+#define EG_ERR_WORKSPACE 8       /* workspace too small or misaligned                           */
+
+typedef struct eg_solver eg_solver;
+
+typedef struct {
+    int64_t nx, ny, nz; /* GLOBAL grid */
+} eg_grid;
+
+/* Precision policy (Table 1 "Mixed-precision" vs "Double precision").
+ *   EG_FP64  : everything binary64 ("DP").
+ *   EG_MIXED : x binary64; scaled bands, Krylov vectors, their arithmetic and the halo exchange
+ *              binary32; global sums binary64 ("MP" after the 64-bit-sum fix).
+ *   EG_FP32  : everything binary32 including the global sums (the original MP sums / toy SP). */
+typedef enum { EG_FP64 = 0, EG_MIXED = 1, EG_FP32 = 2 } eg_precision;
+
+/* Latitude-band decomposition over nranks GPUs (one process per GPU).  Rows [j_begin, j_end) are
+ * local.  NULL = one GPU owning all rows.  With nranks > 1 the bands must be contiguous in rank
+ * order and aligned to the 8 fixed reduction row-groups (group g = rows [g*ny/G, (g+1)*ny/G),
+ * G = min(8, ny)), i.e. nranks must divide G; that fixed grouping makes every global sum — and
+ * so x and the history — bitwise identical for any nranks.  nccl_unique_id points to the 128-byte
+ * ncclUniqueId from eg_nccl_unique_id() on rank 0, broadcast by the caller (NULL if nranks == 1). */
+typedef struct {
+    int64_t j_begin, j_end;
+    int32_t rank, nranks;
+    const void* nccl_unique_id;
+} eg_dist;
+
+/* flags for eg_solve_params.flags */
+#define EG_SOLVE_NO_GRAPH 1u  /* launch each kernel directly instead of replaying a CUDA graph  */
+#define EG_SOLVE_PROFILE 2u   /* record CUDA events around every kernel (implies NO_GRAPH);     */
+                              /* read with eg_profile_get                                       */
+
+typedef struct {
+    double tol;             /* R_c; 0 = no halting criterion, run maxit   */
+    int32_t maxit;          /* >= 0                                                          */
+    int32_t restart_every;  /* mandatory restart period (P:553-557, 150 in the UM); <= 0 off */
+    uint32_t flags;         /* EG_SOLVE_*                                                    */
+    int32_t check_every;    /* iterations between host polls of the device flags; 0 = auto   */
+} eg_solve_params;
+
+typedef struct {
+    int32_t iters;       /* completed BiCGStab iterations (an s-step exit counts, A-7/A-8)   */
+    int32_t converged;   /* 1 iff the verified true residual R_true < tol (A-6)             */
+    int32_t restarts;    /* mandatory + breakdown + failed-verification restarts             */
+    int32_t breakdowns;  /* scalar-weight breakdowns (A-12)                                  */
+    int32_t status;      /* same code eg_solve returns                                       */
+    double final_R;      /* last recorded R (history[iters])                                 */
+    double true_R;       /* ||bhat - Ahat x|| / ||bhat|| recomputed with fp64 accumulation   */
+} eg_solve_info;
+
+/* Bytes of device workspace the caller must provide to eg_solver_create for this grid, local
+ * band and precision (PyTorch owns all device memory).  Returns EG_OK or EG_ERR_ARG. */
+int eg_workspace_bytes(const eg_grid* grid, const eg_dist* dist, eg_precision prec, size_t* bytes);
+
+/* a1 — create a solver: scales the operator "outside the solver" (Eq. 5):
+ * Ahat_d = a_d / a_C (binary64 IEEE division, then rounded to the working precision), the fp64
+ * diagonal kept for scaling b.  bands[7]: DEVICE fp64 arrays of the local rows (layout above);
+ * read during this call only — the caller may free them after return.  workspace: DEVICE buffer
+ * of >= eg_workspace_bytes, 256-byte aligned, owned by the caller, must outlive the solver.
+ * stream: the cudaStream_t all work is ordered on.  With dist->nranks > 1 this call is collective
+ * (creates the NCCL communicator).  Blocks until the validation flags are read.
+ * Errors: EG_ERR_ARG (dims, nx < 3, decomposition, nonzero band at an absent neighbour or
+ * non-finite band), EG_ERR_SINGULAR_DIAG, EG_ERR_WORKSPACE, EG_ERR_CUDA, EG_ERR_NCCL.
+ * On error *out is NULL. */
+int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* const bands[7],
+                     eg_precision prec, void* workspace, size_t workspace_bytes, void* stream,
+                     eg_solver** out);
+
+/* a1 again on an existing solver: re-scale a NEW operator of the same grid / band / precision into
+ * the workspace ("the matrix is time varying and so needs to be recomputed at every time step",
+ * P:217-220).  Same inputs, errors and blocking behaviour as eg_solver_create, without allocation
+ * or communicator setup.  On error the previous operator is no longer valid. */
+int eg_solver_set_operator(eg_solver* s, const double* const bands[7]);
+
+/* y = Ahat x, the scaled operator the solver iterates with (unit diagonal + 6 bands; periodic in i,
+ * absent neighbours contribute 0).  x, y: DEVICE arrays of the local rows in the working precision
+ * (float for EG_MIXED / EG_FP32, double for EG_FP64).  Exchanges halo rows when distributed
+ * (collective).  Stream-ordered; returns without synchronising. */
+int eg_apply_operator(eg_solver* s, const void* x, void* y);
+
+/* z = T^-1 r per column (the applied preconditioner, reading A-3): T = tridiag(D_k, 1, U_k) of the
+ * scaled vertical bands, Thomas recurrence without pivoting (A-14), working precision, no
+ * communication (no vertical decomposition).  Stream-ordered. */
+int eg_precondition(eg_solver* s, const void* r, void* z);
+
+/* Solve Ahat x = D_g^-1 b by right-preconditioned BiCGStab (algorithm in DESIGN.md).
+ * b: fp64 local rows.  x0: fp64 local rows or NULL (= 0).  x: fp64 output, local rows.
+ * b, x0 and x may each be DEVICE or HOST memory (host buffers are copied in / out inside the call).
+ * history: HOST array of >= params->maxit + 1 doubles: history[0] = true R of x0,
+ * history[i] = R after iteration i (may be NULL).  info: HOST, may be NULL.
+ * Blocks until done.  Not converging within maxit is NOT an error (info->converged = 0).
+ * Errors: EG_ERR_ARG, EG_ERR_DEGENERATE_RHS, EG_ERR_NONFINITE, EG_ERR_BREAKDOWN, EG_ERR_CUDA,
+ * EG_ERR_NCCL; info / history / x stay valid up to the failure point. */
+int eg_solve(eg_solver* s, const double* b, const double* x0, const eg_solve_params* params,
+             double* x, double* history, eg_solve_info* info);
+
+/* Release the NCCL communicator, events and graphs (not the caller's workspace). NULL is a no-op. */
+void eg_solver_destroy(eg_solver* s);
+
+/* Human-readable detail of the last error on this handle ("" if none).  Valid until the next call. */
+const char* eg_last_error(const eg_solver* s);
+const char* eg_status_str(int status);
+
+/* Fill out[128] with a fresh ncclUniqueId (call on rank 0, broadcast to the others). */
+int eg_nccl_unique_id(char out[128]);
+
+/* ---- kernel-level profiling (EG_SOLVE_PROFILE): CUDA events on the solver's stream ---- */
+int eg_num_kernels(void);
+const char* eg_kernel_name(int kernel_id);
+/* Accumulated device time (ms) and launch count of one kernel since the last reset, and its
+ * ALGORITHMIC HBM bytes per launch for this solver's grid / precision. */
+int eg_profile_get(const eg_solver* s, int kernel_id, double* total_ms, int64_t* launches,
+                   double* alg_bytes_per_launch);
+int eg_profile_reset(eg_solver* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,740 @@
+// egsolve.cu — the C ABI (include/egsolve.h) over the sm_100a kernels in kernels.cuh.
+//
+// Host responsibilities only: validation, workspace carving, launch geometry, the restart /
+// verification state machine of DESIGN.md §Algorithm (mirrors), CUDA-graph
+// replay of the iteration, NCCL halo exchange and group-sum all-gather for latitude bands, and
+// per-kernel CUDA-event profiling.  All arithmetic of the method runs in the kernels.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "egsolve.h"
+#include "kernels.cuh"
+
+using namespace eg;
+
+namespace {
+
+enum KernelId {
+    KID_SCALE = 0, KID_START, KID_FIN, KID_THOMAS_P, KID_STENCIL_A, KID_THOMAS_S, KID_STENCIL_B,
+    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_COUNT
+};
+const char* kKernelNames[KID_COUNT] = {"scale", "start", "finalize", "thomas_p", "stencil_dot_A",
+                                       "thomas_s", "stencil_dot_B", "update_xr", "apply",
+                                       "precondition", "convert"};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+    size_t off_bands, off_diag, off_bhat, off_x64, off_x32, off_xg, off_vec, off_z, off_slots,
+        off_gsum, off_state, total;
+    size_t vsz;      // sizeof(V)
+    size_t xsz;      // sizeof(X)
+    int64_t n, row, nyl;
+    int tiles, G;
+};
+
+int vsize(int mode) { return mode == EG_FP64 ? 8 : 4; }
+int xsize(int mode) { return mode == EG_FP32 ? 4 : 8; }
+
+bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L) {
+    const size_t A = 256;
+    L->row = g->nx * g->nz;
+    L->nyl = nyl;
+    L->n = nyl * L->row;
+    L->vsz = vsize(mode);
+    L->xsz = xsize(mode);
+    L->tiles = (int)((g->nx + RW - 1) / RW);
+    L->G = (int)std::min<int64_t>(8, g->ny);
+    const size_t n = (size_t)L->n, row = (size_t)L->row;
+    size_t o = 0;
+    L->off_bands = o; o = align_up(o + 6 * n * L->vsz, A);
+    L->off_diag = o;  o = align_up(o + n * 8, A);
+    L->off_bhat = o;  o = align_up(o + n * 8, A);
+    L->off_x64 = o;   o = align_up(o + n * 8, A);
+    L->off_x32 = o;   o = align_up(o + (mode == EG_FP32 ? n * 4 : 0), A);
+    L->off_xg = o;    o = align_up(o + 2 * row * 8, A);
+    L->off_vec = o;   o = align_up(o + 6 * align_up(n * L->vsz, A), A);
+    L->off_z = o;     o = align_up(o + 2 * align_up((n + 2 * row) * L->vsz, A), A);
+    L->off_slots = o; o = align_up(o + 3 * (size_t)nyl * L->tiles * 8, A);
+    L->off_gsum = o;  o = align_up(o + 2 * 8 * 3 * 8, A);
+    L->off_state = o; o = align_up(o + sizeof(DevState), A);
+    L->total = o;
+    return true;
+}
+
+struct PendingEv { int kid; cudaEvent_t a, b; };
+
+}  // namespace
+
+struct eg_solver {
+    eg_grid grid{};
+    int64_t j_begin = 0, j_end = 0;
+    int rank = 0, nranks = 1;
+    int mode = EG_MIXED;
+    cudaStream_t st = nullptr;
+    cudaStream_t cap_st = nullptr;  // private stream used only to capture the iteration graph
+    Layout L{};
+    Geo geo{};
+    unsigned char* ws = nullptr;
+    // carved pointers
+    void* bands[6]{};
+    double* diag = nullptr;
+    double* bhat = nullptr;
+    double* x64 = nullptr;
+    float* x32 = nullptr;
+    double* xg = nullptr;  // [2][row] ghost rows of x (X-typed)
+    void* vec[6]{};        // r, rh, p, v, s, t
+    void* zext[2]{};       // ghosted z, zs (row -1 .. nyl)
+    double* slots = nullptr;
+    double* gsum = nullptr;  // [G][3] local
+    double* gall = nullptr;  // [G][3] all ranks
+    DevState* dstate = nullptr;
+    DevState* hstate = nullptr;  // pinned host mirror
+    int wth = 128;               // Thomas CTA width
+    size_t smem_th = 0;
+    // graph of one iteration, keyed on the iterate pointer
+    cudaGraphExec_t graph = nullptr;
+    void* graph_x = nullptr;
+    // NCCL
+    ncclComm_t comm = nullptr;
+    // profiling
+    bool profiling = false;
+    std::vector<cudaEvent_t> evpool;
+    std::vector<PendingEv> pending;
+    double prof_ms[KID_COUNT]{};
+    int64_t prof_n[KID_COUNT]{};
+    std::string err;
+};
+
+namespace {
+
+int fail(eg_solver* s, int code, const char* fmt, ...) {
+    if (s) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        s->err = buf;
+    }
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(s, EG_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,            \
+                        cudaGetErrorString(e_));                                              \
+    } while (0)
+
+#define NK(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(s, EG_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,            \
+                        ncclGetErrorString(r_));                                              \
+    } while (0)
+
+// -------- profiling helpers --------
+cudaEvent_t take_event(eg_solver* s) {
+    if (s->evpool.empty()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    cudaEvent_t e = s->evpool.back();
+    s->evpool.pop_back();
+    return e;
+}
+
+struct ProfScope {
+    eg_solver* s;
+    int kid;
+    cudaEvent_t a = nullptr;
+    ProfScope(eg_solver* s_, int k) : s(s_), kid(k) {
+        if (s->profiling) {
+            a = take_event(s);
+            cudaEventRecord(a, s->st);
+        }
+    }
+    ~ProfScope() {
+        if (s->profiling) {
+            cudaEvent_t b = take_event(s);
+            cudaEventRecord(b, s->st);
+            s->pending.push_back({kid, a, b});
+        }
+    }
+};
+
+void drain_profile(eg_solver* s) {
+    for (auto& p : s->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            s->prof_ms[p.kid] += ms;
+            s->prof_n[p.kid] += 1;
+        }
+        s->evpool.push_back(p.a);
+        s->evpool.push_back(p.b);
+    }
+    s->pending.clear();
+}
+
+template <int MODE>
+Vecs<MODE> vecs(eg_solver* s, void* x_it) {
+    using V = typename Prec<MODE>::V;
+    using X = typename Prec<MODE>::X;
+    Vecs<MODE> v;
+    v.E = (const V*)s->bands[0]; v.W = (const V*)s->bands[1]; v.N = (const V*)s->bands[2];
+    v.S = (const V*)s->bands[3]; v.U = (const V*)s->bands[4]; v.D = (const V*)s->bands[5];
+    v.diag = s->diag;
+    v.bhat = s->bhat;
+    v.x = (X*)x_it;
+    v.xg_lo = (const X*)s->xg;
+    v.xg_hi = (const X*)((unsigned char*)s->xg + s->L.row * 8);
+    v.r = (V*)s->vec[0]; v.rh = (V*)s->vec[1]; v.p = (V*)s->vec[2];
+    v.v = (V*)s->vec[3]; v.s = (V*)s->vec[4]; v.t = (V*)s->vec[5];
+    v.z = (V*)s->zext[0] + s->L.row;
+    v.zs = (V*)s->zext[1] + s->L.row;
+    v.slots = s->slots;
+    v.st = s->dstate;
+    return v;
+}
+
+// -------- multi-GPU plumbing (latitude bands) --------
+// exchange the boundary rows of a ghosted array with the j-neighbours
+int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz) {
+    if (s->nranks == 1) return EG_OK;
+    const size_t rowb = (size_t)s->L.row * esz;
+    ncclDataType_t ty = esz == 8 ? ncclDouble : ncclFloat;
+    unsigned char* first = (unsigned char*)row0;
+    unsigned char* last = first + (size_t)(s->L.nyl - 1) * rowb;
+    NK(ncclGroupStart());
+    if (s->rank > 0) {
+        NK(ncclSend(first, s->L.row, ty, s->rank - 1, s->comm, s->st));
+        NK(ncclRecv(ghost_lo, s->L.row, ty, s->rank - 1, s->comm, s->st));
+    }
+    if (s->rank < s->nranks - 1) {
+        NK(ncclSend(last, s->L.row, ty, s->rank + 1, s->comm, s->st));
+        NK(ncclRecv(ghost_hi, s->L.row, ty, s->rank + 1, s->comm, s->st));
+    }
+    NK(ncclGroupEnd());
+    return EG_OK;
+}
+
+int halo_ghosted(eg_solver* s, void* zrow0) {
+    const size_t esz = s->L.vsz, rowb = (size_t)s->L.row * esz;
+    unsigned char* r0 = (unsigned char*)zrow0;
+    return halo(s, r0, r0 - rowb, r0 + (size_t)s->L.nyl * rowb, esz);
+}
+
+template <int MODE, int WHICH>
+int finalize(eg_solver* s, int first) {
+    ProfScope ps(s, KID_FIN);
+    if (s->nranks == 1) {
+        k_fin<MODE, WHICH><<<1, 1024, 0, s->st>>>(s->geo, s->slots, s->dstate, s->gsum, first);
+        CK(cudaGetLastError());
+        return EG_OK;
+    }
+    constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
+    k_fin_groups<MODE, WHICH><<<1, 1024, 0, s->st>>>(s->geo, s->slots, s->dstate, s->gsum);
+    CK(cudaGetLastError());
+    const int gl = s->geo.g_hi - s->geo.g_lo;
+    NK(ncclAllGather(s->gsum, s->gall, (size_t)gl * NQ, ncclDouble, s->comm, s->st));
+    k_fin_logic<MODE, WHICH><<<1, 32, 0, s->st>>>(s->geo, s->gall, s->dstate, first);
+    CK(cudaGetLastError());
+    return EG_OK;
+}
+
+// -------- the iteration (rows a3-a10) --------
+template <int MODE>
+int iteration(eg_solver* s, void* x_it) {
+    using V = typename Prec<MODE>::V;
+    Vecs<MODE> v = vecs<MODE>(s, x_it);
+    const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
+    const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+    int rc;
+    {
+        ProfScope ps(s, KID_THOMAS_P);
+        k_thomas<MODE, 1><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+        CK(cudaGetLastError());
+    }
+    if ((rc = halo_ghosted(s, v.z))) return rc;
+    {
+        ProfScope ps(s, KID_STENCIL_A);
+        k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh);
+        CK(cudaGetLastError());
+    }
+    if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
+    {
+        ProfScope ps(s, KID_THOMAS_S);
+        k_thomas<MODE, 2><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+        CK(cudaGetLastError());
+    }
+    if ((rc = halo_ghosted(s, v.zs))) return rc;
+    {
+        ProfScope ps(s, KID_STENCIL_B);
+        k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s);
+        CK(cudaGetLastError());
+    }
+    if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
+    {
+        ProfScope ps(s, KID_UPDATE);
+        k_update<MODE><<<gr, RW, 0, s->st>>>(s->geo, v);
+        CK(cudaGetLastError());
+    }
+    if ((rc = finalize<MODE, W_C>(s, 0))) return rc;
+    (void)sizeof(V);
+    return EG_OK;
+}
+
+// start / restart / verification (rows a2, a11)
+template <int MODE>
+int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero) {
+    using X = typename Prec<MODE>::X;
+    Vecs<MODE> v = vecs<MODE>(s, x_it);
+    int rc;
+    if (!xzero && s->nranks > 1) {  // fp64 (X) ghost rows of x
+        X* x = (X*)x_it;
+        if ((rc = halo(s, x, s->xg, (unsigned char*)s->xg + s->L.row * 8, sizeof(X)))) return rc;
+    }
+    const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+    {
+        ProfScope ps(s, KID_START);
+        k_start<MODE><<<gr, RW, 0, s->st>>>(s->geo, v, b, entry, xzero);
+        CK(cudaGetLastError());
+    }
+    return finalize<MODE, W_START>(s, entry);
+}
+
+int read_state(eg_solver* s) {
+    CK(cudaMemcpyAsync(s->hstate, s->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    if (s->profiling) drain_profile(s);
+    return EG_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <int MODE>
+int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_params* prm, double* x,
+               double* history, eg_solve_info* info) {
+    using X = typename Prec<MODE>::X;
+    const int64_t n = s->L.n;
+    int rc = EG_OK;
+    s->profiling = (prm->flags & EG_SOLVE_PROFILE) != 0;
+    const bool use_graph = !(prm->flags & (EG_SOLVE_NO_GRAPH | EG_SOLVE_PROFILE));
+    eg_solve_info inf{};
+
+    // ---- inputs: b (host -> staged into bhat, scaled in place), x iterate ----
+    const double* bdev = b;
+    if (!is_device_ptr(b)) {
+        CK(cudaMemcpyAsync(s->bhat, b, n * 8, cudaMemcpyHostToDevice, s->st));
+        bdev = s->bhat;
+    }
+    const bool xdev = is_device_ptr(x);
+    void* x_it;
+    if (MODE == 2) x_it = s->x32;
+    else x_it = xdev ? (void*)x : (void*)s->x64;
+    if (x0) {
+        if (MODE == 2) {
+            const double* x0d = x0;
+            if (!is_device_ptr(x0)) {
+                CK(cudaMemcpyAsync(s->x64, x0, n * 8, cudaMemcpyHostToDevice, s->st));
+                x0d = s->x64;
+            }
+            ProfScope ps(s, KID_CONVERT);
+            k_convert<double, float><<<1184, 256, 0, s->st>>>(x0d, s->x32, n);
+            CK(cudaGetLastError());
+        } else if (x0 != x_it) {
+            CK(cudaMemcpyAsync(x_it, x0, n * 8, cudaMemcpyDefault, s->st));
+        }
+    }
+
+    // ---- device state ----
+    DevState* h = s->hstate;
+    memset(h, 0, sizeof(DevState));
+    h->tol = prm->tol;
+    h->maxit = prm->maxit;
+    h->restart_every = prm->restart_every;
+    h->eps_v = MODE == 0 ? 0x1.0p-53 : 0x1.0p-24;
+    h->omega = h->omega_v = 1.0;
+    CK(cudaMemcpyAsync(s->dstate, h, sizeof(DevState), cudaMemcpyHostToDevice, s->st));
+
+    if ((rc = start<MODE>(s, x_it, bdev, 1, x0 == nullptr))) return rc;
+    if ((rc = read_state(s))) return rc;
+    if (h->halt == H_DEGENERATE) rc = EG_ERR_DEGENERATE_RHS;
+    else if (h->halt == H_NONFINITE) rc = EG_ERR_NONFINITE;
+    if (history && rc == EG_OK) history[0] = h->hist[0];
+    int copied = 0;
+    int bd_at = -1;
+    const int chunk_max = prm->check_every > 0 ? std::min(prm->check_every, HIST_CAP) : 8;
+
+    // graph for this iterate pointer
+    if (use_graph && rc == EG_OK && (s->graph == nullptr || s->graph_x != x_it)) {
+        if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
+        cudaGraph_t gph;
+        if (!s->cap_st) CK(cudaStreamCreateWithFlags(&s->cap_st, cudaStreamNonBlocking));
+        cudaStream_t user = s->st;
+        s->st = s->cap_st;  // the user's stream may be the legacy stream, which cannot capture
+        cudaError_t cb = cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal);
+        int irc = cb == cudaSuccess ? iteration<MODE>(s, x_it) : EG_OK;
+        cudaGraph_t tmp = nullptr;
+        cudaError_t ce = cb == cudaSuccess ? cudaStreamEndCapture(s->st, &tmp) : cb;
+        gph = tmp;
+        s->st = user;
+        if (irc) return irc;
+        CK(ce);
+        CK(cudaGraphInstantiate(&s->graph, gph, 0));
+        cudaGraphDestroy(gph);
+        s->graph_x = x_it;
+    }
+
+    while (rc == EG_OK) {
+        if (h->halt == H_START_CONVERGED) { inf.converged = 1; break; }
+        if (h->halt == H_START_MAXIT) break;
+        // run iterations until the device raises a halt flag
+        while (h->halt == H_RUN) {
+            const int left = h->maxit - h->iter;
+            const int k = std::max(1, std::min(chunk_max, left));
+            for (int c = 0; c < k; ++c) {
+                if (use_graph) CK(cudaGraphLaunch(s->graph, s->st));
+                else if ((rc = iteration<MODE>(s, x_it))) return rc;
+            }
+            if ((rc = read_state(s))) return rc;
+            if (history)
+                for (int i = copied + 1; i <= h->iter; ++i) history[i] = h->hist[i % HIST_CAP];
+            copied = h->iter;
+        }
+        const int halt = h->halt;
+        if (halt == H_NONFINITE) { rc = EG_ERR_NONFINITE; break; }
+        if (halt == H_BD_ABORT || halt == H_BD_END) {
+            inf.breakdowns++;
+            if (bd_at == h->iter) { rc = EG_ERR_BREAKDOWN; break; }
+            bd_at = h->iter;
+        }
+        // H_CONVERGED -> verify; H_RESTART / breakdown -> restart; H_MAXIT -> final true residual.
+        // All four recompute r = round(bhat - Ahat x) with fp64 accumulation (A-6, A-11).
+        if ((rc = start<MODE>(s, x_it, bdev, 0, 0))) return rc;
+        if ((rc = read_state(s))) return rc;
+        if (halt == H_MAXIT) break;
+        if (h->halt == H_START_CONVERGED) { inf.converged = 1; break; }
+        if (h->halt == H_START_MAXIT) break;
+        inf.restarts++;
+    }
+
+    // ---- output x (fp64) ----
+    if (MODE == 2) {
+        double* dst = xdev ? x : s->x64;
+        {
+            ProfScope ps(s, KID_CONVERT);
+            k_convert<float, double><<<1184, 256, 0, s->st>>>(s->x32, dst, n);
+            CK(cudaGetLastError());
+        }
+        if (!xdev) CK(cudaMemcpyAsync(x, s->x64, n * 8, cudaMemcpyDeviceToHost, s->st));
+    } else if (!xdev) {
+        CK(cudaMemcpyAsync(x, x_it, n * 8, cudaMemcpyDeviceToHost, s->st));
+    }
+    CK(cudaStreamSynchronize(s->st));
+    if (s->profiling) drain_profile(s);
+    inf.iters = h->iter;
+    inf.final_R = h->final_R;
+    inf.true_R = h->true_R;
+    inf.status = rc;
+    if (info) *info = inf;
+    (void)sizeof(X);
+    return rc;
+}
+
+template <int MODE>
+int create_impl(eg_solver* s, const double* const bands[7]) {
+    using V = typename Prec<MODE>::V;
+    Bands7 in;
+    for (int d = 0; d < 7; ++d) in.b[d] = bands[d];
+    int* err = (int*)&s->dstate->err;
+    CK(cudaMemsetAsync(s->dstate, 0, sizeof(DevState), s->st));
+    const dim3 grid((unsigned)((s->grid.nx + 255) / 256), (unsigned)s->grid.nz, (unsigned)s->L.nyl);
+    {
+        ProfScope ps(s, KID_SCALE);
+        k_scale<V><<<grid, 256, 0, s->st>>>(s->geo, in, (V*)s->bands[0], (V*)s->bands[1],
+                                            (V*)s->bands[2], (V*)s->bands[3], (V*)s->bands[4],
+                                            (V*)s->bands[5], s->diag, err);
+        CK(cudaGetLastError());
+    }
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    if (herr & 2) return fail(s, EG_ERR_SINGULAR_DIAG, "a_C is zero or non-finite at some point");
+    if (herr & 1)
+        return fail(s, EG_ERR_ARG, "non-finite band, or nonzero band at an absent neighbour");
+    return EG_OK;
+}
+
+template <int MODE>
+int apply_impl(eg_solver* s, const void* x, void* y) {
+    Vecs<MODE> v = vecs<MODE>(s, s->x64);
+    using V = typename Prec<MODE>::V;
+    const V* zin = (const V*)x;
+    int rc;
+    if (s->nranks > 1) {  // stage into the ghosted buffer and exchange halo rows
+        CK(cudaMemcpyAsync(v.z, x, s->L.n * sizeof(V), cudaMemcpyDeviceToDevice, s->st));
+        if ((rc = halo_ghosted(s, v.z))) return rc;
+        zin = v.z;
+    }
+    const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+    ProfScope ps(s, KID_APPLY);
+    k_stencil<MODE, 0><<<gr, RW, 0, s->st>>>(s->geo, v, zin, (V*)y, nullptr);
+    CK(cudaGetLastError());
+    return EG_OK;
+}
+
+template <int MODE>
+int precond_impl(eg_solver* s, const void* r, void* z) {
+    using V = typename Prec<MODE>::V;
+    Vecs<MODE> v = vecs<MODE>(s, s->x64);
+    const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
+    ProfScope ps(s, KID_PRECOND);
+    k_thomas<MODE, 0><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, (const V*)r, (V*)z);
+    CK(cudaGetLastError());
+    return EG_OK;
+}
+
+template <int MODE>
+int set_thomas_smem(eg_solver* s) {
+    CK(cudaFuncSetAttribute(k_thomas<MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    CK(cudaFuncSetAttribute(k_thomas<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    CK(cudaFuncSetAttribute(k_thomas<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    return EG_OK;
+}
+
+bool valid_dist(const eg_grid* g, const eg_dist* d, int64_t* jb, int64_t* je, int* rank, int* nranks) {
+    if (!d) { *jb = 0; *je = g->ny; *rank = 0; *nranks = 1; return true; }
+    *jb = d->j_begin; *je = d->j_end; *rank = d->rank; *nranks = d->nranks;
+    if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return false;
+    if (d->j_begin < 0 || d->j_end > g->ny || d->j_end <= d->j_begin) return false;
+    if (d->nranks == 1) return d->j_begin == 0 && d->j_end == g->ny;
+    const int G = (int)std::min<int64_t>(8, g->ny);
+    if (G % d->nranks) return false;
+    const int per = G / d->nranks;
+    const int64_t b0 = (int64_t)(d->rank * per) * g->ny / G, b1 = (int64_t)((d->rank + 1) * per) * g->ny / G;
+    return d->j_begin == b0 && d->j_end == b1;
+}
+
+bool valid_grid(const eg_grid* g) {
+    return g && g->nx >= 3 && g->ny >= 1 && g->nz >= 1 && g->nx * g->nz < (int64_t)1 << 31 &&
+           g->ny < 65536 && g->nz < 65536;
+}
+
+}  // namespace
+
+// =================================== C ABI ===================================
+
+extern "C" {
+
+int eg_workspace_bytes(const eg_grid* grid, const eg_dist* dist, eg_precision prec, size_t* bytes) {
+    int64_t jb, je;
+    int rank, nranks;
+    if (!valid_grid(grid) || !bytes || prec < EG_FP64 || prec > EG_FP32) return EG_ERR_ARG;
+    if (!valid_dist(grid, dist, &jb, &je, &rank, &nranks)) return EG_ERR_ARG;
+    Layout L;
+    make_layout(grid, je - jb, prec, &L);
+    *bytes = L.total;
+    return EG_OK;
+}
+
+int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* const bands[7],
+                     eg_precision prec, void* workspace, size_t workspace_bytes, void* stream,
+                     eg_solver** out) {
+    if (!out) return EG_ERR_ARG;
+    *out = nullptr;
+    if (!valid_grid(grid) || !bands || prec < EG_FP64 || prec > EG_FP32 || !workspace)
+        return EG_ERR_ARG;
+    for (int d = 0; d < 7; ++d)
+        if (!bands[d]) return EG_ERR_ARG;
+    eg_solver* s = new eg_solver();
+    s->grid = *grid;
+    s->mode = prec;
+    s->st = (cudaStream_t)stream;
+    if (!valid_dist(grid, dist, &s->j_begin, &s->j_end, &s->rank, &s->nranks)) {
+        delete s;
+        return EG_ERR_ARG;
+    }
+    make_layout(grid, s->j_end - s->j_begin, prec, &s->L);
+    if (workspace_bytes < s->L.total || ((uintptr_t)workspace & 255)) {
+        delete s;
+        return EG_ERR_WORKSPACE;
+    }
+    s->ws = (unsigned char*)workspace;
+    const Layout& L = s->L;
+    for (int d = 0; d < 6; ++d) s->bands[d] = s->ws + L.off_bands + (size_t)d * L.n * L.vsz;
+    s->diag = (double*)(s->ws + L.off_diag);
+    s->bhat = (double*)(s->ws + L.off_bhat);
+    s->x64 = (double*)(s->ws + L.off_x64);
+    s->x32 = (float*)(s->ws + L.off_x32);
+    s->xg = (double*)(s->ws + L.off_xg);
+    for (int d = 0; d < 6; ++d) s->vec[d] = s->ws + L.off_vec + (size_t)d * align_up(L.n * L.vsz, 256);
+    for (int d = 0; d < 2; ++d)
+        s->zext[d] = s->ws + L.off_z + (size_t)d * align_up((L.n + 2 * L.row) * L.vsz, 256);
+    s->slots = (double*)(s->ws + L.off_slots);
+    s->gsum = (double*)(s->ws + L.off_gsum);
+    s->gall = s->gsum + 8 * 3;
+    s->dstate = (DevState*)(s->ws + L.off_state);
+    if (cudaMallocHost(&s->hstate, sizeof(DevState)) != cudaSuccess) {
+        delete s;
+        return EG_ERR_CUDA;
+    }
+    Geo& g = s->geo;
+    g.nx = grid->nx; g.ny = grid->ny; g.nz = grid->nz;
+    g.row = L.row; g.nyl = L.nyl; g.j0 = s->j_begin; g.n = L.n; g.tiles = L.tiles;
+    g.G = L.G;
+    g.g_lo = s->rank * (L.G / s->nranks);
+    g.g_hi = (s->rank + 1) * (L.G / s->nranks);
+    // Thomas CTA width: keep 2*nz*W*sizeof(V) of factors in shared memory <= ~76 KB
+    s->wth = 128;
+    while (s->wth > 32 && 2 * (size_t)grid->nz * s->wth * L.vsz > 77824) s->wth /= 2;
+    s->smem_th = 2 * (size_t)grid->nz * s->wth * L.vsz;
+    if (s->smem_th > 227 * 1024) {
+        int rc = fail(s, EG_ERR_ARG, "nz=%lld too large for the shared-memory Thomas kernel", (long long)grid->nz);
+        eg_solver_destroy(s);
+        return rc;
+    }
+    int rc = prec == EG_FP64 ? set_thomas_smem<0>(s) : prec == EG_MIXED ? set_thomas_smem<1>(s) : set_thomas_smem<2>(s);
+    if (rc == EG_OK && s->nranks > 1) {
+        if (!dist->nccl_unique_id) {
+            rc = EG_ERR_ARG;
+        } else {
+            ncclUniqueId id;
+            memcpy(&id, dist->nccl_unique_id, sizeof id);
+            ncclResult_t r = ncclCommInitRank(&s->comm, s->nranks, id, s->rank);
+            if (r != ncclSuccess) rc = fail(s, EG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+        }
+    }
+    if (rc == EG_OK)
+        rc = prec == EG_FP64 ? create_impl<0>(s, bands) : prec == EG_MIXED ? create_impl<1>(s, bands) : create_impl<2>(s, bands);
+    if (rc != EG_OK) {
+        eg_solver_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return EG_OK;
+}
+
+int eg_solver_set_operator(eg_solver* s, const double* const bands[7]) {
+    if (!s || !bands) return EG_ERR_ARG;
+    for (int d = 0; d < 7; ++d)
+        if (!bands[d]) return EG_ERR_ARG;
+    return s->mode == EG_FP64 ? create_impl<0>(s, bands) : s->mode == EG_MIXED ? create_impl<1>(s, bands) : create_impl<2>(s, bands);
+}
+
+int eg_apply_operator(eg_solver* s, const void* x, void* y) {
+    if (!s || !x || !y) return EG_ERR_ARG;
+    s->profiling = false;
+    return s->mode == EG_FP64 ? apply_impl<0>(s, x, y) : s->mode == EG_MIXED ? apply_impl<1>(s, x, y) : apply_impl<2>(s, x, y);
+}
+
+int eg_precondition(eg_solver* s, const void* r, void* z) {
+    if (!s || !r || !z) return EG_ERR_ARG;
+    s->profiling = false;
+    return s->mode == EG_FP64 ? precond_impl<0>(s, r, z) : s->mode == EG_MIXED ? precond_impl<1>(s, r, z) : precond_impl<2>(s, r, z);
+}
+
+int eg_solve(eg_solver* s, const double* b, const double* x0, const eg_solve_params* params, double* x,
+             double* history, eg_solve_info* info) {
+    if (!s || !b || !x || !params || params->maxit < 0 || !(params->tol >= 0.0))
+        return s ? fail(s, EG_ERR_ARG, "bad solve arguments") : EG_ERR_ARG;
+    int rc = s->mode == EG_FP64 ? solve_impl<0>(s, b, x0, params, x, history, info)
+           : s->mode == EG_MIXED ? solve_impl<1>(s, b, x0, params, x, history, info)
+                                 : solve_impl<2>(s, b, x0, params, x, history, info);
+    if (rc != EG_OK && info) info->status = rc;
+    return rc;
+}
+
+void eg_solver_destroy(eg_solver* s) {
+    if (!s) return;
+    if (s->graph) cudaGraphExecDestroy(s->graph);
+    if (s->cap_st) cudaStreamDestroy(s->cap_st);
+    if (s->comm) ncclCommDestroy(s->comm);
+    for (auto& p : s->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    for (auto e : s->evpool) cudaEventDestroy(e);
+    if (s->hstate) cudaFreeHost(s->hstate);
+    delete s;
+}
+
+const char* eg_last_error(const eg_solver* s) { return s ? s->err.c_str() : ""; }
+
+const char* eg_status_str(int status) {
+    switch (status) {
+        case EG_OK: return "EG_OK";
+        case EG_ERR_ARG: return "EG_ERR_ARG";
+        case EG_ERR_SINGULAR_DIAG: return "EG_ERR_SINGULAR_DIAG";
+        case EG_ERR_DEGENERATE_RHS: return "EG_ERR_DEGENERATE_RHS";
+        case EG_ERR_BREAKDOWN: return "EG_ERR_BREAKDOWN";
+        case EG_ERR_NONFINITE: return "EG_ERR_NONFINITE";
+        case EG_ERR_CUDA: return "EG_ERR_CUDA";
+        case EG_ERR_NCCL: return "EG_ERR_NCCL";
+        case EG_ERR_WORKSPACE: return "EG_ERR_WORKSPACE";
+        default: return "EG_ERR_UNKNOWN";
+    }
+}
+
+int eg_nccl_unique_id(char out[128]) {
+    if (!out) return EG_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return EG_ERR_NCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(out, &id, 128);
+    return EG_OK;
+}
+
+int eg_num_kernels(void) { return KID_COUNT; }
+
+const char* eg_kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kKernelNames[kid] : ""; }
+
+int eg_profile_get(const eg_solver* s, int kid, double* total_ms, int64_t* launches,
+                   double* alg_bytes_per_launch) {
+    if (!s || kid < 0 || kid >= KID_COUNT) return EG_ERR_ARG;
+    if (total_ms) *total_ms = s->prof_ms[kid];
+    if (launches) *launches = s->prof_n[kid];
+    if (alg_bytes_per_launch) {
+        // algorithmic HBM bytes per point, V = vector / band bytes, X = x bytes
+        const double V = (double)s->L.vsz, X = (double)s->L.xsz, n = (double)s->L.n;
+        double per = 0;
+        switch (kid) {
+            case KID_SCALE: per = 7 * 8 + 6 * V + 8; break;            // 7 fp64 in; 6 V + diag out
+            case KID_START: per = 8 + X + 6 * V + 2 * V; break;        // bhat, x, 6 bands; r, rhat0
+            case KID_THOMAS_P: per = 5 * V + 2 * V; break;             // r,p,v,U,D; p,z
+            case KID_STENCIL_A: per = 8 * V + V; break;                // z,6 bands,rhat0; v
+            case KID_THOMAS_S: per = 4 * V + 2 * V; break;             // r,v,U,D; s,z_s
+            case KID_STENCIL_B: per = 8 * V + V; break;                // z_s,6 bands,s; t
+            case KID_UPDATE: per = X + 5 * V + X + V; break;           // x,z,z_s,s,t,rhat0; x,r
+            case KID_APPLY: per = 7 * V + V; break;
+            case KID_PRECOND: per = 3 * V + V; break;
+            case KID_CONVERT: per = 12; break;
+            default: per = 0;
+        }
+        *alg_bytes_per_launch = per * n;
+    }
+    return EG_OK;
+}
+
+int eg_profile_reset(eg_solver* s) {
+    if (!s) return EG_ERR_ARG;
+    for (int k = 0; k < KID_COUNT; ++k) { s->prof_ms[k] = 0; s->prof_n[k] = 0; }
+    return EG_OK;
+}
+
+}  // extern "C"

@@ -16,4 +16,4 @@ def pytest_configure(config):
 
 def pytest_sessionstart(session):
     # build the in-tree shared libraries once (no-op when up to date)
-    subprocess.check_call(["make", "-s", "gen/libeggen.so", "oracle/liboracle.so"], cwd=ROOT, stdout=subprocess.DEVNULL)
+    subprocess.check_call(["make", "-s", "all"], cwd=ROOT, stdout=subprocess.DEVNULL)

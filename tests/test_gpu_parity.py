@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): apply rel-L2 <= 1e-13 (fp64) / <= 1e-6 (fp32, against the
+oracle's fp64 evaluation of the same fp32 inputs); precondition <= 1e-12 / 1e-5;
+solve: iterations within +-2, true residual < tol, ||x_gpu - x_orc|| / ||x_orc|| <= 10 tol,
+fixed-iteration histories within 1e-3 (mixed / fp32) and 1e-10 (fp64) while R >= 1e-5.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+egs = pytest.importorskip("paper_1811_03852_b200")
+
+RAGGED = gen.Problem(200, 37, 13, seed=8)     # nx not a multiple of the 128-column tile, odd rows
+SMALLEST = gen.Problem(3, 1, 1, seed=9)       # degenerate: one latitude row, one level
+CASES = [gen.CONFIGS["C1"], RAGGED, gen.Problem(130, 9, 70, seed=10), SMALLEST]
+MODES = ["fp64", "mixed", "fp32"]
+
+
+def _vnp(mode):
+    return np.float64 if mode == "fp64" else np.float32
+
+
+def _make(prob, mode):
+    bands, b = gen.host(prob)
+    bd = torch.from_numpy(bands).cuda()
+    s = egs.Solver((prob.nx, prob.ny, prob.nz), bd, mode)
+    return s, bands, b
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.mark.parametrize("prob", CASES, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+@pytest.mark.parametrize("mode", MODES)
+def test_apply_parity(prob, mode):
+    s, bands, _ = _make(prob, mode)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, _ = oracle.scale(g, bands, mode)
+    x = np.random.default_rng(1).standard_normal(prob.n).astype(_vnp(mode))
+    y = s.apply(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    yo = oracle.apply(g, ahat, x.astype(np.float64))
+    assert _rel(y, yo) <= (1e-13 if mode == "fp64" else 1e-6)
+
+
+@pytest.mark.parametrize("prob", CASES, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+@pytest.mark.parametrize("mode", MODES)
+def test_precondition_parity(prob, mode):
+    s, bands, _ = _make(prob, mode)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, _ = oracle.scale(g, bands, mode)
+    r = np.random.default_rng(2).standard_normal(prob.n).astype(_vnp(mode))
+    z = s.precondition(torch.from_numpy(r).cuda()).cpu().numpy().astype(np.float64)
+    zo = oracle.thomas(g, "fp64", ahat, r.astype(np.float64))
+    assert _rel(z, zo) <= (1e-12 if mode == "fp64" else 1e-5)
+
+
+@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED, gen.Problem(130, 9, 70, seed=10)],
+                         ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("tol", [1e-3, 1e-4])
+def test_solve_parity(prob, mode, tol):
+    s, bands, b = _make(prob, mode)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, diag = oracle.scale(g, bands, mode)
+    xo, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=tol, maxit=200)
+    x, info, h = s.solve(torch.from_numpy(b).cuda(), tol=tol, maxit=200)
+    x = x.cpu().numpy()
+    assert info.converged and io.converged
+    assert abs(info.iters - io.iters) <= 2
+    assert info.true_R < tol
+    # true residual recomputed independently by the oracle in fp64 on the fp64 operator
+    a64, d64 = oracle.scale(g, bands, "fp64")
+    rt = oracle.residual64(g, a64, b / d64, x)
+    assert np.linalg.norm(rt) / np.linalg.norm(b / d64) < tol
+    assert _rel(x, xo) <= 10 * tol
+
+
+@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED], ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+@pytest.mark.parametrize("mode", MODES)
+def test_fixed_iteration_history_parity(prob, mode):
+    s, bands, b = _make(prob, mode)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, diag = oracle.scale(g, bands, mode)
+    _, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=0.0, maxit=8)
+    _, info, h = s.solve(torch.from_numpy(b).cuda(), tol=0.0, maxit=8)
+    assert info.iters == io.iters == 8 and not info.converged
+    keep = ho >= 1e-5
+    rt = 1e-10 if mode == "fp64" else 1e-3
+    assert np.all(np.abs(h[keep] - ho[keep]) <= rt * ho[keep])
+
+
+def test_c2_mixed_vs_fp64_iteration_match():
+    """BASELINE config 2: fp32 (mixed) solve vs all-fp64 solve, identical iteration counts."""
+    prob = gen.CONFIGS["C2"]
+    bands, b = gen.host(prob)
+    bd = torch.from_numpy(bands).cuda()
+    bt = torch.from_numpy(b).cuda()
+    g = (prob.nx, prob.ny, prob.nz)
+    res = {}
+    for mode in ("mixed", "fp64"):
+        s = egs.Solver(g, bd, mode)
+        x, info, h = s.solve(bt, tol=1e-4, maxit=200)
+        res[mode] = (x.cpu().numpy(), info, h)
+        ahat, diag = oracle.scale(g, bands, mode)
+        xo, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=1e-4, maxit=200)
+        assert abs(info.iters - io.iters) <= 2 and info.true_R < 1e-4
+        assert _rel(res[mode][0], xo) <= 1e-3
+    assert res["mixed"][1].iters == res["fp64"][1].iters
+    assert abs(res["mixed"][2][1] - res["fp64"][2][1]) <= 5e-7 * res["fp64"][2][1]
+
+
+def test_determinism_and_host_buffers():
+    prob = RAGGED
+    s, bands, b = _make(prob, "mixed")
+    x1, i1, h1 = s.solve(torch.from_numpy(b).cuda(), tol=1e-5, maxit=100)
+    x2, i2, h2 = s.solve(torch.from_numpy(b).cuda(), tol=1e-5, maxit=100)
+    assert torch.equal(x1, x2) and np.array_equal(h1, h2)
+    x3, i3, h3 = s.solve(b.copy(), tol=1e-5, maxit=100)            # host numpy in / out
+    assert isinstance(x3, np.ndarray) and np.array_equal(x3, x1.cpu().numpy()) and np.array_equal(h3, h1)
+    xg, ig, hg = s.solve(torch.from_numpy(b).cuda(), tol=1e-5, maxit=100, flags=egs.EG_SOLVE_NO_GRAPH)
+    assert torch.equal(xg, x1) and np.array_equal(hg, h1)            # graph replay == direct launch
+
+
+def test_warm_start_and_zero_iterations():
+    prob = gen.CONFIGS["C1"]
+    s, bands, b = _make(prob, "fp64")
+    x, info, _ = s.solve(torch.from_numpy(b).cuda(), tol=1e-10, maxit=200)
+    x2, info2, h2 = s.solve(torch.from_numpy(b).cuda(), x0=x.clone(), tol=1e-8, maxit=200)
+    assert info2.iters == 0 and info2.converged and torch.equal(x2, x)
+
+
+def test_power_of_two_scaling_bitwise():
+    prob = RAGGED
+    s, bands, b = _make(prob, "mixed")
+    x1, i1, h1 = s.solve(torch.from_numpy(b).cuda(), tol=1e-5, maxit=100)
+    x2, i2, h2 = s.solve(torch.from_numpy(4.0 * b).cuda(), tol=1e-5, maxit=100)
+    assert np.array_equal(h1, h2) and torch.equal(4.0 * x1, x2)
+
+
+def test_restart_bookkeeping_matches_oracle():
+    prob = gen.Problem(64, 48, 10, seed=3)
+    s, bands, b = _make(prob, "fp64")
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, diag = oracle.scale(g, bands, "fp64")
+    _, ho, io = oracle.solve(g, "fp64", ahat, diag, b, tol=1e-9, maxit=200, restart_every=3)
+    _, info, h = s.solve(torch.from_numpy(b).cuda(), tol=1e-9, maxit=200, restart_every=3)
+    assert info.restarts == io.restarts and info.iters == io.iters and info.converged
+
+
+def test_error_paths():
+    prob = gen.Problem(16, 8, 4, seed=4)
+    bands, b = gen.host(prob)
+    g = (prob.nx, prob.ny, prob.nz)
+    bad = bands.copy(); bad[0, 7] = 0.0
+    with pytest.raises(egs.EgError) as e:
+        egs.Solver(g, torch.from_numpy(bad).cuda(), "mixed")
+    assert e.value.status == 2
+    bad = bands.copy(); bad[5, prob.nx * (prob.nz - 1)] = -1.0      # U band on the top level
+    with pytest.raises(egs.EgError) as e:
+        egs.Solver(g, torch.from_numpy(bad).cuda(), "mixed")
+    assert e.value.status == 1
+    s = egs.Solver(g, torch.from_numpy(bands).cuda(), "mixed")
+    with pytest.raises(egs.EgError) as e:
+        s.solve(torch.zeros(prob.n, dtype=torch.float64, device="cuda"))
+    assert e.value.status == 3
+    bb = b.copy(); bb[5] = np.nan
+    _, info, _ = s.solve(torch.from_numpy(bb).cuda(), raise_on_error=False)
+    assert info.status == 5
+
+
+def test_no_horizontal_coupling_one_iteration():
+    prob = gen.Problem(130, 6, 10, seed=5, ch=(0.0, 0.0))
+    s, bands, b = _make(prob, "mixed")
+    x, info, h = s.solve(torch.from_numpy(b).cuda(), tol=1e-4, maxit=20)
+    assert info.iters == 1 and info.converged
+
+
+def test_profile_counts_kernels():
+    prob = gen.CONFIGS["C1"]
+    s, bands, b = _make(prob, "mixed")
+    s.profile_reset()
+    s.solve(torch.from_numpy(b).cuda(), tol=0.0, maxit=4, flags=egs.EG_SOLVE_PROFILE)
+    p = s.profile()
+    for k in ("thomas_p", "stencil_dot_A", "thomas_s", "stencil_dot_B", "update_xr"):
+        assert p[k][1] == 4 and p[k][0] > 0 and p[k][2] > 0
