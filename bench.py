@@ -43,28 +43,40 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line).  The sampler is
+    started before the region; only samples whose timestamps fall inside [mark_start, mark_end]
+    are summarised."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.t0 = self.t1 = None
+        self.lines = []
 
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(1.0)  # let the sampler come up before the timed region
         except Exception:
             self.p = None
         return self
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def __exit__(self, *a):
-        self.lines = []
         if self.p is not None:
+            time.sleep(0.2)
             self.p.terminate()
             try:
                 out, _ = self.p.communicate(timeout=5)
@@ -73,22 +85,30 @@ class Clocks:
                 self.p.kill()
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        import datetime
+        sm, mx, reasons, n_all = [], 0.0, set(), 0
+        for l in self.lines:
             f = [t.strip() for t in l.split(",")]
-            if len(f) < 7:
+            if len(f) < 8:
+                continue
+            n_all += 1
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if ts is not None and self.t0 is not None and not (self.t0 - 0.05 <= ts <= self.t1 + 0.05):
                 continue
             try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[3:7]):
+            for nm, v in zip(self.NAMES, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi sample in window"],
+                    "samples_total": n_all}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
 
@@ -232,7 +252,9 @@ def run_ours(args, prob, ws, rank, local):
         step(egs.EG_SOLVE_PROFILE)
     s.profile_reset()
     with Clocks(local) as clk:
+        clk.mark_start()
         ms, infos = timed(args.steps, egs.EG_SOLVE_PROFILE)
+        clk.mark_end()
     prof = s.profile()
     iters = sum(i.iters for i in infos)
     value = iters / (ms / 1000.0)

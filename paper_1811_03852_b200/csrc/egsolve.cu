@@ -84,7 +84,8 @@ struct eg_solver {
     Geo geo{};
     unsigned char* ws = nullptr;
     // carved pointers
-    void* bands[6]{};
+    void* B4 = nullptr;    // [n][4] scaled (E, W, N, S)
+    void* B2 = nullptr;    // [n][2] scaled (U, D)
     double* diag = nullptr;
     double* bhat = nullptr;
     double* x64 = nullptr;
@@ -97,7 +98,8 @@ struct eg_solver {
     double* gall = nullptr;  // [G][3] all ranks
     DevState* dstate = nullptr;
     DevState* hstate = nullptr;  // pinned host mirror
-    int wth = 128;               // Thomas CTA width
+    int wth = 128;               // Thomas CTA width (columns)
+    int cpt = 1;                 // columns per thread of the Thomas / update kernels (2 if nx even)
     size_t smem_th = 0;
     // graph of one iteration, keyed on the iterate pointer
     cudaGraphExec_t graph = nullptr;
@@ -192,8 +194,8 @@ Vecs<MODE> vecs(eg_solver* s, void* x_it) {
     using V = typename Prec<MODE>::V;
     using X = typename Prec<MODE>::X;
     Vecs<MODE> v;
-    v.E = (const V*)s->bands[0]; v.W = (const V*)s->bands[1]; v.N = (const V*)s->bands[2];
-    v.S = (const V*)s->bands[3]; v.U = (const V*)s->bands[4]; v.D = (const V*)s->bands[5];
+    v.B4 = (const V*)s->B4;
+    v.B2 = (const V*)s->B2;
     v.diag = s->diag;
     v.bhat = s->bhat;
     v.x = (X*)x_it;
@@ -260,10 +262,12 @@ int iteration(eg_solver* s, void* x_it) {
     Vecs<MODE> v = vecs<MODE>(s, x_it);
     const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+    const int tth = s->wth / s->cpt;
     int rc;
     {
         ProfScope ps(s, KID_THOMAS_P);
-        k_thomas<MODE, 1><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+        if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+        else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
         CK(cudaGetLastError());
     }
     if ((rc = halo_ghosted(s, v.z))) return rc;
@@ -275,7 +279,8 @@ int iteration(eg_solver* s, void* x_it) {
     if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
     {
         ProfScope ps(s, KID_THOMAS_S);
-        k_thomas<MODE, 2><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+        if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+        else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
         CK(cudaGetLastError());
     }
     if ((rc = halo_ghosted(s, v.zs))) return rc;
@@ -287,7 +292,8 @@ int iteration(eg_solver* s, void* x_it) {
     if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
     {
         ProfScope ps(s, KID_UPDATE);
-        k_update<MODE><<<gr, RW, 0, s->st>>>(s->geo, v);
+        if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
+        else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
         CK(cudaGetLastError());
     }
     if ((rc = finalize<MODE, W_C>(s, 0))) return rc;
@@ -308,7 +314,9 @@ int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero) {
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     {
         ProfScope ps(s, KID_START);
-        k_start<MODE><<<gr, RW, 0, s->st>>>(s->geo, v, b, entry, xzero);
+        if (entry && xzero) k_start<MODE, true, true><<<gr, RW, 0, s->st>>>(s->geo, v, b);
+        else if (entry) k_start<MODE, true, false><<<gr, RW, 0, s->st>>>(s->geo, v, b);
+        else k_start<MODE, false, false><<<gr, RW, 0, s->st>>>(s->geo, v, b);
         CK(cudaGetLastError());
     }
     return finalize<MODE, W_START>(s, entry);
@@ -470,9 +478,7 @@ int create_impl(eg_solver* s, const double* const bands[7]) {
     const dim3 grid((unsigned)((s->grid.nx + 255) / 256), (unsigned)s->grid.nz, (unsigned)s->L.nyl);
     {
         ProfScope ps(s, KID_SCALE);
-        k_scale<V><<<grid, 256, 0, s->st>>>(s->geo, in, (V*)s->bands[0], (V*)s->bands[1],
-                                            (V*)s->bands[2], (V*)s->bands[3], (V*)s->bands[4],
-                                            (V*)s->bands[5], s->diag, err);
+        k_scale<V><<<grid, 256, 0, s->st>>>(s->geo, in, (V*)s->B4, (V*)s->B2, s->diag, err);
         CK(cudaGetLastError());
     }
     int herr = 0;
@@ -508,17 +514,24 @@ int precond_impl(eg_solver* s, const void* r, void* z) {
     Vecs<MODE> v = vecs<MODE>(s, s->x64);
     const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
     ProfScope ps(s, KID_PRECOND);
-    k_thomas<MODE, 0><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, (const V*)r, (V*)z);
+    if (s->cpt == 2) k_thomas<MODE, 0, 2><<<gt, s->wth / 2, s->smem_th, s->st>>>(s->geo, v, (const V*)r, (V*)z);
+    else k_thomas<MODE, 0, 1><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, (const V*)r, (V*)z);
     CK(cudaGetLastError());
+    return EG_OK;
+}
+
+template <int MODE, int CPT>
+int set_thomas_smem_c(eg_solver* s) {
+    CK(cudaFuncSetAttribute(k_thomas<MODE, 0, CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    CK(cudaFuncSetAttribute(k_thomas<MODE, 1, CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    CK(cudaFuncSetAttribute(k_thomas<MODE, 2, CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
     return EG_OK;
 }
 
 template <int MODE>
 int set_thomas_smem(eg_solver* s) {
-    CK(cudaFuncSetAttribute(k_thomas<MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
-    CK(cudaFuncSetAttribute(k_thomas<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
-    CK(cudaFuncSetAttribute(k_thomas<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
-    return EG_OK;
+    int rc = set_thomas_smem_c<MODE, 1>(s);
+    return rc ? rc : set_thomas_smem_c<MODE, 2>(s);
 }
 
 bool valid_dist(const eg_grid* g, const eg_dist* d, int64_t* jb, int64_t* je, int* rank, int* nranks) {
@@ -580,7 +593,8 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     }
     s->ws = (unsigned char*)workspace;
     const Layout& L = s->L;
-    for (int d = 0; d < 6; ++d) s->bands[d] = s->ws + L.off_bands + (size_t)d * L.n * L.vsz;
+    s->B4 = s->ws + L.off_bands;
+    s->B2 = s->ws + L.off_bands + (size_t)4 * L.n * L.vsz;
     s->diag = (double*)(s->ws + L.off_diag);
     s->bhat = (double*)(s->ws + L.off_bhat);
     s->x64 = (double*)(s->ws + L.off_x64);
@@ -607,6 +621,7 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     s->wth = 128;
     while (s->wth > 32 && 2 * (size_t)grid->nz * s->wth * L.vsz > 77824) s->wth /= 2;
     s->smem_th = 2 * (size_t)grid->nz * s->wth * L.vsz;
+    s->cpt = (grid->nx % 2 == 0) ? 2 : 1;
     if (s->smem_th > 227 * 1024) {
         int rc = fail(s, EG_ERR_ARG, "nz=%lld too large for the shared-memory Thomas kernel", (long long)grid->nz);
         eg_solver_destroy(s);

@@ -12,9 +12,15 @@
 //   fin_C     : beta, R, history, convergence / breakdown / restart (a10)
 // plus scale (a1), start (a2 / a11: bhat, r = round(bhat - Ahat x) in fp64) and the finalisers.
 //
-// Every reducing kernel writes one partial per (latitude row, column tile) slot; the finaliser sums
-// slots in a fixed order inside 8 fixed latitude row-groups, then the groups in order, so sums are
-// bitwise reproducible run to run and for any number of GPUs.
+// Memory layout: every field is longitude-fastest, q = i + nx*(k + nz*jl); the
+// scaled bands are packed per point as B4[q] = (E, W, N, S) and B2[q] = (U, D) so one 16-byte and
+// one 8-byte load (fp32) fetch all six.  Column kernels give each thread CPT consecutive columns and
+// walk the levels k, prefetching KB levels ahead into registers (double-buffered batches) so that
+// every warp keeps many independent loads in flight while it runs the per-column recurrences.
+//
+// Every reducing kernel writes one partial per (latitude row, 128-column tile) slot; the finaliser
+// sums slots in a fixed order inside 8 fixed latitude row-groups, then the groups in order, so sums
+// are bitwise reproducible run to run and for any number of GPUs.
 #pragma once
 #include "common.cuh"
 
@@ -26,17 +32,18 @@ struct Geo {
     int64_t nyl;         // local rows
     int64_t j0;          // global index of local row 0
     int64_t n;           // nyl*row
-    int tiles;           // column tiles of width RW per row (reduction slots per row)
+    int tiles;           // 128-column tiles per row (= reduction slots per row)
     int G, g_lo, g_hi;   // reduction row-groups: all, and this rank's [g_lo, g_hi)
 };
 
-constexpr int RW = 128;  // columns per CTA of the row-tiled kernels (= threads per CTA)
+constexpr int RW = 128;  // columns per CTA of the row-tiled kernels (one reduction slot each)
 
 template <int MODE>
 struct Vecs {
     using V = typename Prec<MODE>::V;
     using X = typename Prec<MODE>::X;
-    const V *E, *W, *N, *S, *U, *D;  // scaled bands (unit diagonal not stored)
+    const V* B4;                     // [n][4] scaled (E, W, N, S); the unit diagonal is not stored
+    const V* B2;                     // [n][2] scaled (U, D)
     const double* diag;              // a_C, fp64 (scales b only)
     double* bhat;                    // D_g^-1 b, fp64
     X* x;                            // iterate
@@ -47,6 +54,15 @@ struct Vecs {
     double* slots;                   // [NQ][nyl][tiles]
     DevState* st;
 };
+
+// ---- aligned vector access ----
+template <class T, int N>
+struct alignas(sizeof(T) * N) VecN { T v[N]; };
+
+template <int N, class T>
+__device__ __forceinline__ VecN<T, N> ldv(const T* p) { return *reinterpret_cast<const VecN<T, N>*>(p); }
+template <int N, class T>
+__device__ __forceinline__ void stv(T* p, const VecN<T, N>& a) { *reinterpret_cast<VecN<T, N>*>(p) = a; }
 
 // FP32 mode keeps its global sums in binary32: emulate exactly by rounding after every add
 template <int MODE> __device__ __forceinline__ double rs(double a) {
@@ -104,91 +120,148 @@ __device__ __forceinline__ void acc_dot(double& acc, V a, V b) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// a1: scale bands (Eq. 5).  grid (ceil(nx/256), nz, nyl), block 256.
+// a1: scale bands (Eq. 5): ahat_d = round_V(a_d / a_C) (binary64 IEEE division), packed
+// into B4 / B2; diag = a_C.  Validation flags: 2 = a_C zero or non-finite, 1 = non-finite band or a
+// nonzero band at an absent neighbour.  grid (ceil(nx/256), nz, nyl), block 256.
 struct Bands7 { const double* b[7]; };
 
 template <class V>
-__global__ void __launch_bounds__(256) k_scale(Geo g, Bands7 in, V* __restrict__ E, V* __restrict__ W,
-                                               V* __restrict__ N, V* __restrict__ S,
-                                               V* __restrict__ U, V* __restrict__ D,
+__global__ void __launch_bounds__(256) k_scale(Geo g, Bands7 in, V* __restrict__ B4, V* __restrict__ B2,
                                                double* __restrict__ diag, int* __restrict__ err) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= g.nx) return;
     const int64_t k = blockIdx.y, jl = blockIdx.z, jg = g.j0 + jl;
     const int64_t q = jl * g.row + k * g.nx + i;
     const double c = in.b[0][q];
+    double a[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) a[d] = in.b[d + 1][q];
     int e = 0;
     if (c == 0.0 || !isfinite(c)) e |= 2;
-    V* out[6] = {E, W, N, S, U, D};
     const bool present[6] = {true, true, jg < g.ny - 1, jg > 0, k < g.nz - 1, k > 0};
+    VecN<V, 4> h4;
+    VecN<V, 2> h2;
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
-        const double a = in.b[d + 1][q];
-        if (!isfinite(a) || (!present[d] && a != 0.0)) e |= 1;
-        out[d][q] = (V)(a / c);  // IEEE binary64 division, then one rounding to V
+        if (!isfinite(a[d]) || (!present[d] && a[d] != 0.0)) e |= 1;
+        const V v = (V)(a[d] / c);  // IEEE binary64 division, then one rounding to V
+        if (d < 4) h4.v[d] = v;
+        else h2.v[d - 4] = v;
     }
+    stv<4>(B4 + 4 * q, h4);
+    stv<2>(B2 + 2 * q, h2);
     diag[q] = c;
     if (e) atomicOr(err, e);
 }
 
 // ---------------------------------------------------------------------------------------------
-// a2 / a11 (entry, restart, verification):  bhat = b / diag (entry only);
+// a2 / a11 (entry, restart, verification):  bhat = b / diag (ENTRY);
 //   res = bhat - Ahat x with fp64 accumulation (bands promoted);  r = rhat0 = round_V(res)
-// partials: q0 = ||bhat||^2 (entry), q1 = ||res||^2 (fp64, true residual), q2 = r . r (S)
-// grid (tiles, nyl), block RW.
-template <int MODE>
-__global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double* __restrict__ b,
-                                              int entry, int xzero) {
+// partials: q0 = ||bhat||^2 (ENTRY), q1 = ||res||^2 (fp64, true residual), q2 = r . r (S).
+// XZERO: x = 0 (written at ENTRY), res = bhat, no operator application.  grid (tiles, nyl), RW.
+template <int MODE, bool ENTRY, bool XZERO>
+__global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double* __restrict__ b) {
     using V = typename Prec<MODE>::V;
     using X = typename Prec<MODE>::X;
-    const int64_t i = (int64_t)blockIdx.x * RW + threadIdx.x;
-    const int64_t jl = blockIdx.y, jg = g.j0 + jl;
+    constexpr int KB = XZERO ? 8 : 2;
     double acc[3] = {0.0, 0.0, 0.0};
+    const int i = blockIdx.x * RW + threadIdx.x;
+    const int64_t jl = blockIdx.y, jg = g.j0 + jl;
     if (i < g.nx) {
-        const bool hasN = jg < g.ny - 1, hasS = jg > 0;
-        const int64_t iE = (i + 1 == g.nx) ? 0 : i + 1, iW = (i == 0) ? g.nx - 1 : i - 1;
+        const int nx = (int)g.nx, nz = (int)g.nz;
         const int64_t rb = jl * g.row;
-        for (int64_t k = 0; k < g.nz; ++k) {
-            const int64_t q = rb + k * g.nx + i;
-            double bh;
-            if (entry) {
-                bh = b[q] / vv.diag[q];
-                vv.bhat[q] = bh;
-                if (MODE == 2) {
-                    const double b32 = (double)(float)bh;
-                    acc[0] = rs<MODE>(acc[0] + (double)(float)(b32 * b32));
-                } else {
-                    acc[0] += bh * bh;
+        const int iE = (i + 1 == nx) ? 0 : i + 1, iW = (i == 0) ? nx - 1 : i - 1;
+        const X* __restrict__ xc = vv.x + rb + i;
+        const X* __restrict__ xE = vv.x + rb + iE;
+        const X* __restrict__ xW = vv.x + rb + iW;
+        // N/S neighbour rows: local, ghost (multi-GPU), or the centre row at a pole (zero band)
+        const X* __restrict__ xN = (jg == g.ny - 1) ? xc : (jl + 1 < g.nyl ? xc + g.row : vv.xg_hi + i);
+        const X* __restrict__ xS = (jg == 0) ? xc : (jl > 0 ? xc - g.row : vv.xg_lo + i);
+        const V* __restrict__ b4 = vv.B4 + 4 * (rb + i);
+        const V* __restrict__ b2 = vv.B2 + 2 * (rb + i);
+        const double* __restrict__ bp = (ENTRY ? b : vv.bhat) + rb + i;
+        const double* __restrict__ dp = vv.diag + rb + i;
+        double* __restrict__ bh_out = vv.bhat + rb + i;
+        X* __restrict__ xo = vv.x + rb + i;
+        V* __restrict__ ro = vv.r + rb + i;
+        V* __restrict__ rho = vv.rh + rb + i;
+        constexpr int NA = XZERO ? 2 : 13;
+        double cur[KB][NA], nxt[KB][NA];
+#pragma unroll
+        for (int e = 0; e < KB; ++e)
+#pragma unroll
+            for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a] = 0.0;
+        double xup_c = 0, xup_n = 0;
+        auto load = [&](int k0, double(&c)[KB][NA], double& xup) {
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {
+                const int k = k0 + e;
+                if (k < nz) {
+                    const int o = k * nx;
+                    c[e][0] = bp[o];
+                    c[e][1] = ENTRY ? dp[o] : 1.0;
+                    if (!XZERO) {
+                        const VecN<V, 4> h4 = ldv<4>(b4 + 4 * o);
+                        const VecN<V, 2> h2 = ldv<2>(b2 + 2 * o);
+                        c[e][2] = (double)h4.v[0]; c[e][3] = (double)h4.v[1];
+                        c[e][4] = (double)h4.v[2]; c[e][5] = (double)h4.v[3];
+                        c[e][6] = (double)h2.v[0]; c[e][7] = (double)h2.v[1];
+                        c[e][8] = (double)xc[o]; c[e][9] = (double)xE[o]; c[e][10] = (double)xW[o];
+                        c[e][11] = (double)xN[o]; c[e][12] = (double)xS[o];
+                    }
                 }
-            } else {
-                bh = vv.bhat[q];
             }
-            double res;
-            if (xzero) {
-                res = bh;
-                if (entry) vv.x[q] = (X)0;
-            } else {
-                const int64_t lk = k * g.nx;
-                double ax = (double)vv.x[q];
-                ax += (double)vv.E[q] * (double)vv.x[rb + lk + iE];
-                ax += (double)vv.W[q] * (double)vv.x[rb + lk + iW];
-                if (hasN) {
-                    const double xn = (jl + 1 < g.nyl) ? (double)vv.x[q + g.row] : (double)vv.xg_hi[lk + i];
-                    ax += (double)vv.N[q] * xn;
+            if (!XZERO) xup = (k0 + KB < nz) ? (double)xc[(k0 + KB) * nx] : 0.0;
+        };
+        load(0, cur, xup_c);
+        double xprev = 0.0;
+        for (int k0 = 0; k0 < nz; k0 += KB) {
+            if (k0 + KB < nz) load(k0 + KB, nxt, xup_n);
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {
+                const int k = k0 + e;
+                if (k < nz) {
+                    const int o = k * nx;
+                    double bh = cur[e][0];
+                    if (ENTRY) {
+                        bh = bh / cur[e][1];
+                        bh_out[o] = bh;
+                        if (MODE == 2) {
+                            const double b32 = (double)(float)bh;
+                            acc[0] = rs<MODE>(acc[0] + (double)(float)(b32 * b32));
+                        } else {
+                            acc[0] += bh * bh;
+                        }
+                    }
+                    double res;
+                    if (XZERO) {
+                        res = bh;
+                        if (ENTRY) xo[o] = (X)0;
+                    } else {
+                        const double xm = e == 0 ? xprev : cur[e - 1][8];
+                        const double xp = e + 1 < KB ? (k + 1 < nz ? cur[e + 1][8] : 0.0) : xup_c;
+                        double ax = cur[e][8];
+                        ax += cur[e][2] * cur[e][9];
+                        ax += cur[e][3] * cur[e][10];
+                        ax += cur[e][4] * cur[e][11];
+                        ax += cur[e][5] * cur[e][12];
+                        ax += cur[e][6] * xp;
+                        ax += cur[e][7] * xm;
+                        res = bh - ax;
+                    }
+                    const V rv = (V)res;
+                    ro[o] = rv;
+                    rho[o] = rv;
+                    acc[1] += res * res;
+                    acc_dot<MODE>(acc[2], rv, rv);
                 }
-                if (hasS) {
-                    const double xs = (jl > 0) ? (double)vv.x[q - g.row] : (double)vv.xg_lo[lk + i];
-                    ax += (double)vv.S[q] * xs;
-                }
-                if (k + 1 < g.nz) ax += (double)vv.U[q] * (double)vv.x[q + g.nx];
-                if (k > 0) ax += (double)vv.D[q] * (double)vv.x[q - g.nx];
-                res = bh - ax;
             }
-            const V rv = (V)res;
-            vv.r[q] = rv;
-            vv.rh[q] = rv;
-            acc[1] += res * res;
-            acc_dot<MODE>(acc[2], rv, rv);
+            if (!XZERO) xprev = cur[KB - 1][8];
+#pragma unroll
+            for (int e = 0; e < KB; ++e)
+#pragma unroll
+                for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a];
+            xup_c = xup_n;
         }
     }
     write_slots<3>(g, vv.slots, acc, MODE == 2 ? 0x5u : 0x0u);
@@ -197,18 +270,24 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
 // ---------------------------------------------------------------------------------------------
 // a3 / a6 / precondition: per-column Thomas solve fused with the vector update that
 // produces its right-hand side.  KIND 0: f = fin;  1: p = r + beta (p - omega v), f = p;
-// 2: s = r - alpha v, f = s.  The forward-elimination factors c'_k and y_k live in shared memory
-// laid out [k][thread] (conflict-free).  grid (ceil(nx/blockDim), nyl), dynamic smem 2*nz*blockDim*V.
-template <int MODE, int KIND>
+// 2: s = r - alpha v, f = s.  Each thread owns CPT consecutive columns (independent recurrences,
+// vector loads); the forward-elimination factors c'_k, y_k live in shared memory laid out
+// [k][column] (conflict-free).  grid (ceil(nx/W), nyl), W = blockDim*CPT columns,
+// dynamic smem 2*nz*W*sizeof(V).
+//   c'_0 = U_0, y_0 = f_0;  k >= 1: m = 1 - D_k c'_{k-1}, c'_k = U_k / m, y_k = (f_k - D_k y_{k-1}) / m
+//   z_{nz-1} = y_{nz-1};    z_k = y_k - c'_k z_{k+1}
+template <int MODE, int KIND, int CPT>
 __global__ void __launch_bounds__(128) k_thomas(Geo g, Vecs<MODE> vv,
                                                 const typename Prec<MODE>::V* __restrict__ fin,
                                                 typename Prec<MODE>::V* __restrict__ zout) {
     using V = typename Prec<MODE>::V;
-    // levels loaded per batch; the next batch is in flight while the current one is eliminated
-    // (one DRAM round trip per level otherwise makes the recurrence latency bound)
-    constexpr int KB = sizeof(V) == 4 ? 8 : 4;
+    // levels per batch; the next batch is in flight while the current one is eliminated.  Occupancy
+    // is bounded by the shared-memory factors (3 CTAs / SM), not registers, so batches are deep.
+    constexpr int KB = (sizeof(V) == 4 ? 16 : 8) / CPT;
+    using VC = VecN<V, CPT>;
+    using VU = VecN<V, 2 * CPT>;
     extern __shared__ __align__(16) unsigned char smraw[];
-    const int W = blockDim.x, tid = threadIdx.x;
+    const int W = blockDim.x * CPT, tid = threadIdx.x;
     V* cps = reinterpret_cast<V*>(smraw);
     V* ys = cps + g.nz * W;
     V beta = 0, omega = 0, alpha = 0;
@@ -224,84 +303,97 @@ __global__ void __launch_bounds__(128) k_thomas(Geo g, Vecs<MODE> vv,
             alpha = (V)st->alpha_v;
         }
     }
-    const int64_t i = (int64_t)blockIdx.x * W + tid;
+    const int i = blockIdx.x * W + tid * CPT;
     if (i >= g.nx) return;
     const int64_t base = (int64_t)blockIdx.y * g.row + i;
-    const int64_t nx = g.nx;
+    const int nx = (int)g.nx;
     const int nz = (int)g.nz;
-    const V* __restrict__ A0 = KIND == 0 ? fin : vv.r;
-    const V* __restrict__ Pp = vv.p;
-    const V* __restrict__ Vv = vv.v;
-    const V* __restrict__ Uu = vv.U;
-    const V* __restrict__ Dd = vv.D;
-    V ca[KB], cp[KB], cv[KB], cu[KB], cd[KB];
-    V na[KB], np[KB], nv[KB], nu[KB], nd[KB];
+    const V* __restrict__ A0 = (KIND == 0 ? fin : vv.r) + base;
+    const V* __restrict__ Pp = vv.p + base;
+    const V* __restrict__ Vv = vv.v + base;
+    const V* __restrict__ UD = vv.B2 + 2 * base;
+    V* __restrict__ Pw = (KIND == 1 ? vv.p : vv.s) + base;
+    V* __restrict__ Zw = zout + base;
+    const int sc = tid * CPT;  // this thread's first column in the shared-memory rows
+    VC ca[KB], cp[KB], cv[KB], na[KB], np[KB], nv[KB];
+    VU cu[KB], nu[KB];
 #pragma unroll
-    for (int e = 0; e < KB; ++e) { ca[e] = cp[e] = cv[e] = cu[e] = cd[e] = (V)0; na[e] = np[e] = nv[e] = nu[e] = nd[e] = (V)0; }
-    auto load = [&](int k0, V(&a)[KB], V(&p)[KB], V(&v)[KB], V(&u)[KB], V(&d)[KB]) {
+    for (int e = 0; e < KB; ++e)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            ca[e].v[c] = cp[e].v[c] = cv[e].v[c] = na[e].v[c] = np[e].v[c] = nv[e].v[c] = (V)0;
+            cu[e].v[2 * c] = cu[e].v[2 * c + 1] = nu[e].v[2 * c] = nu[e].v[2 * c + 1] = (V)0;
+        }
+    auto load = [&](int k0, VC(&a)[KB], VC(&p)[KB], VC(&v)[KB], VU(&u)[KB]) {
 #pragma unroll
         for (int e = 0; e < KB; ++e) {
             const int k = k0 + e;
             if (k < nz) {
-                const int64_t q = base + (int64_t)k * nx;
-                a[e] = A0[q];
-                if (KIND == 1 && !fresh) { p[e] = Pp[q]; v[e] = Vv[q]; }
-                if (KIND == 2) v[e] = Vv[q];
-                u[e] = Uu[q];
-                d[e] = Dd[q];
+                const int o = k * nx;
+                a[e] = ldv<CPT>(A0 + o);
+                if (KIND == 1 && !fresh) { p[e] = ldv<CPT>(Pp + o); v[e] = ldv<CPT>(Vv + o); }
+                if (KIND == 2) v[e] = ldv<CPT>(Vv + o);
+                u[e] = ldv<2 * CPT>(UD + 2 * o);
             }
         }
     };
-    load(0, ca, cp, cv, cu, cd);
-    V cp_prev = 0, y_prev = 0;
+    load(0, ca, cp, cv, cu);
+    V cprev[CPT], yprev[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) cprev[c] = yprev[c] = (V)0;
     for (int k0 = 0; k0 < nz; k0 += KB) {
-        if (k0 + KB < nz) load(k0 + KB, na, np, nv, nu, nd);
+        if (k0 + KB < nz) load(k0 + KB, na, np, nv, nu);
 #pragma unroll
         for (int e = 0; e < KB; ++e) {
             const int k = k0 + e;
             if (k < nz) {
-                const int64_t q = base + (int64_t)k * nx;
-                V f;
-                if (KIND == 0) {
-                    f = ca[e];
-                } else if (KIND == 1) {
-                    f = fresh ? ca[e] : fma(beta, fma(-omega, cv[e], cp[e]), ca[e]);
-                    vv.p[q] = f;
-                } else {
-                    f = fma(-alpha, cv[e], ca[e]);
-                    vv.s[q] = f;
+                VC f, cc, yy;
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    if (KIND == 0) f.v[c] = ca[e].v[c];
+                    else if (KIND == 1) f.v[c] = fresh ? ca[e].v[c] : fma(beta, fma(-omega, cv[e].v[c], cp[e].v[c]), ca[e].v[c]);
+                    else f.v[c] = fma(-alpha, cv[e].v[c], ca[e].v[c]);
+                    const V u = cu[e].v[2 * c], d = cu[e].v[2 * c + 1];
+                    if (k == 0) {
+                        cc.v[c] = u;
+                        yy.v[c] = f.v[c];
+                    } else {
+                        const V inv = rcp_fast<V>(fma(-d, cprev[c], (V)1));
+                        cc.v[c] = u * inv;
+                        yy.v[c] = fma(-d, yprev[c], f.v[c]) * inv;
+                    }
+                    cprev[c] = cc.v[c];
+                    yprev[c] = yy.v[c];
                 }
-                V c, y;
-                if (k == 0) {
-                    c = cu[e];
-                    y = f;
-                } else {
-                    const V inv = rcp<V>(fma(-cd[e], cp_prev, (V)1));
-                    c = cu[e] * inv;
-                    y = fma(-cd[e], y_prev, f) * inv;
-                }
-                cps[k * W + tid] = c;
-                ys[k * W + tid] = y;
-                cp_prev = c;
-                y_prev = y;
+                if (KIND != 0) stv<CPT>(Pw + k * nx, f);
+                stv<CPT>(cps + k * W + sc, cc);
+                stv<CPT>(ys + k * W + sc, yy);
             }
         }
 #pragma unroll
-        for (int e = 0; e < KB; ++e) { ca[e] = na[e]; cp[e] = np[e]; cv[e] = nv[e]; cu[e] = nu[e]; cd[e] = nd[e]; }
+        for (int e = 0; e < KB; ++e) { ca[e] = na[e]; cp[e] = np[e]; cv[e] = nv[e]; cu[e] = nu[e]; }
     }
-    V zn = y_prev;
-    zout[base + (int64_t)(nz - 1) * nx] = zn;
+    VC zn;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) zn.v[c] = yprev[c];
+    stv<CPT>(Zw + (nz - 1) * nx, zn);
 #pragma unroll 4
     for (int k = nz - 2; k >= 0; --k) {
-        zn = fma(-cps[k * W + tid], zn, ys[k * W + tid]);
-        zout[base + (int64_t)k * nx] = zn;
+        const VC cc = ldv<CPT>(cps + k * W + sc), yy = ldv<CPT>(ys + k * W + sc);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) zn.v[c] = fma(-cc.v[c], zn.v[c], yy.v[c]);
+        stv<CPT>(Zw + k * nx, zn);
     }
 }
 
 // ---------------------------------------------------------------------------------------------
-// a4 / a7 / apply: y = Ahat z (unit diagonal + 6 bands; periodic i; absent neighbours skipped)
+// a4 / a7 / apply: y = Ahat z (unit diagonal + 6 bands; periodic i; absent neighbours contribute 0)
 // DOTS 0: none;  1: sigma = aux . y (aux = rhat0);  2: t.s, t.t, s.s (aux = s).
-// Thread per column walking k; z(k-1), z(k), z(k+1) carried in registers.  grid (tiles, nyl).
+// Thread per column walking k.  Loads of KB levels (B4, B2, z centre / E / W / N / S, aux) are
+// issued as one batch into registers while the previous batch is combined (double-buffered
+// register prefetch).  Absent N/S neighbours at the poles read the centre row instead (a valid
+// address) and are multiplied by their zero band (validated at create); the top / bottom U / D
+// bands are zero the same way.  grid (tiles, nyl), block RW.
 template <int MODE, int DOTS>
 __global__ void __launch_bounds__(RW) k_stencil(Geo g, Vecs<MODE> vv,
                                                 const typename Prec<MODE>::V* __restrict__ z,
@@ -310,41 +402,83 @@ __global__ void __launch_bounds__(RW) k_stencil(Geo g, Vecs<MODE> vv,
     using V = typename Prec<MODE>::V;
     if (DOTS != 0 && vv.st->halt != H_RUN) return;
     constexpr int NQ = DOTS == 2 ? 3 : 1;
+    constexpr int KB = sizeof(V) == 4 ? 4 : 2;
+    constexpr int NA = DOTS ? 12 : 11;
     double acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-    const int64_t i = (int64_t)blockIdx.x * RW + threadIdx.x;
+    const int i = blockIdx.x * RW + threadIdx.x;
     const int64_t jl = blockIdx.y, jg = g.j0 + jl;
     if (i < g.nx) {
-        const bool hasN = jg < g.ny - 1, hasS = jg > 0;
-        const int64_t nx = g.nx, row = g.row;
-        const int nz = (int)g.nz;
-        const int64_t iE = (i + 1 == nx) ? 0 : i + 1, iW = (i == 0) ? nx - 1 : i - 1;
-        const int64_t rb = jl * row;
-        V zm = 0, z0 = z[rb + i];
-#pragma unroll 2
-        for (int k = 0; k < nz; ++k) {
-            const int64_t lk = rb + (int64_t)k * nx;
-            const int64_t q = lk + i;
-            const V zp = (k + 1 < nz) ? z[q + nx] : (V)0;
-            V a = z0;
-            a = fma(vv.E[q], z[lk + iE], a);
-            a = fma(vv.W[q], z[lk + iW], a);
-            if (hasN) a = fma(vv.N[q], z[q + row], a);
-            if (hasS) a = fma(vv.S[q], z[q - row], a);
-            if (k + 1 < nz) a = fma(vv.U[q], zp, a);
-            if (k > 0) a = fma(vv.D[q], zm, a);
-            y[q] = a;
-            if (DOTS == 1) {
-                acc_dot<MODE>(acc[0], aux[q], a);
-            } else if (DOTS == 2) {
-                const V sv = aux[q];
-                acc_dot<MODE>(acc[0], a, sv);
-                acc_dot<MODE>(acc[1], a, a);
-                acc_dot<MODE>(acc[2], sv, sv);
+        const int nx = (int)g.nx, nz = (int)g.nz;
+        const int64_t rb = jl * g.row;
+        const int iE = (i + 1 == nx) ? 0 : i + 1, iW = (i == 0) ? nx - 1 : i - 1;
+        const V* __restrict__ zc = z + rb + i;
+        const V* __restrict__ zE = z + rb + iE;
+        const V* __restrict__ zW = z + rb + iW;
+        const V* __restrict__ zN = (jg < g.ny - 1) ? zc + g.row : zc;
+        const V* __restrict__ zS = (jg > 0) ? zc - g.row : zc;
+        const V* __restrict__ b4 = vv.B4 + 4 * (rb + i);
+        const V* __restrict__ b2 = vv.B2 + 2 * (rb + i);
+        const V* __restrict__ ax = DOTS ? aux + rb + i : zc;
+        V* __restrict__ yo = y + rb + i;
+        V cur[KB][NA], nxt[KB][NA];
+#pragma unroll
+        for (int e = 0; e < KB; ++e)
+#pragma unroll
+            for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a] = (V)0;
+        V zup_c = 0, zup_n = 0;
+        auto load = [&](int k0, V(&b)[KB][NA], V& zup) {
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {
+                const int k = k0 + e;
+                if (k < nz) {
+                    const int o = k * nx;
+                    const VecN<V, 4> h4 = ldv<4>(b4 + 4 * o);
+                    const VecN<V, 2> h2 = ldv<2>(b2 + 2 * o);
+                    b[e][0] = h4.v[0]; b[e][1] = h4.v[1]; b[e][2] = h4.v[2];
+                    b[e][3] = h4.v[3]; b[e][4] = h2.v[0]; b[e][5] = h2.v[1];
+                    b[e][6] = zc[o]; b[e][7] = zE[o]; b[e][8] = zW[o];
+                    b[e][9] = zN[o]; b[e][10] = zS[o];
+                    if (DOTS) b[e][NA - 1] = ax[o];
+                }
             }
-            zm = z0;
-            z0 = zp;
+            zup = (k0 + KB < nz) ? zc[(k0 + KB) * nx] : (V)0;
+        };
+        load(0, cur, zup_c);
+        V zprev = 0;
+        for (int k0 = 0; k0 < nz; k0 += KB) {
+            if (k0 + KB < nz) load(k0 + KB, nxt, zup_n);
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {
+                const int k = k0 + e;
+                if (k < nz) {
+                    const V zm = e == 0 ? zprev : cur[e - 1][6];
+                    const V zp = e + 1 < KB ? (k + 1 < nz ? cur[e + 1][6] : (V)0) : zup_c;
+                    V a = cur[e][6];
+                    a = fma(cur[e][0], cur[e][7], a);
+                    a = fma(cur[e][1], cur[e][8], a);
+                    a = fma(cur[e][2], cur[e][9], a);
+                    a = fma(cur[e][3], cur[e][10], a);
+                    a = fma(cur[e][4], zp, a);
+                    a = fma(cur[e][5], zm, a);
+                    yo[k * nx] = a;
+                    if (DOTS == 1) {
+                        acc_dot<MODE>(acc[0], cur[e][NA - 1], a);
+                    } else if (DOTS == 2) {
+                        const V sv = cur[e][NA - 1];
+                        acc_dot<MODE>(acc[0], a, sv);
+                        acc_dot<MODE>(acc[1], a, a);
+                        acc_dot<MODE>(acc[2], sv, sv);
+                    }
+                }
+            }
+            zprev = cur[KB - 1][6];
+#pragma unroll
+            for (int e = 0; e < KB; ++e)
+#pragma unroll
+                for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a];
+            zup_c = zup_n;
         }
     }
     if (DOTS != 0) write_slots<NQ>(g, vv.slots, acc, MODE == 2 ? 0x7u : 0x0u);
@@ -352,35 +486,89 @@ __global__ void __launch_bounds__(RW) k_stencil(Geo g, Vecs<MODE> vv,
 
 // ---------------------------------------------------------------------------------------------
 // a9: x += alpha z + omega z_s (X precision, scalars unrounded, A-10); r = s - omega t;
-// partials rhat0 . r, r . r.  On an s-step exit only x += alpha z.  grid (tiles, nyl).
-template <int MODE>
+// partials rhat0 . r, r . r.  On an s-step exit only x += alpha z.  CPT columns per thread,
+// double-buffered register batches of KB levels.  grid (tiles, nyl), block RW / CPT.
+template <int MODE, int CPT>
 __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
     using V = typename Prec<MODE>::V;
     using X = typename Prec<MODE>::X;
+    constexpr int KB = (sizeof(V) == 4 ? 8 : 4) / CPT > 0 ? (sizeof(V) == 4 ? 8 : 4) / CPT : 1;
+    using VC = VecN<V, CPT>;
+    using XC = VecN<X, CPT>;
     const DevState* st = vv.st;
     if (st->halt != H_RUN) return;
     const bool sexit = st->sexit != 0;
     const X alpha = (X)st->alpha, omega = (X)st->omega;
     const V omega_v = (V)st->omega_v;
     double acc[2] = {0.0, 0.0};
-    const int64_t i = (int64_t)blockIdx.x * RW + threadIdx.x;
+    const int i = blockIdx.x * RW + threadIdx.x * CPT;
     if (i < g.nx) {
+        const int nx = (int)g.nx, nz = (int)g.nz;
         const int64_t base = (int64_t)blockIdx.y * g.row + i;
-        const int nz = (int)g.nz;
+        X* __restrict__ xp = vv.x + base;
+        const V* __restrict__ zp = vv.z + base;
+        const V* __restrict__ zsp = vv.zs + base;
+        const V* __restrict__ sp = vv.s + base;
+        const V* __restrict__ tp = vv.t + base;
+        const V* __restrict__ rhp = vv.rh + base;
+        V* __restrict__ rp = vv.r + base;
         if (sexit) {
             for (int k = 0; k < nz; ++k) {
-                const int64_t q = base + (int64_t)k * g.nx;
-                vv.x[q] = fma(alpha, (X)vv.z[q], vv.x[q]);
+                XC xv = ldv<CPT>(xp + k * nx);
+                const VC zv = ldv<CPT>(zp + k * nx);
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) xv.v[c] = fma(alpha, (X)zv.v[c], xv.v[c]);
+                stv<CPT>(xp + k * nx, xv);
             }
         } else {
-#pragma unroll 4
-            for (int k = 0; k < nz; ++k) {
-                const int64_t q = base + (int64_t)k * g.nx;
-                vv.x[q] = fma(omega, (X)vv.zs[q], fma(alpha, (X)vv.z[q], vv.x[q]));
-                const V rq = fma(-omega_v, vv.t[q], vv.s[q]);
-                vv.r[q] = rq;
-                acc_dot<MODE>(acc[0], vv.rh[q], rq);
-                acc_dot<MODE>(acc[1], rq, rq);
+            XC cx[KB], nxv[KB];
+            VC cz[KB], czs[KB], cs[KB], ct[KB], crh[KB];
+            VC nz_[KB], nzs[KB], ns[KB], nt[KB], nrh[KB];
+#pragma unroll
+            for (int e = 0; e < KB; ++e)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    cx[e].v[c] = nxv[e].v[c] = (X)0;
+                    cz[e].v[c] = czs[e].v[c] = cs[e].v[c] = ct[e].v[c] = crh[e].v[c] = (V)0;
+                    nz_[e].v[c] = nzs[e].v[c] = ns[e].v[c] = nt[e].v[c] = nrh[e].v[c] = (V)0;
+                }
+            auto load = [&](int k0, XC(&x_)[KB], VC(&z_)[KB], VC(&zs_)[KB], VC(&s_)[KB], VC(&t_)[KB],
+                            VC(&rh_)[KB]) {
+#pragma unroll
+                for (int e = 0; e < KB; ++e) {
+                    const int k = k0 + e;
+                    if (k < nz) {
+                        const int o = k * nx;
+                        x_[e] = ldv<CPT>(xp + o); z_[e] = ldv<CPT>(zp + o); zs_[e] = ldv<CPT>(zsp + o);
+                        s_[e] = ldv<CPT>(sp + o); t_[e] = ldv<CPT>(tp + o); rh_[e] = ldv<CPT>(rhp + o);
+                    }
+                }
+            };
+            load(0, cx, cz, czs, cs, ct, crh);
+            for (int k0 = 0; k0 < nz; k0 += KB) {
+                if (k0 + KB < nz) load(k0 + KB, nxv, nz_, nzs, ns, nt, nrh);
+#pragma unroll
+                for (int e = 0; e < KB; ++e) {
+                    const int k = k0 + e;
+                    if (k < nz) {
+                        const int o = k * nx;
+                        XC xv;
+                        VC rv;
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) {
+                            xv.v[c] = fma(omega, (X)czs[e].v[c], fma(alpha, (X)cz[e].v[c], cx[e].v[c]));
+                            rv.v[c] = fma(-omega_v, ct[e].v[c], cs[e].v[c]);
+                            acc_dot<MODE>(acc[0], crh[e].v[c], rv.v[c]);
+                            acc_dot<MODE>(acc[1], rv.v[c], rv.v[c]);
+                        }
+                        stv<CPT>(xp + o, xv);
+                        stv<CPT>(rp + o, rv);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < KB; ++e) {
+                    cx[e] = nxv[e]; cz[e] = nz_[e]; czs[e] = nzs[e]; cs[e] = ns[e]; ct[e] = nt[e]; crh[e] = nrh[e];
+                }
             }
         }
     }

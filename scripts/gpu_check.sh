@@ -6,7 +6,7 @@ tail -25 gpurun_out/pytest_gpu.log
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo smoke rc $?; tail -3 gpurun_out/smoke.log
 timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc $?
 tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
-if [ "${NCU:-1}" = "1" ]; then
+if [ "${NCU:-0}" = "1" ]; then
   timeout 300 python scripts/profile_step.py > gpurun_out/prof_plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file gpurun_out/launches.csv python scripts/profile_step.py > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc $?
