@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libegsolve.so")
+_SO = os.environ.get("EGSOLVE_LIB") or os.path.join(_HERE, "libegsolve.so")  # override: A/B builds
 
 EG_FP64, EG_MIXED, EG_FP32 = 0, 1, 2
 PRECISIONS = {"fp64": EG_FP64, "mixed": EG_MIXED, "fp32": EG_FP32}

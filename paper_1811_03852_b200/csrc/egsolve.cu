@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -101,6 +102,8 @@ struct eg_solver {
     int wth = 128;               // Thomas CTA width (columns)
     int cpt = 1;                 // columns per thread of the Thomas / update kernels (2 if nx even)
     size_t smem_th = 0;
+    bool use_tm = false;         // fp32 Thomas with TMEM-resident factors (nz <= 128)
+    size_t smem_tm = 0;
     // graph of one iteration, keyed on the iterate pointer
     cudaGraphExec_t graph = nullptr;
     void* graph_x = nullptr;
@@ -264,10 +267,17 @@ int iteration(eg_solver* s, void* x_it) {
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     const int tth = s->wth / s->cpt;
     int rc;
+    const dim3 gtm((unsigned)((s->grid.nx + 127) / 128), (unsigned)s->L.nyl);
     {
         ProfScope ps(s, KID_THOMAS_P);
-        if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
-        else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+        if constexpr (MODE != 0) {
+            if (s->use_tm) k_thomas_tm<MODE, 1><<<gtm, 128, s->smem_tm, s->st>>>(s->geo, v, nullptr, v.z);
+            else if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+            else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+        } else {
+            if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+            else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+        }
         CK(cudaGetLastError());
     }
     if ((rc = halo_ghosted(s, v.z))) return rc;
@@ -279,8 +289,14 @@ int iteration(eg_solver* s, void* x_it) {
     if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
     {
         ProfScope ps(s, KID_THOMAS_S);
-        if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
-        else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+        if constexpr (MODE != 0) {
+            if (s->use_tm) k_thomas_tm<MODE, 2><<<gtm, 128, s->smem_tm, s->st>>>(s->geo, v, nullptr, v.zs);
+            else if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+            else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+        } else {
+            if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+            else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+        }
         CK(cudaGetLastError());
     }
     if ((rc = halo_ghosted(s, v.zs))) return rc;
@@ -514,6 +530,14 @@ int precond_impl(eg_solver* s, const void* r, void* z) {
     Vecs<MODE> v = vecs<MODE>(s, s->x64);
     const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
     ProfScope ps(s, KID_PRECOND);
+    if constexpr (MODE != 0) {
+        if (s->use_tm) {
+            const dim3 gtm((unsigned)((s->grid.nx + 127) / 128), (unsigned)s->L.nyl);
+            k_thomas_tm<MODE, 0><<<gtm, 128, s->smem_tm, s->st>>>(s->geo, v, (const V*)r, (V*)z);
+            CK(cudaGetLastError());
+            return EG_OK;
+        }
+    }
     if (s->cpt == 2) k_thomas<MODE, 0, 2><<<gt, s->wth / 2, s->smem_th, s->st>>>(s->geo, v, (const V*)r, (V*)z);
     else k_thomas<MODE, 0, 1><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, (const V*)r, (V*)z);
     CK(cudaGetLastError());
@@ -531,7 +555,15 @@ int set_thomas_smem_c(eg_solver* s) {
 template <int MODE>
 int set_thomas_smem(eg_solver* s) {
     int rc = set_thomas_smem_c<MODE, 1>(s);
-    return rc ? rc : set_thomas_smem_c<MODE, 2>(s);
+    if (!rc) rc = set_thomas_smem_c<MODE, 2>(s);
+    if constexpr (MODE != 0) {
+        if (!rc && s->use_tm) {
+            CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
+            CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
+            CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
+        }
+    }
+    return rc;
 }
 
 bool valid_dist(const eg_grid* g, const eg_dist* d, int64_t* jb, int64_t* je, int* rank, int* nranks) {
@@ -622,6 +654,12 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     while (s->wth > 32 && 2 * (size_t)grid->nz * s->wth * L.vsz > 77824) s->wth /= 2;
     s->smem_th = 2 * (size_t)grid->nz * s->wth * L.vsz;
     s->cpt = (grid->nx % 2 == 0) ? 2 : 1;
+    // TMEM-factor Thomas (fp32 working precision, nz <= 128); EG_NO_TMEM=1 selects the shared-memory one
+    {
+        const char* no_tm = getenv("EG_NO_TMEM");
+        s->use_tm = prec != EG_FP64 && grid->nz <= 128 && !(no_tm && no_tm[0] == '1');
+        s->smem_tm = std::max<size_t>(TM_SMEM, (size_t)grid->nz * 128 * sizeof(float));
+    }
     if (s->smem_th > 227 * 1024) {
         int rc = fail(s, EG_ERR_ARG, "nz=%lld too large for the shared-memory Thomas kernel", (long long)grid->nz);
         eg_solver_destroy(s);

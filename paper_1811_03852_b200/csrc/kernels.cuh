@@ -64,6 +64,11 @@ __device__ __forceinline__ VecN<T, N> ldv(const T* p) { return *reinterpret_cast
 template <int N, class T>
 __device__ __forceinline__ void stv(T* p, const VecN<T, N>& a) { *reinterpret_cast<VecN<T, N>*>(p) = a; }
 
+// L2 prefetch of a future level (no register cost): the register batches then see L2 latency
+__device__ __forceinline__ void pf_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // FP32 mode keeps its global sums in binary32: emulate exactly by rounding after every add
 template <int MODE> __device__ __forceinline__ double rs(double a) {
     return MODE == 2 ? (double)(float)a : a;
@@ -387,6 +392,182 @@ __global__ void __launch_bounds__(128) k_thomas(Geo g, Vecs<MODE> vv,
 }
 
 // ---------------------------------------------------------------------------------------------
+// Same Thomas solve (fp32 working precision), with the elimination factors c'_k kept in TENSOR
+// MEMORY instead of shared memory.  TMEM (256 KB / SM) is otherwise idle in this memory-bound
+// solver: each thread owns one TMEM lane (warp w -> lanes 32w..32w+31) and stores / reloads its
+// column's c'_k eight levels at a time (tcgen05.st / tcgen05.ld .32x32b.x8); y_k stays in shared
+// memory ([k][column], conflict-free).  Per 128-column CTA: 128 TMEM columns + nz*512 B of shared
+// memory, so 4 CTAs (16 warps) fit on an SM instead of 3 (12 warps at 2 columns / thread with
+// both factors in shared memory, i.e. 6 warps): twice the loads in flight.  Dynamic shared memory
+// is padded to 50 KB (+1 KB reserved per CTA) so that at most 4 CTAs (= 4 x 128 = all 512 TMEM columns) are ever resident
+// on an SM and tcgen05.alloc never waits.  Requires nz <= 128.  grid (ceil(nx/128), nyl), 128 thr.
+constexpr int TM_SMEM = 50 * 1024;
+// L2 prefetch distances in levels (0 = off) of the Thomas, stencil and update kernels
+#ifndef TM_PF
+#define TM_PF 16
+#endif
+#ifndef ST_PF
+#define ST_PF 0
+#endif
+#ifndef UP_PF
+#define UP_PF 0
+#endif
+
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const float (&c)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+        "r"(__float_as_uint(c[0])), "r"(__float_as_uint(c[1])), "r"(__float_as_uint(c[2])),
+        "r"(__float_as_uint(c[3])), "r"(__float_as_uint(c[4])), "r"(__float_as_uint(c[5])),
+        "r"(__float_as_uint(c[6])), "r"(__float_as_uint(c[7]))
+        : "memory");
+}
+
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, float (&c)[8]) {
+    uint32_t r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int e = 0; e < 8; ++e) c[e] = __uint_as_float(r[e]);
+}
+
+template <int MODE, int KIND>
+__global__ void __launch_bounds__(128, 4) k_thomas_tm(Geo g, Vecs<MODE> vv, const float* __restrict__ fin,
+                                                      float* __restrict__ zout) {
+    using V = float;
+    static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
+    constexpr int KB = 8;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ uint32_t tm_base;
+    V* ys = reinterpret_cast<V*>(smraw);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    V beta = 0, omega = 0, alpha = 0;
+    bool fresh = false;
+    if (KIND != 0) {
+        const DevState* st = vv.st;
+        if (st->halt != H_RUN) return;  // uniform: before any collective
+        if (KIND == 1) {
+            fresh = st->fresh != 0;
+            beta = (V)st->beta_v;
+            omega = (V)st->omega_v;
+        } else {
+            alpha = (V)st->alpha_v;
+        }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tm_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t taddr = tm_base + ((uint32_t)(warp * 32) << 16);
+
+    const int nx = (int)g.nx, nz = (int)g.nz;
+    const int i_raw = blockIdx.x * 128 + tid;
+    const bool act = i_raw < nx;
+    const int i = act ? i_raw : nx - 1;  // inactive lanes read a valid column, never store
+    const int64_t base = (int64_t)blockIdx.y * g.row + i;
+    const V* __restrict__ A0 = (KIND == 0 ? fin : vv.r) + base;
+    // p = v = 0 after a (re)start: read r in their place with beta = 0, so the update is exactly
+    // f = r + 0*(r - omega r) = r without a data-dependent branch
+    const V* __restrict__ Pp = (KIND == 1 && fresh ? vv.r : vv.p) + base;
+    const V* __restrict__ Vv = (KIND == 1 && fresh ? vv.r : vv.v) + base;
+    if (KIND == 1 && fresh) beta = 0.f;
+    const V* __restrict__ UD = vv.B2 + 2 * base;
+    V* __restrict__ Pw = (KIND == 1 ? vv.p : vv.s) + base;
+    V* __restrict__ Zw = zout + base;
+    V ca[KB], cp[KB], cv[KB], na[KB], np[KB], nv[KB];
+    VecN<V, 2> cu[KB], nu[KB];
+#pragma unroll
+    for (int e = 0; e < KB; ++e) {
+        ca[e] = cp[e] = cv[e] = na[e] = np[e] = nv[e] = 0.f;
+        cu[e].v[0] = cu[e].v[1] = nu[e].v[0] = nu[e].v[1] = 0.f;
+    }
+    auto load = [&](int k0, V(&a)[KB], V(&p)[KB], V(&v)[KB], VecN<V, 2>(&u)[KB]) {
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const int o = min(k0 + e, nz - 1) * nx;  // tail levels re-read the last one (L1 hit)
+            a[e] = A0[o];
+            if (KIND == 1) { p[e] = Pp[o]; v[e] = Vv[o]; }
+            if (KIND == 2) v[e] = Vv[o];
+            u[e] = ldv<2>(UD + 2 * o);
+            if (TM_PF > 0 && k0 + e + TM_PF < nz) {  // warp-uniform condition
+                const int of = (k0 + e + TM_PF) * nx;
+                if ((tid & 7) == 0) {  // one prefetch per 32-byte sector of each array
+                    pf_l2(A0 + of);
+                    if (KIND == 1) { pf_l2(Pp + of); pf_l2(Vv + of); }
+                    if (KIND == 2) pf_l2(Vv + of);
+                    pf_l2(UD + 2 * of);
+                    pf_l2(UD + 2 * of + 8);
+                }
+            }
+        }
+    };
+    load(0, ca, cp, cv, cu);
+    V cprev = 0.f, yprev = 0.f;
+    for (int k0 = 0; k0 < nz; k0 += KB) {
+        if (k0 + KB < nz) load(k0 + KB, na, np, nv, nu);
+        float cb[KB];
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const int k = k0 + e;
+            cb[e] = 0.f;
+            if (k < nz) {
+                V f;
+                if (KIND == 0) f = ca[e];
+                else if (KIND == 1) f = fmaf(beta, fmaf(-omega, cv[e], cp[e]), ca[e]);
+                else f = fmaf(-alpha, cv[e], ca[e]);
+                if (KIND != 0 && act) Pw[k * nx] = f;
+                const V u = cu[e].v[0], d = cu[e].v[1];
+                V c, y;
+                if (k == 0) {
+                    c = u;
+                    y = f;
+                } else {
+                    const V inv = rcp_fast<V>(fmaf(-d, cprev, 1.f));
+                    c = u * inv;
+                    y = fmaf(-d, yprev, f) * inv;
+                }
+                cb[e] = c;
+                ys[k * 128 + tid] = y;
+                cprev = c;
+                yprev = y;
+            }
+        }
+        tm_st8(taddr + (uint32_t)k0, cb);
+#pragma unroll
+        for (int e = 0; e < KB; ++e) { ca[e] = na[e]; cp[e] = np[e]; cv[e] = nv[e]; cu[e] = nu[e]; }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    V zn = yprev;
+    if (act) Zw[(nz - 1) * nx] = zn;
+    for (int k0 = ((nz - 1) / KB) * KB; k0 >= 0; k0 -= KB) {
+        float cb[KB];
+        tm_ld8(taddr + (uint32_t)k0, cb);
+#pragma unroll
+        for (int e = KB - 1; e >= 0; --e) {
+            const int k = k0 + e;
+            if (k <= nz - 2) {
+                zn = fmaf(-cb[e], zn, ys[k * 128 + tid]);
+                if (act) Zw[k * nx] = zn;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tm_base) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // a4 / a7 / apply: y = Ahat z (unit diagonal + 6 bands; periodic i; absent neighbours contribute 0)
 // DOTS 0: none;  1: sigma = aux . y (aux = rhat0);  2: t.s, t.t, s.s (aux = s).
 // Thread per column walking k.  Loads of KB levels (B4, B2, z centre / E / W / N / S, aux) are
@@ -395,7 +576,7 @@ __global__ void __launch_bounds__(128) k_thomas(Geo g, Vecs<MODE> vv,
 // address) and are multiplied by their zero band (validated at create); the top / bottom U / D
 // bands are zero the same way.  grid (tiles, nyl), block RW.
 template <int MODE, int DOTS>
-__global__ void __launch_bounds__(RW) k_stencil(Geo g, Vecs<MODE> vv,
+__global__ void __launch_bounds__(RW, 4) k_stencil(Geo g, Vecs<MODE> vv,
                                                 const typename Prec<MODE>::V* __restrict__ z,
                                                 typename Prec<MODE>::V* __restrict__ y,
                                                 const typename Prec<MODE>::V* __restrict__ aux) {
@@ -431,19 +612,26 @@ __global__ void __launch_bounds__(RW) k_stencil(Geo g, Vecs<MODE> vv,
         auto load = [&](int k0, V(&b)[KB][NA], V& zup) {
 #pragma unroll
             for (int e = 0; e < KB; ++e) {
-                const int k = k0 + e;
-                if (k < nz) {
-                    const int o = k * nx;
-                    const VecN<V, 4> h4 = ldv<4>(b4 + 4 * o);
-                    const VecN<V, 2> h2 = ldv<2>(b2 + 2 * o);
-                    b[e][0] = h4.v[0]; b[e][1] = h4.v[1]; b[e][2] = h4.v[2];
-                    b[e][3] = h4.v[3]; b[e][4] = h2.v[0]; b[e][5] = h2.v[1];
-                    b[e][6] = zc[o]; b[e][7] = zE[o]; b[e][8] = zW[o];
-                    b[e][9] = zN[o]; b[e][10] = zS[o];
-                    if (DOTS) b[e][NA - 1] = ax[o];
+                const int o = min(k0 + e, nz - 1) * nx;  // tail levels re-read the last one
+                const VecN<V, 4> h4 = ldv<4>(b4 + 4 * o);
+                const VecN<V, 2> h2 = ldv<2>(b2 + 2 * o);
+                b[e][0] = h4.v[0]; b[e][1] = h4.v[1]; b[e][2] = h4.v[2];
+                b[e][3] = h4.v[3]; b[e][4] = h2.v[0]; b[e][5] = h2.v[1];
+                b[e][6] = zc[o]; b[e][7] = zE[o]; b[e][8] = zW[o];
+                b[e][9] = zN[o]; b[e][10] = zS[o];
+                if (DOTS) b[e][NA - 1] = ax[o];
+                if (ST_PF > 0 && k0 + e + ST_PF < nz) {  // warp-uniform
+                    const int of = (k0 + e + ST_PF) * nx;
+                    const int l = threadIdx.x & 31;
+                    if ((l & 7) == 0) {  // one per 32-byte sector: z, aux, B2
+                        pf_l2(zc + of);
+                        if (DOTS) pf_l2(ax + of);
+                        pf_l2(b2 + 2 * of);
+                    }
+                    if ((l & 1) == 0) pf_l2(b4 + 4 * of);  // B4: 16 B per point
                 }
             }
-            zup = (k0 + KB < nz) ? zc[(k0 + KB) * nx] : (V)0;
+            zup = zc[min(k0 + KB, nz - 1) * nx];  // multiplied by U = 0 on the top level
         };
         load(0, cur, zup_c);
         V zprev = 0;
@@ -454,7 +642,7 @@ __global__ void __launch_bounds__(RW) k_stencil(Geo g, Vecs<MODE> vv,
                 const int k = k0 + e;
                 if (k < nz) {
                     const V zm = e == 0 ? zprev : cur[e - 1][6];
-                    const V zp = e + 1 < KB ? (k + 1 < nz ? cur[e + 1][6] : (V)0) : zup_c;
+                    const V zp = e + 1 < KB ? cur[e + 1][6] : zup_c;  // U = 0 at k = nz-1
                     V a = cur[e][6];
                     a = fma(cur[e][0], cur[e][7], a);
                     a = fma(cur[e][1], cur[e][8], a);
@@ -536,11 +724,16 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
                             VC(&rh_)[KB]) {
 #pragma unroll
                 for (int e = 0; e < KB; ++e) {
-                    const int k = k0 + e;
-                    if (k < nz) {
-                        const int o = k * nx;
-                        x_[e] = ldv<CPT>(xp + o); z_[e] = ldv<CPT>(zp + o); zs_[e] = ldv<CPT>(zsp + o);
-                        s_[e] = ldv<CPT>(sp + o); t_[e] = ldv<CPT>(tp + o); rh_[e] = ldv<CPT>(rhp + o);
+                    const int o = min(k0 + e, nz - 1) * nx;  // tail levels re-read the last one
+                    x_[e] = ldv<CPT>(xp + o); z_[e] = ldv<CPT>(zp + o); zs_[e] = ldv<CPT>(zsp + o);
+                    s_[e] = ldv<CPT>(sp + o); t_[e] = ldv<CPT>(tp + o); rh_[e] = ldv<CPT>(rhp + o);
+                    if (UP_PF > 0 && k0 + e + UP_PF < nz) {  // warp-uniform
+                        const int of = (k0 + e + UP_PF) * nx;
+                        const int l = threadIdx.x & 31;
+                        if ((l * CPT * (int)sizeof(V)) % 32 == 0) {
+                            pf_l2(zp + of); pf_l2(zsp + of); pf_l2(sp + of); pf_l2(tp + of); pf_l2(rhp + of);
+                        }
+                        if ((l * CPT * (int)sizeof(X)) % 32 == 0) pf_l2(xp + of);
                     }
                 }
             };
