@@ -338,6 +338,25 @@ int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero) {
     return finalize<MODE, W_START>(s, entry);
 }
 
+// true residual of the current x only, r / rhat0 untouched (A-6 verification, final true_R)
+template <int MODE>
+int verify(eg_solver* s, void* x_it) {
+    using X = typename Prec<MODE>::X;
+    Vecs<MODE> v = vecs<MODE>(s, x_it);
+    int rc;
+    if (s->nranks > 1) {
+        X* x = (X*)x_it;
+        if ((rc = halo(s, x, s->xg, (unsigned char*)s->xg + s->L.row * 8, sizeof(X)))) return rc;
+    }
+    const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+    {
+        ProfScope ps(s, KID_START);
+        k_start<MODE, false, false, false><<<gr, RW, 0, s->st>>>(s->geo, v, nullptr);
+        CK(cudaGetLastError());
+    }
+    return finalize<MODE, W_VERIFY>(s, 0);
+}
+
 int read_state(eg_solver* s) {
     CK(cudaMemcpyAsync(s->hstate, s->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
@@ -451,14 +470,22 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
             if (bd_at == h->iter) { rc = EG_ERR_BREAKDOWN; break; }
             bd_at = h->iter;
         }
-        // H_CONVERGED -> verify; H_RESTART / breakdown -> restart; H_MAXIT -> final true residual.
-        // All four recompute r = round(bhat - Ahat x) with fp64 accumulation (A-6, A-11).
+        // H_CONVERGED -> verify the true residual (A-6); H_MAXIT -> final true residual only;
+        // H_RESTART / breakdown / failed verification -> restart: r = round(bhat - Ahat x) with fp64
+        // accumulation (A-11), which re-checks R_true < tol itself.
+        if (halt == H_CONVERGED || halt == H_MAXIT) {
+            if ((rc = verify<MODE>(s, x_it))) return rc;
+            if ((rc = read_state(s))) return rc;
+            if (h->halt == H_NONFINITE) { rc = EG_ERR_NONFINITE; break; }
+            if (halt == H_MAXIT) break;
+            if (h->halt == H_START_CONVERGED) { inf.converged = 1; break; }
+            if (h->iter >= h->maxit) break;
+        }
+        inf.restarts++;  // counted before the restart re-checks R_true (as the oracle does)
         if ((rc = start<MODE>(s, x_it, bdev, 0, 0))) return rc;
         if ((rc = read_state(s))) return rc;
-        if (halt == H_MAXIT) break;
         if (h->halt == H_START_CONVERGED) { inf.converged = 1; break; }
         if (h->halt == H_START_MAXIT) break;
-        inf.restarts++;
     }
 
     // ---- output x (fp64) ----

@@ -163,8 +163,9 @@ __global__ void __launch_bounds__(256) k_scale(Geo g, Bands7 in, V* __restrict__
 // a2 / a11 (entry, restart, verification):  bhat = b / diag (ENTRY);
 //   res = bhat - Ahat x with fp64 accumulation (bands promoted);  r = rhat0 = round_V(res)
 // partials: q0 = ||bhat||^2 (ENTRY), q1 = ||res||^2 (fp64, true residual), q2 = r . r (S).
-// XZERO: x = 0 (written at ENTRY), res = bhat, no operator application.  grid (tiles, nyl), RW.
-template <int MODE, bool ENTRY, bool XZERO>
+// XZERO: x = 0 (written at ENTRY), res = bhat, no operator application.  WRITE = false: verification
+// only (true residual norm, r / rhat0 untouched).  grid (tiles, nyl), RW.
+template <int MODE, bool ENTRY, bool XZERO, bool WRITE = true>
 __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double* __restrict__ b) {
     using V = typename Prec<MODE>::V;
     using X = typename Prec<MODE>::X;
@@ -254,11 +255,13 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
                         ax += cur[e][7] * xm;
                         res = bh - ax;
                     }
-                    const V rv = (V)res;
-                    ro[o] = rv;
-                    rho[o] = rv;
                     acc[1] += res * res;
-                    acc_dot<MODE>(acc[2], rv, rv);
+                    if (WRITE) {
+                        const V rv = (V)res;
+                        ro[o] = rv;
+                        rho[o] = rv;
+                        acc_dot<MODE>(acc[2], rv, rv);
+                    }
                 }
             }
             if (!XZERO) xprev = cur[KB - 1][8];
@@ -769,10 +772,10 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Finalisers.  fin_groups: warp w sums quantity (w % NQ) of local group (w / NQ): lanes take fixed
-// contiguous chunks of the group's (row, tile) slots, then a fixed shuffle tree.
+// Finalisers.  fin_groups: warp w sums quantity (w % NQ) of local group (w / NQ): lane l sums the
+// group's (row, tile) slots l, l+32, l+64, ... in four fixed chains, then a fixed shuffle tree.
 // fin_logic (thread 0): groups in order -> totals -> BiCGStab scalars and control flags.
-enum Which { W_START = 0, W_A = 1, W_B = 2, W_C = 3 };
+enum Which { W_START = 0, W_A = 1, W_B = 2, W_C = 3, W_VERIFY = 4 };
 
 template <int NQ>
 __device__ __forceinline__ void fin_groups(const Geo& g, const double* __restrict__ slots, uint32_t r32,
@@ -785,12 +788,27 @@ __device__ __forceinline__ void fin_groups(const Geo& g, const double* __restric
     const int64_t L = (re - rb) * g.tiles;
     const double* src = slots + (int64_t)qq * g.nyl * g.tiles + rb * g.tiles;
     const bool f = (r32 >> qq) & 1u;
-    const int64_t c = (L + 31) / 32, e0 = lane * c, e1 = min(L, e0 + c);
-    double s = 0.0;
-    for (int64_t e = e0; e < e1; ++e) {
-        s += src[e];
-        if (f) s = (double)(float)s;
+    // lane l sums slots l + 32 m for m = 0, 1, 2, ... into four chains (m mod 4), combined in
+    // fixed order: coalesced, latency-tolerant, and the same tree for any launch / rank count
+    double a4[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t e = lane;
+    for (; e + 96 < L; e += 128) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            a4[c] += src[e + 32 * c];
+            if (f) a4[c] = (double)(float)a4[c];
+        }
     }
+    for (int c = 0; e < L; e += 32, ++c) {
+        a4[c] += src[e];
+        if (f) a4[c] = (double)(float)a4[c];
+    }
+    double s = (a4[0] + a4[1]);
+    if (f) s = (double)(float)s;
+    double s2 = (a4[2] + a4[3]);
+    if (f) s2 = (double)(float)s2;
+    s += s2;
+    if (f) s = (double)(float)s;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         s += __shfl_down_sync(0xffffffffu, s, o);
@@ -803,7 +821,7 @@ template <int MODE, int WHICH>
 __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict__ gall, DevState* st,
                                           int first) {
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
-    const uint32_t r32 = MODE == 2 ? (WHICH == W_START ? 0x5u : 0x7u) : 0x0u;
+    const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
     using V = typename Prec<MODE>::V;
     double tot[NQ];
 #pragma unroll
@@ -815,6 +833,12 @@ __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict
             if (f) t = (double)(float)t;
         }
         tot[q] = t;
+    }
+    if (WHICH == W_VERIFY) {  // true residual of the current x only (A-6)
+        const double rt = sqrt(tot[1]) / st->nb;
+        st->true_R = rt;
+        st->halt = !isfinite(rt) ? H_NONFINITE : (rt < st->tol ? H_START_CONVERGED : H_VERIFY_FAILED);
+        return;
     }
     if (WHICH == W_START) {
         if (first) {
@@ -890,8 +914,8 @@ template <int MODE, int WHICH>
 __global__ void __launch_bounds__(1024) k_fin(Geo g, const double* __restrict__ slots, DevState* st,
                                               double* __restrict__ gsum, int first) {
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
-    const uint32_t r32 = MODE == 2 ? (WHICH == W_START ? 0x5u : 0x7u) : 0x0u;
-    if (WHICH != W_START && st->halt != H_RUN) return;
+    const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
+    if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;
     if (WHICH == W_C && st->sexit) {  // s-step exit: no sums needed
         if (threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gsum, st, first);
         return;
@@ -906,8 +930,8 @@ template <int MODE, int WHICH>
 __global__ void __launch_bounds__(1024) k_fin_groups(Geo g, const double* __restrict__ slots,
                                                      const DevState* st, double* __restrict__ gsum) {
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
-    const uint32_t r32 = MODE == 2 ? (WHICH == W_START ? 0x5u : 0x7u) : 0x0u;
-    if (WHICH != W_START && st->halt != H_RUN) return;
+    const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
+    if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;
     if (WHICH == W_C && st->sexit) return;
     fin_groups<NQ>(g, slots, r32, gsum);
 }
