@@ -243,7 +243,7 @@ int halo_ghosted(eg_solver* s, void* zrow0) {
 template <int MODE, int WHICH>
 int finalize(eg_solver* s, int first) {
     ProfScope ps(s, KID_FIN);
-    if (s->nranks == 1) {
+    if (s->comm == nullptr) {  // one GPU: group sums and logic in one CTA
         k_fin<MODE, WHICH><<<1, 1024, 0, s->st>>>(s->geo, s->slots, s->dstate, s->gsum, first);
         CK(cudaGetLastError());
         return EG_OK;
@@ -693,15 +693,19 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         return rc;
     }
     int rc = prec == EG_FP64 ? set_thomas_smem<0>(s) : prec == EG_MIXED ? set_thomas_smem<1>(s) : set_thomas_smem<2>(s);
-    if (rc == EG_OK && s->nranks > 1) {
-        if (!dist->nccl_unique_id) {
-            rc = EG_ERR_ARG;
-        } else {
-            ncclUniqueId id;
-            memcpy(&id, dist->nccl_unique_id, sizeof id);
-            ncclResult_t r = ncclCommInitRank(&s->comm, s->nranks, id, s->rank);
-            if (r != ncclSuccess) rc = fail(s, EG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
-        }
+    // EG_FORCE_NCCL=1 runs a single GPU through the multi-rank path (1-rank communicator: local
+    // group sums -> ncclAllGather -> logic kernel, all inside the captured graph) so that path is
+    // exercised by the single-GPU parity tests.
+    const char* force = getenv("EG_FORCE_NCCL");
+    const bool force_nccl = s->nranks == 1 && force && force[0] == '1';
+    if (rc == EG_OK && (s->nranks > 1 || force_nccl)) {
+        ncclUniqueId id;
+        ncclResult_t r = ncclSuccess;
+        if (force_nccl) r = ncclGetUniqueId(&id);
+        else if (!dist->nccl_unique_id) rc = EG_ERR_ARG;
+        else memcpy(&id, dist->nccl_unique_id, sizeof id);
+        if (rc == EG_OK && r == ncclSuccess) r = ncclCommInitRank(&s->comm, s->nranks, id, s->rank);
+        if (r != ncclSuccess) rc = fail(s, EG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
     }
     if (rc == EG_OK)
         rc = prec == EG_FP64 ? create_impl<0>(s, bands) : prec == EG_MIXED ? create_impl<1>(s, bands) : create_impl<2>(s, bands);

@@ -191,3 +191,24 @@ def test_profile_counts_kernels():
     p = s.profile()
     for k in ("thomas_p", "stencil_dot_A", "thomas_s", "stencil_dot_B", "update_xr"):
         assert p[k][1] == 4 and p[k][0] > 0 and p[k][2] > 0
+
+
+@pytest.mark.parametrize("mode", ["mixed", "fp64"])
+def test_multirank_finaliser_path_bitwise_equal(mode, monkeypatch):
+    """EG_FORCE_NCCL=1 runs one GPU through the multi-rank path (local row-group sums ->
+    ncclAllGather -> logic kernel, captured in the iteration graph).  The fixed grouping makes it
+    bitwise identical to the single-GPU finaliser."""
+    prob = RAGGED
+    bands, b = gen.host(prob)
+    g = (prob.nx, prob.ny, prob.nz)
+    bd = torch.from_numpy(bands).cuda()
+    s1 = egs.Solver(g, bd, mode)
+    x1, i1, h1 = s1.solve(torch.from_numpy(b).cuda(), tol=1e-6, maxit=100)
+    monkeypatch.setenv("EG_FORCE_NCCL", "1")
+    s2 = egs.Solver(g, bd, mode)
+    monkeypatch.delenv("EG_FORCE_NCCL")
+    x2, i2, h2 = s2.solve(torch.from_numpy(b).cuda(), tol=1e-6, maxit=100)
+    assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
+    y1 = s1.apply(torch.ones(prob.n, dtype=s1.vdtype, device="cuda"))
+    y2 = s2.apply(torch.ones(prob.n, dtype=s2.vdtype, device="cuda"))
+    assert torch.equal(y1, y2)
