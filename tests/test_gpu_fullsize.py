@@ -1,0 +1,88 @@
+"""Parity at BASELINE.json's full operational size (C5: 2560 x 1920 x 70, 344 M unknowns), in the
+launch configuration bench.py times (the default solver, CUDA-graph replay, generator on device).
+
+* apply / precondition: sampled latitude rows (poles, seam rows, interior) against the oracle run
+  on a 3-row sub-grid around each sampled row (the sub-grid's artificial edges are decoupled; rows
+  outside the sample are never compared).
+* solve (MIXED, tol 1e-4): the full CPU oracle solve of the same inputs (about 70 GB of host RAM
+  and a minute on the GPU box's cores) — iterations within 2, ||dx||/||x|| <= 10 tol, and the GPU's
+  x has oracle-recomputed true residual < tol.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+torch = pytest.importorskip("torch")
+egs = pytest.importorskip("paper_1811_03852_b200")
+
+C5 = gen.CONFIGS["C5"]
+ROWS = [0, 1, 959, 960, 1918, 1919]
+
+
+@pytest.fixture(scope="module")
+def c5():
+    prob = C5
+    bands = torch.empty((7, prob.n), dtype=torch.float64, device="cuda")
+    b = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    gen.device(prob, bands, b)
+    s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, "mixed")
+    yield prob, bands, b, s
+    s.close()
+
+
+def _subgrid_oracle(prob, j, mode):
+    """scaled bands of rows [j0, j1) around j with the artificial edges decoupled"""
+    j0, j1 = max(0, j - 1), min(prob.ny, j + 2)
+    row = prob.nx * prob.nz
+    bands, _ = gen.host(prob, j0, j1)
+    if j0 > 0:
+        bands[4, :row] = 0.0     # S band of the first sub-grid row
+    if j1 < prob.ny:
+        bands[3, -row:] = 0.0    # N band of the last sub-grid row
+    ahat, _ = oracle.scale((prob.nx, j1 - j0, prob.nz), bands, mode)
+    return j0, j1, ahat
+
+
+def test_c5_apply_and_precondition_sampled_rows(c5):
+    prob, bands, b, s = c5
+    row = prob.nx * prob.nz
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(prob.n, generator=g, device="cuda", dtype=torch.float32)
+    y = s.apply(x)
+    z = s.precondition(x)
+    torch.cuda.synchronize()
+    for j in ROWS:
+        j0, j1, ahat = _subgrid_oracle(prob, j, "mixed")
+        xs = x[j0 * row:j1 * row].double().cpu().numpy()
+        yo = oracle.apply((prob.nx, j1 - j0, prob.nz), ahat, xs)[(j - j0) * row:(j - j0 + 1) * row]
+        yg = y[j * row:(j + 1) * row].double().cpu().numpy()
+        assert np.linalg.norm(yg - yo) <= 1e-6 * np.linalg.norm(yo), j
+        zo = oracle.thomas((prob.nx, j1 - j0, prob.nz), "fp64", ahat, xs)[(j - j0) * row:(j - j0 + 1) * row]
+        zg = z[j * row:(j + 1) * row].double().cpu().numpy()
+        assert np.linalg.norm(zg - zo) <= 1e-5 * np.linalg.norm(zo), j
+
+
+def test_c5_solve_matches_full_oracle(c5):
+    prob, bands, b, s = c5
+    x, info, hist = s.solve(b, tol=1e-4, maxit=200)
+    assert info.converged and info.true_R < 1e-4
+    xg = x.cpu().numpy()
+    del x
+    hb, hrhs = gen.host(prob)
+    assert np.array_equal(hrhs, b.cpu().numpy())           # the device generator's bits
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, diag = oracle.scale(g, hb, "mixed")
+    del hb
+    xo, ho, io = oracle.solve(g, "mixed", ahat, diag, hrhs, tol=1e-4, maxit=200)
+    assert io.converged and abs(info.iters - io.iters) <= 2
+    assert np.linalg.norm(xg - xo) <= 10 * 1e-4 * np.linalg.norm(xo)
+    # the GPU's x against the oracle's fp64 residual on the fp32-rounded operator it iterated with
+    bhat = hrhs / diag
+    r = oracle.residual64(g, ahat, bhat, xg)
+    assert np.linalg.norm(r) / np.linalg.norm(bhat) < 1e-4
+    n = min(len(hist), len(ho))
+    assert np.allclose(hist[:n], ho[:n], rtol=1e-3)
