@@ -17,6 +17,7 @@
 
 #include "egsolve.h"
 #include "kernels.cuh"
+#include "phase.cuh"
 
 using namespace eg;
 
@@ -24,16 +25,16 @@ namespace {
 
 enum KernelId {
     KID_SCALE = 0, KID_START, KID_FIN, KID_THOMAS_P, KID_STENCIL_A, KID_THOMAS_S, KID_STENCIL_B,
-    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_COUNT
+    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"scale", "start", "finalize", "thomas_p", "stencil_dot_A",
                                        "thomas_s", "stencil_dot_B", "update_xr", "apply",
-                                       "precondition", "convert"};
+                                       "precondition", "convert", "phase_A", "phase_B"};
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-    size_t off_bands, off_diag, off_bhat, off_x64, off_x32, off_xg, off_vec, off_z, off_slots,
+    size_t off_bands, off_diag, off_bhat, off_x64, off_x32, off_xg, off_vec, off_z, off_pv, off_slots,
         off_gsum, off_state, total;
     size_t vsz;      // sizeof(V)
     size_t xsz;      // sizeof(X)
@@ -63,6 +64,8 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L) {
     L->off_xg = o;    o = align_up(o + 2 * row * 8, A);
     L->off_vec = o;   o = align_up(o + 6 * align_up(n * L->vsz, A), A);
     L->off_z = o;     o = align_up(o + 2 * align_up((n + 2 * row) * L->vsz, A), A);
+    L->off_pv = o;    o = align_up(o + (size_t)nyl * L->tiles * sizeof(int), A);  // wavefront ready flags
+    // reduction slots per row: 128-column tiles (unfused kernels) or 64-longitude strips (phases)
     L->off_slots = o; o = align_up(o + 3 * (size_t)nyl * L->tiles * 8, A);
     L->off_gsum = o;  o = align_up(o + 2 * 8 * 3 * 8, A);
     L->off_state = o; o = align_up(o + sizeof(DevState), A);
@@ -94,6 +97,10 @@ struct eg_solver {
     double* xg = nullptr;  // [2][row] ghost rows of x (X-typed)
     void* vec[6]{};        // r, rh, p, v, s, t
     void* zext[2]{};       // ghosted z, zs (row -1 .. nyl)
+    int* wave_flags = nullptr;  // [nyl][tiles] ready flags of the wavefront phase kernels
+    bool use_wave = false;      // fused wavefront phases (fp32 working precision, one GPU)
+    int wave_ctas = 0;
+    int epoch_base = 1;         // first epoch of the next solve (flags are never reset)
     double* slots = nullptr;
     double* gsum = nullptr;  // [G][3] local
     double* gall = nullptr;  // [G][3] all ranks
@@ -241,27 +248,59 @@ int halo_ghosted(eg_solver* s, void* zrow0) {
 }
 
 template <int MODE, int WHICH>
-int finalize(eg_solver* s, int first) {
+int finalize(eg_solver* s, int first, int tiles = 0) {
     ProfScope ps(s, KID_FIN);
+    Geo geo = s->geo;
+    if (tiles > 0) geo.tiles = tiles;  // slots per row of the producing kernel
     if (s->comm == nullptr) {  // one GPU: group sums and logic in one CTA
-        k_fin<MODE, WHICH><<<1, 1024, 0, s->st>>>(s->geo, s->slots, s->dstate, s->gsum, first);
+        k_fin<MODE, WHICH><<<1, 1024, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum, first);
         CK(cudaGetLastError());
         return EG_OK;
     }
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
-    k_fin_groups<MODE, WHICH><<<1, 1024, 0, s->st>>>(s->geo, s->slots, s->dstate, s->gsum);
+    k_fin_groups<MODE, WHICH><<<1, 1024, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum);
     CK(cudaGetLastError());
     const int gl = s->geo.g_hi - s->geo.g_lo;
     NK(ncclAllGather(s->gsum, s->gall, (size_t)gl * NQ, ncclDouble, s->comm, s->st));
-    k_fin_logic<MODE, WHICH><<<1, 32, 0, s->st>>>(s->geo, s->gall, s->dstate, first);
+    k_fin_logic<MODE, WHICH><<<1, 32, 0, s->st>>>(geo, s->gall, s->dstate, first);
     CK(cudaGetLastError());
     return EG_OK;
 }
 
 // -------- the iteration (rows a3-a10) --------
 template <int MODE>
+int iteration_fused(eg_solver* s, void* x_it) {
+    Vecs<MODE> v = vecs<MODE>(s, x_it);
+    int rc;
+    if constexpr (MODE != 0) {
+        {
+            ProfScope ps(s, KID_PHASE_A);
+            k_wave<MODE, 1><<<s->wave_ctas, WAVE_THREADS, s->smem_tm, s->st>>>(s->geo, v, s->wave_flags);
+            CK(cudaGetLastError());
+        }
+        if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
+        {
+            ProfScope ps(s, KID_PHASE_B);
+            k_wave<MODE, 2><<<s->wave_ctas, WAVE_THREADS, s->smem_tm, s->st>>>(s->geo, v, s->wave_flags);
+            CK(cudaGetLastError());
+        }
+        if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
+        const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+        {
+            ProfScope ps(s, KID_UPDATE);
+            if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
+            else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
+            CK(cudaGetLastError());
+        }
+        if ((rc = finalize<MODE, W_C>(s, 0))) return rc;
+    }
+    return EG_OK;
+}
+
+template <int MODE>
 int iteration(eg_solver* s, void* x_it) {
     using V = typename Prec<MODE>::V;
+    if (s->use_wave) return iteration_fused<MODE>(s, x_it);
     Vecs<MODE> v = vecs<MODE>(s, x_it);
     const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
@@ -416,6 +455,14 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     h->restart_every = prm->restart_every;
     h->eps_v = MODE == 0 ? 0x1.0p-53 : 0x1.0p-24;
     h->omega = h->omega_v = 1.0;
+    // wavefront flags are stamped with epochs that only ever grow: reserve this solve's range
+    // (at most ~5 finalisers per iteration) and wrap around with a flag reset well before overflow
+    if (s->epoch_base > (1 << 30)) {
+        CK(cudaMemsetAsync(s->wave_flags, 0, (size_t)s->L.nyl * s->L.tiles * sizeof(int), s->st));
+        s->epoch_base = 1;
+    }
+    h->epoch = s->epoch_base;
+    s->epoch_base += 8 * (prm->maxit + 4);
     CK(cudaMemcpyAsync(s->dstate, h, sizeof(DevState), cudaMemcpyHostToDevice, s->st));
 
     if ((rc = start<MODE>(s, x_it, bdev, 1, x0 == nullptr))) return rc;
@@ -459,6 +506,8 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
                 else if ((rc = iteration<MODE>(s, x_it))) return rc;
             }
             if ((rc = read_state(s))) return rc;
+            if (h->iter < copied || h->iter > h->maxit || h->iter - copied > HIST_CAP)
+                return fail(s, EG_ERR_CUDA, "device solver state is inconsistent (iter %d)", h->iter);
             if (history)
                 for (int i = copied + 1; i <= h->iter; ++i) history[i] = h->hist[i % HIST_CAP];
             copied = h->iter;
@@ -662,6 +711,7 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     for (int d = 0; d < 6; ++d) s->vec[d] = s->ws + L.off_vec + (size_t)d * align_up(L.n * L.vsz, 256);
     for (int d = 0; d < 2; ++d)
         s->zext[d] = s->ws + L.off_z + (size_t)d * align_up((L.n + 2 * L.row) * L.vsz, 256);
+    s->wave_flags = (int*)(s->ws + L.off_pv);
     s->slots = (double*)(s->ws + L.off_slots);
     s->gsum = (double*)(s->ws + L.off_gsum);
     s->gall = s->gsum + 8 * 3;
@@ -706,6 +756,30 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         else memcpy(&id, dist->nccl_unique_id, sizeof id);
         if (rc == EG_OK && r == ncclSuccess) r = ncclCommInitRank(&s->comm, s->nranks, id, s->rank);
         if (r != ncclSuccess) rc = fail(s, EG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    if (rc == EG_OK) {  // fused wavefront phases: fp32 vectors, one GPU, TMEM Thomas available
+        // opt-in (EG_WAVE=1): on B200 it is slower than the tuned 5-kernel schedule because ~600
+        // resident 128x70-point work items stream ~130 MB between writing a z row and reading it
+        // back, more than L2 holds (DESIGN.md §Fused phases)
+        const char* wv = getenv("EG_WAVE");
+        const char* nf = getenv("EG_NO_FUSE");
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        s->wave_ctas = 4 * nsm;
+        // deadlock freedom needs more resident CTAs than tiles per row (phase.cuh)
+        s->use_wave = s->use_tm && s->comm == nullptr && 2 * s->L.tiles < s->wave_ctas && wv && wv[0] == '1' &&
+                      !(nf && nf[0] == '1');
+        if (s->use_wave) {
+            cudaError_t e1 = prec == EG_MIXED
+                ? cudaFuncSetAttribute(k_wave<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm)
+                : cudaFuncSetAttribute(k_wave<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm);
+            cudaError_t e2 = prec == EG_MIXED
+                ? cudaFuncSetAttribute(k_wave<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm)
+                : cudaFuncSetAttribute(k_wave<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm);
+            cudaError_t e3 = cudaMemsetAsync(s->wave_flags, 0, (size_t)s->L.nyl * s->L.tiles * sizeof(int), s->st);
+            if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) rc = fail(s, EG_ERR_CUDA, "wave setup");
+        }
     }
     if (rc == EG_OK)
         rc = prec == EG_FP64 ? create_impl<0>(s, bands) : prec == EG_MIXED ? create_impl<1>(s, bands) : create_impl<2>(s, bands);
@@ -808,6 +882,8 @@ int eg_profile_get(const eg_solver* s, int kid, double* total_ms, int64_t* launc
             case KID_APPLY: per = 7 * V + V; break;
             case KID_PRECOND: per = 3 * V + V; break;
             case KID_CONVERT: per = 12; break;
+            case KID_PHASE_A: per = 4 * V + 6 * V + 3 * V; break;   // r,p,v,rhat0 + B4,B2; p',z,v'
+            case KID_PHASE_B: per = 2 * V + 6 * V + 3 * V; break;   // r,v' + B4,B2; s,z_s,t
             default: per = 0;
         }
         *alg_bytes_per_launch = per * n;

@@ -437,45 +437,42 @@ __device__ __forceinline__ void tm_ld8(uint32_t taddr, float (&c)[8]) {
     for (int e = 0; e < 8; ++e) c[e] = __uint_as_float(r[e]);
 }
 
-template <int MODE, int KIND>
-__global__ void __launch_bounds__(128, 4) k_thomas_tm(Geo g, Vecs<MODE> vv, const float* __restrict__ fin,
-                                                      float* __restrict__ zout) {
-    using V = float;
-    static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
-    constexpr int KB = 8;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    __shared__ uint32_t tm_base;
-    V* ys = reinterpret_cast<V*>(smraw);
-    const int tid = threadIdx.x, warp = tid >> 5;
-    V beta = 0, omega = 0, alpha = 0;
-    bool fresh = false;
-    if (KIND != 0) {
-        const DevState* st = vv.st;
-        if (st->halt != H_RUN) return;  // uniform: before any collective
-        if (KIND == 1) {
-            fresh = st->fresh != 0;
-            beta = (V)st->beta_v;
-            omega = (V)st->omega_v;
-        } else {
-            alpha = (V)st->alpha_v;
-        }
-    }
-    if (warp == 0) {
+// TMEM allocation of 128 columns by warp 0 (with the fence / barrier / fence hand-off) and release
+__device__ __forceinline__ uint32_t tm_alloc128(uint32_t* slot) {
+    if ((threadIdx.x >> 5) == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&tm_base))
+                         (uint32_t)__cvta_generic_to_shared(slot))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t taddr = tm_base + ((uint32_t)(warp * 32) << 16);
+    return *slot;
+}
 
+__device__ __forceinline__ void tm_free128(uint32_t base) {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(base) : "memory");
+    }
+}
+
+// One 128-column tile of one latitude row: f = update(inputs), z = T^-1 f, with c'_k in this
+// thread's TMEM lane and y_k in shared memory ys[k][128].  All 128 threads of the CTA call it
+// (warp-collective TMEM access); `act` masks columns beyond nx.  KIND as in k_thomas.
+template <int MODE, int KIND>
+__device__ __forceinline__ void thomas_tm_tile(const Geo& g, const Vecs<MODE>& vv, int64_t row_base, int i,
+                                               bool act, uint32_t taddr, float* ys, float beta, float omega,
+                                               float alpha, bool fresh, const float* __restrict__ fin,
+                                               float* __restrict__ zout) {
+    using V = float;
+    constexpr int KB = 8;
+    const int tid = threadIdx.x;
     const int nx = (int)g.nx, nz = (int)g.nz;
-    const int i_raw = blockIdx.x * 128 + tid;
-    const bool act = i_raw < nx;
-    const int i = act ? i_raw : nx - 1;  // inactive lanes read a valid column, never store
-    const int64_t base = (int64_t)blockIdx.y * g.row + i;
+    const int64_t base = row_base + i;
     const V* __restrict__ A0 = (KIND == 0 ? fin : vv.r) + base;
     // p = v = 0 after a (re)start: read r in their place with beta = 0, so the update is exactly
     // f = r + 0*(r - omega r) = r without a data-dependent branch
@@ -562,12 +559,36 @@ __global__ void __launch_bounds__(128, 4) k_thomas_tm(Geo g, Vecs<MODE> vv, cons
             }
         }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tm_base) : "memory");
+}
+
+template <int MODE, int KIND>
+__global__ void __launch_bounds__(128, 4) k_thomas_tm(Geo g, Vecs<MODE> vv, const float* __restrict__ fin,
+                                                      float* __restrict__ zout) {
+    static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ uint32_t tm_base;
+    float beta = 0.f, omega = 0.f, alpha = 0.f;
+    bool fresh = false;
+    if (KIND != 0) {
+        const DevState* st = vv.st;
+        if (st->halt != H_RUN) return;  // uniform: before any collective
+        if (KIND == 1) {
+            fresh = st->fresh != 0;
+            beta = (float)st->beta_v;
+            omega = (float)st->omega_v;
+        } else {
+            alpha = (float)st->alpha_v;
+        }
     }
+    const uint32_t base = tm_alloc128(&tm_base);
+    const int warp = threadIdx.x >> 5;
+    const int nx = (int)g.nx;
+    const int i_raw = blockIdx.x * 128 + threadIdx.x;
+    const bool act = i_raw < nx;
+    const int i = act ? i_raw : nx - 1;  // inactive lanes read a valid column, never store
+    thomas_tm_tile<MODE, KIND>(g, vv, (int64_t)blockIdx.y * g.row, i, act, base + ((uint32_t)(warp * 32) << 16),
+                               reinterpret_cast<float*>(smraw), beta, omega, alpha, fresh, fin, zout);
+    tm_free128(base);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -915,6 +936,7 @@ __global__ void __launch_bounds__(1024) k_fin(Geo g, const double* __restrict__ 
                                               double* __restrict__ gsum, int first) {
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
     const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
+    if (threadIdx.x == 0) { st->epoch += 1; st->wave_ctr = 0; }  // for the next wavefront launch
     if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;
     if (WHICH == W_C && st->sexit) {  // s-step exit: no sums needed
         if (threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gsum, st, first);
@@ -938,6 +960,7 @@ __global__ void __launch_bounds__(1024) k_fin_groups(Geo g, const double* __rest
 
 template <int MODE, int WHICH>
 __global__ void k_fin_logic(Geo g, const double* __restrict__ gall, DevState* st, int first) {
+    if (threadIdx.x == 0) { st->epoch += 1; st->wave_ctr = 0; }
     if (threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gall, st, first);
 }
 

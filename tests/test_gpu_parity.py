@@ -62,8 +62,12 @@ def test_precondition_parity(prob, mode):
     assert _rel(z, zo) <= (1e-12 if mode == "fp64" else 1e-5)
 
 
-@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED, gen.Problem(130, 9, 70, seed=10)],
-                         ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+FUSED_ODD = gen.Problem(128, 37, 13, seed=11)   # fused phase path (nx % 64 == 0), odd ny / nz
+FUSED_THIN = gen.Problem(192, 3, 70, seed=12)   # fewer rows than the per-CTA row ranges
+
+
+@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED, gen.Problem(130, 9, 70, seed=10), FUSED_ODD,
+                                  FUSED_THIN], ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("tol", [1e-3, 1e-4])
 def test_solve_parity(prob, mode, tol):
@@ -83,7 +87,7 @@ def test_solve_parity(prob, mode, tol):
     assert _rel(x, xo) <= 10 * tol
 
 
-@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED], ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED, FUSED_ODD], ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
 @pytest.mark.parametrize("mode", MODES)
 def test_fixed_iteration_history_parity(prob, mode):
     s, bands, b = _make(prob, mode)
@@ -189,7 +193,10 @@ def test_profile_counts_kernels():
     s.profile_reset()
     s.solve(torch.from_numpy(b).cuda(), tol=0.0, maxit=4, flags=egs.EG_SOLVE_PROFILE)
     p = s.profile()
-    for k in ("thomas_p", "stencil_dot_A", "thomas_s", "stencil_dot_B", "update_xr"):
+    fused = p["phase_A"][1] > 0
+    names = ("phase_A", "phase_B", "update_xr") if fused else (
+        "thomas_p", "stencil_dot_A", "thomas_s", "stencil_dot_B", "update_xr")
+    for k in names:
         assert p[k][1] == 4 and p[k][0] > 0 and p[k][2] > 0
 
 
@@ -212,3 +219,28 @@ def test_multirank_finaliser_path_bitwise_equal(mode, monkeypatch):
     y1 = s1.apply(torch.ones(prob.n, dtype=s1.vdtype, device="cuda"))
     y2 = s2.apply(torch.ones(prob.n, dtype=s2.vdtype, device="cuda"))
     assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], FUSED_ODD, FUSED_THIN, gen.CONFIGS["C2"]],
+                         ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+@pytest.mark.parametrize("mode", ["mixed", "fp32"])
+def test_fused_phases_match_unfused_schedule(prob, mode, monkeypatch):
+    """The opt-in fused wavefront phase kernels (EG_WAVE=1: Thomas + stencil per work item) compute
+    z, v, s, t with the same operations as the 5-kernel schedule and the same reduction slots, so
+    the solve is bitwise identical."""
+    bands, b = gen.host(prob)
+    g = (prob.nx, prob.ny, prob.nz)
+    bd = torch.from_numpy(bands).cuda()
+    bt = torch.from_numpy(b).cuda()
+    monkeypatch.setenv("EG_WAVE", "1")
+    s1 = egs.Solver(g, bd, mode)
+    monkeypatch.delenv("EG_WAVE")
+    s2 = egs.Solver(g, bd, mode)
+    for tol, maxit in ((0.0, 8), (1e-5, 100)):
+        x1, i1, h1 = s1.solve(bt, tol=tol, maxit=maxit)
+        x2, i2, h2 = s2.solve(bt, tol=tol, maxit=maxit)
+        assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
+    s1.profile_reset()
+    s1.solve(bt, tol=0.0, maxit=3, flags=egs.EG_SOLVE_PROFILE)
+    p = s1.profile()
+    assert p["phase_A"][1] == 3 and p["phase_B"][1] == 3 and p["thomas_p"][1] == 0
