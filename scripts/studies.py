@@ -1,0 +1,198 @@
+"""Studies on top of the solver, run on the GPU:
+
+  table1    NEXT-3: Table 1 analogue: 11 seeded "dates" x R_c in {1e-3, 1e-4}
+            x {mixed, fp64} at C5 size: mean (standard error) iterations and time-to-solution
+            (set_operator + solve, CUDA events).
+  timestep  NEXT-4: time-varying operator workflow: per "time step" the
+            operator is rebuilt (a new seed) and 4 solves follow, each warm-started from the previous
+            solution with a perturbed right-hand side.
+  precision NEXT-2: deep-convergence precision study: R_i histories of
+            fp32 / mixed / fp64 run without a halting criterion (tol = 0) on a harder operator, with
+            and without the mandatory restart.
+
+    python scripts/studies.py table1 [--config C5] [--dates 11] > profiles/r01_table1.json
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+import paper_1811_03852_b200 as egs  # noqa: E402
+
+
+def _mean_se(v):
+    m = statistics.mean(v)
+    se = statistics.stdev(v) / math.sqrt(len(v)) if len(v) > 1 else 0.0
+    return m, se
+
+
+def _problem(base, seed):
+    return base.with_(seed=seed)
+
+
+def table1(args):
+    base = gen.CONFIGS[args.config]
+    st = torch.cuda.Stream()
+    dev = torch.device("cuda")
+    res = {m: {tol: {"iters": [], "ms": [], "true_R": []} for tol in (1e-3, 1e-4)} for m in ("mixed", "fp64")}
+    first_R = {"mixed": [], "fp64": []}
+    with torch.cuda.stream(st):
+        bands = torch.empty((7, base.n), dtype=torch.float64, device=dev)
+        b = torch.empty(base.n, dtype=torch.float64, device=dev)
+        x = torch.empty(base.n, dtype=torch.float64, device=dev)
+        gen.device(base, bands, b, stream=st)
+        solvers = {m: egs.Solver((base.nx, base.ny, base.nz), bands, m, stream=st) for m in ("mixed", "fp64")}
+        for d in range(args.dates):
+            prob = _problem(base, args.seed0 + d)
+            gen.device(prob, bands, b, stream=st)
+            for m, s in solvers.items():
+                for tol in (1e-3, 1e-4):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    torch.cuda.synchronize()
+                    e0.record(st)
+                    s.set_operator(bands)
+                    _, info, hist = s.solve(b, tol=tol, maxit=args.maxit, out=x)
+                    e1.record(st)
+                    torch.cuda.synchronize()
+                    r = res[m][tol]
+                    r["iters"].append(info.iters)
+                    r["ms"].append(e0.elapsed_time(e1))
+                    r["true_R"].append(info.true_R)
+                    if tol == 1e-4:
+                        first_R[m].append(float(hist[1]))
+    out = {"study": "NEXT-3 Table 1 analogue", "config": args.config, "grid": [base.nx, base.ny, base.nz],
+           "dates": args.dates, "seeds": [args.seed0 + d for d in range(args.dates)],
+           "paper": {"1e-3": {"mixed": [8.4, 0.346], "fp64": [8.4, 0.592]},
+                     "1e-4": {"mixed": [29.3, 1.18], "fp64": [29.3, 2.06]},
+                     "note": "PAPER.md:506-507, 96 XC40 nodes, real UM states (context only)"},
+           "rows": {}}
+    for tol in (1e-3, 1e-4):
+        row = {}
+        for m in ("mixed", "fp64"):
+            it_m, it_se = _mean_se(res[m][tol]["iters"])
+            t_m, t_se = _mean_se(res[m][tol]["ms"])
+            row[m] = {"iters_mean": it_m, "iters_se": it_se, "ms_mean": t_m, "ms_se": t_se,
+                      "iters": res[m][tol]["iters"], "max_true_R": max(res[m][tol]["true_R"])}
+        row["identical_iterations"] = res["mixed"][tol]["iters"] == res["fp64"][tol]["iters"]
+        row["fp64_over_mixed_time"] = row["fp64"]["ms_mean"] / row["mixed"]["ms_mean"]
+        out["rows"][f"{tol:g}"] = row
+    out["R1_rel_diff_max"] = max(abs(a - c) / c for a, c in zip(first_R["mixed"], first_R["fp64"]))
+    return out
+
+
+def timestep(args):
+    base = gen.CONFIGS[args.config]
+    st = torch.cuda.Stream()
+    dev = torch.device("cuda")
+    rows = []
+    with torch.cuda.stream(st):
+        bands = torch.empty((7, base.n), dtype=torch.float64, device=dev)
+        b = torch.empty(base.n, dtype=torch.float64, device=dev)
+        gen.device(base, bands, b, stream=st)
+        s = egs.Solver((base.nx, base.ny, base.nz), bands, args.precision, stream=st)
+        x = torch.zeros(base.n, dtype=torch.float64, device=dev)
+        g = torch.Generator(device=dev).manual_seed(7)
+        for step in range(args.steps):
+            gen.device(_problem(base, args.seed0 + step), bands, b, stream=st)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(st)
+            s.set_operator(bands)  # "recomputed at every time step"
+            e1.record(st)
+            torch.cuda.synchronize()
+            set_ms = e0.elapsed_time(e1)
+            for k in range(4):  # "solved four times per time step"
+                rhs = b + 0.01 * k * torch.randn(base.n, generator=g, device=dev, dtype=torch.float64)
+                x0 = x.clone() if (step > 0 or k > 0) else None
+                e0.record(st)
+                _, info, _ = s.solve(rhs, x0=x0, tol=args.tol, maxit=200, out=x)
+                e1.record(st)
+                torch.cuda.synchronize()
+                rows.append({"step": step, "solve": k, "warm": x0 is not None, "iters": info.iters,
+                             "ms": e0.elapsed_time(e1), "set_operator_ms": set_ms if k == 0 else 0.0,
+                             "true_R": info.true_R, "converged": info.converged})
+    return {"study": "NEXT-4 time-varying operator workflow", "config": args.config,
+            "precision": args.precision, "tol": args.tol, "rows": rows,
+            "mean_iters_cold": statistics.mean(r["iters"] for r in rows if not r["warm"]),
+            "mean_iters_warm": statistics.mean(r["iters"] for r in rows if r["warm"]),
+            "mean_set_operator_ms": statistics.mean(r["set_operator_ms"] for r in rows if r["solve"] == 0)}
+
+
+def precision(args):
+    """Deep convergence without a halting criterion on a harder operator
+    (knob, not from the paper: c_v ~ U(cv_lo, cv_hi), delta ~ U(dl_lo, dl_hi)).  For each mode and
+    restart setting: the recurrence history R_i of one tol = 0 run, and the TRUE residual after i
+    iterations (one tol = 0, maxit = i solve per i, verified in fp64) — below eps_32 the two differ,
+    which is the regime Fig. 1 / Fig. 3 are about."""
+    prob = gen.Problem(args.nx, args.ny, args.nz, seed=args.seed0, cv=(args.cv_lo, args.cv_hi),
+                       dl=(args.dl_lo, args.dl_hi))
+    bands, b = gen.host(prob)
+    bd = torch.from_numpy(bands).cuda()
+    bt = torch.from_numpy(b).cuda()
+    out = {"study": "NEXT-2 deep-convergence precision study", "grid": [prob.nx, prob.ny, prob.nz],
+           "knob": f"c_v ~ U({args.cv_lo}, {args.cv_hi}), delta ~ U({args.dl_lo}, {args.dl_hi}) (harder than "
+                   "BASELINE.json; not from the paper)",
+           "maxit": args.maxit, "runs": {}}
+    ths = (1e-3, 1e-4, 1e-5, 1e-6, 1e-7, 1e-8, 1e-9)
+    for m in ("fp32", "mixed", "fp64"):
+        s = egs.Solver((prob.nx, prob.ny, prob.nz), bd, m)
+        for restart in (0, 150):
+            _, info, hist = s.solve(bt, tol=0.0, maxit=args.maxit, restart_every=restart, raise_on_error=False)
+            true = []
+            for i in range(0, args.maxit + 1, args.true_stride):
+                _, inf_i, _ = s.solve(bt, tol=0.0, maxit=i, restart_every=restart, raise_on_error=False)
+                true.append((i, inf_i.true_R))
+
+            def first(seq, th):
+                for i, v in seq:
+                    if v <= th:
+                        return i
+                return None
+            out["runs"][f"{m}/restart{restart}"] = {
+                "status": info.status, "iters": info.iters, "restarts": info.restarts,
+                "breakdowns": info.breakdowns, "final_true_R": info.true_R,
+                "first_iter_recurrence_below": {f"{t:g}": first(list(enumerate(hist)), t) for t in ths},
+                "first_iter_true_below": {f"{t:g}": first(true, t) for t in ths},
+                "min_true_R": min(v for _, v in true),
+                "history": [float(v) for v in hist], "true_history": true}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("study", choices=["table1", "timestep", "precision"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--dates", type=int, default=11)
+    ap.add_argument("--seed0", type=int, default=4)
+    ap.add_argument("--maxit", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--tol", type=float, default=1e-4)
+    ap.add_argument("--precision", default="mixed")
+    ap.add_argument("--nx", type=int, default=192)
+    ap.add_argument("--ny", type=int, default=144)
+    ap.add_argument("--nz", type=int, default=70)
+    ap.add_argument("--cv-lo", type=float, default=5.0)
+    ap.add_argument("--cv-hi", type=float, default=20.0)
+    ap.add_argument("--dl-lo", type=float, default=1e-4)
+    ap.add_argument("--dl-hi", type=float, default=1e-3)
+    ap.add_argument("--true-stride", type=int, default=2)
+    a = ap.parse_args()
+    t0 = time.time()
+    out = {"table1": table1, "timestep": timestep, "precision": precision}[a.study](a)
+    out["wall_s"] = time.time() - t0
+    out["device"] = torch.cuda.get_device_name()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
