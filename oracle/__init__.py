@@ -27,7 +27,8 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SINGULAR_DIAG", 3: "ERR_DEGENERATE_RHS"
 
 class _Params(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int32),
-                ("restart_every", ctypes.c_int32), ("precond_scale", ctypes.c_double)]
+                ("restart_every", ctypes.c_int32), ("precond_scale", ctypes.c_double),
+                ("sor_sweeps", ctypes.c_int32), ("sor_omega", ctypes.c_double)]
 
 
 class _Info(ctypes.Structure):
@@ -71,6 +72,8 @@ def lib():
                                    ctypes.POINTER(_Params), dp, dp, ctypes.POINTER(_Info)]
         L.oracle_solve.restype = ctypes.c_int
         L.oracle_threads.restype = ctypes.c_int
+        L.oracle_trisor.argtypes = [i64, i64, i64, ctypes.c_int, dp, dp, ctypes.c_int, ctypes.c_double, dp, dp]
+        L.oracle_trisor.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -133,6 +136,18 @@ def thomas(grid, mode, ahat6, f):
     return z
 
 
+def trisor(grid, mode, ahat6, f, sweeps=3, omega=1.5, x_init=None):
+    """NEXT-1 tri-SOR (Eq. 7), red-black column ordering (see oracle.h)."""
+    nx, ny, nz = grid
+    z = np.empty(nx * ny * nz, np.float64)
+    rc = lib().oracle_trisor(nx, ny, nz, _mode(mode), _dp(np.ascontiguousarray(ahat6)),
+                             _dp(np.ascontiguousarray(f, np.float64)), int(sweeps), float(omega),
+                             _dp(None if x_init is None else np.ascontiguousarray(x_init, np.float64)), _dp(z))
+    if rc:
+        raise OracleError(rc)
+    return z
+
+
 def residual64(grid, ahat6, bhat, x):
     nx, ny, nz = grid
     r = np.empty(nx * ny * nz, np.float64)
@@ -147,13 +162,13 @@ def dot(grid, mode, a, b) -> float:
 
 
 def solve(grid, mode, ahat6, diag, b, x0=None, tol=1e-4, maxit=200, restart_every=150,
-          precond_scale=1.0, raise_on_error=False):
+          precond_scale=1.0, raise_on_error=False, sor_sweeps=0, sor_omega=1.5):
     """BiCGStab (see oracle.h).  Returns (x, hist[: iters+1], Info)."""
     nx, ny, nz = grid
     n = nx * ny * nz
     x = np.empty(n, np.float64)
     hist = np.full(maxit + 1, np.nan)
-    prm = _Params(tol, maxit, restart_every, precond_scale)
+    prm = _Params(tol, maxit, restart_every, precond_scale, sor_sweeps, sor_omega)
     info = _Info()
     rc = lib().oracle_solve(nx, ny, nz, _mode(mode), _dp(np.ascontiguousarray(ahat6)), _dp(diag),
                             _dp(np.ascontiguousarray(b, np.float64)),

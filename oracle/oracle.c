@@ -155,6 +155,55 @@ void oracle_thomas(int64_t nx, int64_t ny, int64_t nz, int mode, const double* a
     }
 }
 
+/* ---- NEXT-1: tri-SOR, Eq. 7, red-black column ordering ---- */
+
+int oracle_trisor(int64_t nx, int64_t ny, int64_t nz, int mode, const double* ahat6, const double* f,
+                  int sweeps, double omega, const double* x_init, double* x) {
+    if (nx < 3 || nx % 2 != 0 || sweeps < 0) return OR_ERR_ARG;
+    const int64_t n = nx * ny * nz;
+    const double* U = ahat6 + (int64_t)U_ * n;
+    const double* D = ahat6 + (int64_t)D_ * n;
+    for (int64_t q = 0; q < n; ++q) x[q] = x_init ? rv(mode, x_init[q]) : 0.0;
+    double* rhs = (double*)malloc(sizeof(double) * (size_t)nz);
+    double* cp = (double*)malloc(sizeof(double) * (size_t)nz);
+    double* y = (double*)malloc(sizeof(double) * (size_t)nz);
+    for (int sw = 0; sw < sweeps; ++sw)
+        for (int colour = 0; colour < 2; ++colour)
+            for (int64_t j = 0; j < ny; ++j)
+                for (int64_t i = 0; i < nx; ++i) {
+                    if ((i + j) % 2 != colour) continue;
+#define Q(k) ((i) + nx * ((k) + nz * (j)))
+                    /* rhs = (1 - omega) T x_old + omega (f - H x) */
+                    for (int64_t k = 0; k < nz; ++k) {
+                        double tx = x[Q(k)];
+                        if (k + 1 < nz) tx = rv(mode, tx + rv(mode, U[Q(k)] * x[Q(k + 1)]));
+                        if (k > 0) tx = rv(mode, tx + rv(mode, D[Q(k)] * x[Q(k - 1)]));
+                        double hx = 0.0;
+                        for (int d = E_; d <= S_; ++d) {
+                            int64_t qn;
+                            if (nbr(nx, ny, nz, d, i, j, k, &qn))
+                                hx = rv(mode, hx + rv(mode, ahat6[(int64_t)d * n + Q(k)] * x[qn]));
+                        }
+                        rhs[k] = rv(mode, rv(mode, (1.0 - omega) * tx) + rv(mode, omega * rv(mode, f[Q(k)] - hx)));
+                    }
+                    /* x_col = T^-1 rhs (same recurrence as oracle_thomas) */
+                    cp[0] = U[Q(0)];
+                    y[0] = rhs[0];
+                    for (int64_t k = 1; k < nz; ++k) {
+                        double m = rv(mode, 1.0 - rv(mode, D[Q(k)] * cp[k - 1]));
+                        cp[k] = rv(mode, U[Q(k)] / m);
+                        y[k] = rv(mode, rv(mode, rhs[k] - rv(mode, D[Q(k)] * y[k - 1])) / m);
+                    }
+                    x[Q(nz - 1)] = y[nz - 1];
+                    for (int64_t k = nz - 2; k >= 0; --k) x[Q(k)] = rv(mode, y[k] - rv(mode, cp[k] * x[Q(k + 1)]));
+#undef Q
+                }
+    free(rhs);
+    free(cp);
+    free(y);
+    return OR_OK;
+}
+
 /* ---- global sums ---- */
 
 double oracle_dot(int64_t nx, int64_t ny, int64_t nz, int mode, const double* a, const double* b) {
@@ -180,7 +229,8 @@ int oracle_solve(int64_t nx, int64_t ny, int64_t nz, int mode, const double* aha
     const int64_t n = nx * ny * nz;
     oracle_info inf;
     memset(&inf, 0, sizeof inf);
-    if (nx < 3 || ny < 1 || nz < 1 || mode < 0 || mode > 2 || !prm || prm->maxit < 0) {
+    if (nx < 3 || ny < 1 || nz < 1 || mode < 0 || mode > 2 || !prm || prm->maxit < 0 ||
+        (prm->sor_sweeps > 0 && nx % 2 != 0)) {
         inf.status = OR_ERR_ARG;
         if (info) *info = inf;
         return OR_ERR_ARG;
@@ -248,8 +298,9 @@ start:
             for (int64_t q = 0; q < n; ++q)
                 p[q] = rv(mode, r[q] + rv(mode, bv * rv(mode, p[q] - rv(mode, ov * v[q]))));
         }
-        /* z = C^-1 p  (C^-1 = T^-1, reading A-3), v = Ahat z */
-        oracle_thomas(nx, ny, nz, mode, ahat6, p, z);
+        /* z = C^-1 p  (C^-1 = T^-1, reading A-3; or tri-SOR, NEXT-1), v = Ahat z */
+        if (prm->sor_sweeps > 0) oracle_trisor(nx, ny, nz, mode, ahat6, p, prm->sor_sweeps, prm->sor_omega, 0, z);
+        else oracle_thomas(nx, ny, nz, mode, ahat6, p, z);
         if (prm->precond_scale != 1.0)
             for (int64_t q = 0; q < n; ++q) z[q] = rv(mode, prm->precond_scale * z[q]);
         oracle_apply_wp(nx, ny, nz, mode, ahat6, z, v);
@@ -260,7 +311,8 @@ start:
             const double av = rv(mode, alpha);
             for (int64_t q = 0; q < n; ++q) s[q] = rv(mode, r[q] - rv(mode, av * v[q]));
         }
-        oracle_thomas(nx, ny, nz, mode, ahat6, s, zs);
+        if (prm->sor_sweeps > 0) oracle_trisor(nx, ny, nz, mode, ahat6, s, prm->sor_sweeps, prm->sor_omega, 0, zs);
+        else oracle_thomas(nx, ny, nz, mode, ahat6, s, zs);
         if (prm->precond_scale != 1.0)
             for (int64_t q = 0; q < n; ++q) zs[q] = rv(mode, prm->precond_scale * zs[q]);
         oracle_apply_wp(nx, ny, nz, mode, ahat6, zs, t);

@@ -68,6 +68,18 @@ void oracle_apply_wp(int64_t nx, int64_t ny, int64_t nz, int mode, const double*
 void oracle_thomas(int64_t nx, int64_t ny, int64_t nz, int mode, const double* ahat6,
                    const double* f, double* z);
 
+/* NEXT-1: tri-SOR preconditioner (Eq. 7) in red-black column ordering:
+ *   (T + omega L) x_n = (1 - omega) T x_{n-1} + omega (f - U x_{n-1}),   Ahat = L + T + U (Eq. 6)
+ * Columns (i, j) are coloured (i + j) % 2 (red = 0 first, then black = 1; nx must be even so the
+ * periodic seam keeps the colouring).  For every column of the current colour, in place:
+ *   rhs_k = (1 - omega) (T x)_k + omega (f_k - sum_{E,W,N,S} ahat_h x_nbr)   (current neighbours)
+ *   x_col = T^-1 rhs                                                        (Thomas, as above)
+ * i.e. L couples a column to already-updated neighbours and U to not-yet-updated ones (reading
+ * DESIGN.md NEXT-1).  x starts from x_init (NULL = 0: the fixed linear preconditioner of BiCGStab).
+ * Every operation rounded to the working precision of `mode`.  Returns OR_ERR_ARG for odd nx. */
+int oracle_trisor(int64_t nx, int64_t ny, int64_t nz, int mode, const double* ahat6, const double* f,
+                  int sweeps, double omega, const double* x_init, double* x);
+
 /* r = bhat - Ahat x in binary64 (bands promoted), the restart / verification residual. */
 void oracle_residual64(int64_t nx, int64_t ny, int64_t nz, const double* ahat6, const double* bhat,
                        const double* x, double* r);
@@ -82,6 +94,8 @@ typedef struct {
     int32_t maxit;
     int32_t restart_every; /* mandatory restart period, 150 in the UM; <=0 off */
     double precond_scale;  /* test hook: M^-1 -> precond_scale * T^-1 (A-3); 1 */
+    int32_t sor_sweeps;    /* 0: M^-1 = T^-1 (hot path, A-3); > 0: tri-SOR with this many sweeps */
+    double sor_omega;      /* tri-SOR over-relaxation (1.5 in the UM) */
 } oracle_params;
 
 typedef struct {
