@@ -121,6 +121,17 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
  * or communicator setup.  On error the previous operator is no longer valid. */
 int eg_solver_set_operator(eg_solver* s, const double* const bands[7]);
 
+/* NEXT-1 — choose the preconditioner C^-1.
+ *   EG_PRECOND_TRIDIAG (default): C^-1 = T^-1, one Jacobi-ordered Eq. 7 sweep from 0 (reading A-3).
+ *   EG_PRECOND_TRISOR: `sweeps` sweeps (the UM uses "typically three") of the tri-SOR
+ *     fixed point (Eq. 7, over-relaxation `omega`, 1.5 in the UM) from x = 0, columns in
+ *     red-black order ((i + j) % 2; L = couplings to already-updated columns, U = to the others).
+ *     Requires nx even (periodic 2-colouring), sweeps >= 1, 0 < omega < 2.
+ * Applies to eg_solve and eg_precondition.  Errors: EG_ERR_ARG. */
+#define EG_PRECOND_TRIDIAG 0
+#define EG_PRECOND_TRISOR 1
+int eg_solver_set_preconditioner(eg_solver* s, int kind, int sweeps, double omega);
+
 /* y = Ahat x, the scaled operator the solver iterates with (unit diagonal + 6 bands; periodic in i,
  * absent neighbours contribute 0).  x, y: DEVICE arrays of the local rows in the working precision
  * (float for EG_MIXED / EG_FP32, double for EG_FP64).  Exchanges halo rows when distributed

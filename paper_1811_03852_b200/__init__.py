@@ -24,7 +24,8 @@ STATUS = {0: "EG_OK", 1: "EG_ERR_ARG", 2: "EG_ERR_SINGULAR_DIAG", 3: "EG_ERR_DEG
           4: "EG_ERR_BREAKDOWN", 5: "EG_ERR_NONFINITE", 6: "EG_ERR_CUDA", 7: "EG_ERR_NCCL",
           8: "EG_ERR_WORKSPACE"}
 # symbols declared in include/egsolve.h (tests check the library exports all of them)
-ABI_SYMBOLS = ("eg_workspace_bytes", "eg_solver_create", "eg_solver_set_operator", "eg_apply_operator", "eg_precondition",
+ABI_SYMBOLS = ("eg_workspace_bytes", "eg_solver_create", "eg_solver_set_operator",
+               "eg_solver_set_preconditioner", "eg_apply_operator", "eg_precondition",
                "eg_solve", "eg_solver_destroy", "eg_last_error", "eg_status_str",
                "eg_nccl_unique_id", "eg_num_kernels", "eg_kernel_name", "eg_profile_get",
                "eg_profile_reset")
@@ -86,6 +87,7 @@ def lib():
                                        ctypes.POINTER(vp), i32, vp, ctypes.c_size_t, vp,
                                        ctypes.POINTER(vp)]
         L.eg_solver_set_operator.argtypes = [vp, ctypes.POINTER(vp)]
+        L.eg_solver_set_preconditioner.argtypes = [vp, i32, i32, ctypes.c_double]
         L.eg_apply_operator.argtypes = [vp, vp, vp]
         L.eg_precondition.argtypes = [vp, vp, vp]
         L.eg_solve.argtypes = [vp, vp, vp, ctypes.POINTER(_Params), vp, vp, ctypes.POINTER(_Info)]
@@ -212,6 +214,12 @@ class Solver:
         assert tuple(bands.shape) == (7, self.n_local)
         ptrs = (ctypes.c_void_p * 7)(*[bands[d].data_ptr() for d in range(7)])
         self._check(lib().eg_solver_set_operator(self._h, ptrs), "eg_solver_set_operator")
+
+    def set_preconditioner(self, kind="tridiag", sweeps=3, omega=1.5):
+        """NEXT-1: "tridiag" (C^-1 = T^-1, default) or "trisor" (red-black tri-SOR, Eq. 7)."""
+        k = {"tridiag": 0, "trisor": 1}[kind]
+        self._check(lib().eg_solver_set_preconditioner(self._h, k, int(sweeps), float(omega)),
+                    "eg_solver_set_preconditioner")
 
     def apply(self, x, out=None):
         """y = Ahat x (working precision tensors, local rows)."""

@@ -25,11 +25,11 @@ namespace {
 
 enum KernelId {
     KID_SCALE = 0, KID_START, KID_FIN, KID_THOMAS_P, KID_STENCIL_A, KID_THOMAS_S, KID_STENCIL_B,
-    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_COUNT
+    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_SOR, KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"scale", "start", "finalize", "thomas_p", "stencil_dot_A",
                                        "thomas_s", "stencil_dot_B", "update_xr", "apply",
-                                       "precondition", "convert", "phase_A", "phase_B"};
+                                       "precondition", "convert", "phase_A", "phase_B", "trisor_half"};
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -101,6 +101,9 @@ struct eg_solver {
     bool use_wave = false;      // fused wavefront phases (fp32 working precision, one GPU)
     int wave_ctas = 0;
     int epoch_base = 1;         // first epoch of the next solve (flags are never reset)
+    int precond = EG_PRECOND_TRIDIAG;  // NEXT-1: EG_PRECOND_TRISOR selects red-black tri-SOR
+    int sor_sweeps = 3;
+    double sor_omega = 1.5;
     double* slots = nullptr;
     double* gsum = nullptr;  // [G][3] local
     double* gall = nullptr;  // [G][3] all ranks
@@ -297,9 +300,62 @@ int iteration_fused(eg_solver* s, void* x_it) {
     return EG_OK;
 }
 
+// NEXT-1: M^-1 f by `sor_sweeps` red-black tri-SOR sweeps (Eq. 7) into the ghosted array z (row 0
+// pointer).  KIND 1 / 2: the first sweep also forms and stores p (s); later sweeps read it back.
+template <int MODE, int KIND>
+int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin, typename Prec<MODE>::V* z) {
+    using V = typename Prec<MODE>::V;
+    const dim3 gs((unsigned)((s->grid.nx / 2 + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
+    const V* fsrc = KIND == 0 ? fin : (KIND == 1 ? v.p : v.s);
+    int rc;
+    for (int sw = 0; sw < s->sor_sweeps; ++sw)
+        for (int colour = 0; colour < 2; ++colour) {
+            {
+                ProfScope ps(s, KID_SOR);
+                if (sw == 0)
+                    k_sor_half<MODE, KIND, true><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, colour, s->sor_omega, 0);
+                else
+                    k_sor_half<MODE, 0, false><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fsrc, z, colour, s->sor_omega,
+                                                                                   KIND != 0);
+                CK(cudaGetLastError());
+            }
+            if ((rc = halo_ghosted(s, z))) return rc;
+        }
+    return EG_OK;
+}
+
+template <int MODE>
+int iteration_trisor(eg_solver* s, void* x_it) {
+    Vecs<MODE> v = vecs<MODE>(s, x_it);
+    const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+    int rc;
+    if ((rc = apply_trisor<MODE, 1>(s, v, nullptr, v.z))) return rc;
+    {
+        ProfScope ps(s, KID_STENCIL_A);
+        k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh);
+        CK(cudaGetLastError());
+    }
+    if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
+    if ((rc = apply_trisor<MODE, 2>(s, v, nullptr, v.zs))) return rc;
+    {
+        ProfScope ps(s, KID_STENCIL_B);
+        k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s);
+        CK(cudaGetLastError());
+    }
+    if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
+    {
+        ProfScope ps(s, KID_UPDATE);
+        if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
+        else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
+        CK(cudaGetLastError());
+    }
+    return finalize<MODE, W_C>(s, 0);
+}
+
 template <int MODE>
 int iteration(eg_solver* s, void* x_it) {
     using V = typename Prec<MODE>::V;
+    if (s->precond == EG_PRECOND_TRISOR) return iteration_trisor<MODE>(s, x_it);
     if (s->use_wave) return iteration_fused<MODE>(s, x_it);
     Vecs<MODE> v = vecs<MODE>(s, x_it);
     const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
@@ -604,6 +660,12 @@ template <int MODE>
 int precond_impl(eg_solver* s, const void* r, void* z) {
     using V = typename Prec<MODE>::V;
     Vecs<MODE> v = vecs<MODE>(s, s->x64);
+    if (s->precond == EG_PRECOND_TRISOR) {  // sweep in the ghosted buffer, then copy out
+        int rc = apply_trisor<MODE, 0>(s, v, (const V*)r, v.z);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(z, v.z, s->L.n * sizeof(V), cudaMemcpyDeviceToDevice, s->st));
+        return EG_OK;
+    }
     const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
     ProfScope ps(s, KID_PRECOND);
     if constexpr (MODE != 0) {
@@ -630,6 +692,10 @@ int set_thomas_smem_c(eg_solver* s) {
 
 template <int MODE>
 int set_thomas_smem(eg_solver* s) {
+    CK(cudaFuncSetAttribute(k_sor_half<MODE, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    CK(cudaFuncSetAttribute(k_sor_half<MODE, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    CK(cudaFuncSetAttribute(k_sor_half<MODE, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    CK(cudaFuncSetAttribute(k_sor_half<MODE, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
     int rc = set_thomas_smem_c<MODE, 1>(s);
     if (!rc) rc = set_thomas_smem_c<MODE, 2>(s);
     if constexpr (MODE != 0) {
@@ -798,6 +864,27 @@ int eg_solver_set_operator(eg_solver* s, const double* const bands[7]) {
     return s->mode == EG_FP64 ? create_impl<0>(s, bands) : s->mode == EG_MIXED ? create_impl<1>(s, bands) : create_impl<2>(s, bands);
 }
 
+int eg_solver_set_preconditioner(eg_solver* s, int kind, int sweeps, double omega) {
+    if (!s) return EG_ERR_ARG;
+    if (kind == EG_PRECOND_TRIDIAG) {
+        s->precond = kind;
+    } else if (kind == EG_PRECOND_TRISOR) {
+        if (s->grid.nx % 2 != 0 || sweeps < 1 || !(omega > 0.0 && omega < 2.0))
+            return fail(s, EG_ERR_ARG, "tri-SOR needs nx even, sweeps >= 1 and 0 < omega < 2");
+        s->precond = kind;
+        s->sor_sweeps = sweeps;
+        s->sor_omega = omega;
+    } else {
+        return fail(s, EG_ERR_ARG, "unknown preconditioner %d", kind);
+    }
+    if (s->graph) {  // the captured iteration depends on the preconditioner
+        cudaGraphExecDestroy(s->graph);
+        s->graph = nullptr;
+        s->graph_x = nullptr;
+    }
+    return EG_OK;
+}
+
 int eg_apply_operator(eg_solver* s, const void* x, void* y) {
     if (!s || !x || !y) return EG_ERR_ARG;
     s->profiling = false;
@@ -884,6 +971,7 @@ int eg_profile_get(const eg_solver* s, int kid, double* total_ms, int64_t* launc
             case KID_CONVERT: per = 12; break;
             case KID_PHASE_A: per = 4 * V + 6 * V + 3 * V; break;   // r,p,v,rhat0 + B4,B2; p',z,v'
             case KID_PHASE_B: per = 2 * V + 6 * V + 3 * V; break;   // r,v' + B4,B2; s,z_s,t
+            case KID_SOR: per = 0.5 * (V + V + 4 * V + 6 * V + V); break;  // half the points: f, x, 4 nbrs, bands; x
             default: per = 0;
         }
         *alg_bytes_per_launch = per * n;

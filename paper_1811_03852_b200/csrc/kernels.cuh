@@ -592,6 +592,149 @@ __global__ void __launch_bounds__(128, 4) k_thomas_tm(Geo g, Vecs<MODE> vv, cons
 }
 
 // ---------------------------------------------------------------------------------------------
+// NEXT-1: one half-sweep of the tri-SOR preconditioner (Eq. 7) in red-black column
+// order, over the columns (i, j) with (i + j) % 2 == colour:
+//   rhs_k = (1 - omega) (T x_old)_k + omega (f_k - (E x_E + W x_W + N x_N + S x_S)_k)
+//   x_col = T^-1 rhs                                   (Thomas, factors in shared memory)
+// The horizontal neighbours of a column all have the other colour, so they are either the values
+// of the previous sweep (red half) or of this sweep's red half (black half): in-place updates are
+// race-free.  FIRST (sweep 1, x = 0): no T x_old term, and the red half needs no neighbours
+// (rhs = omega f); with KIND 1 / 2 the first sweep also forms f = p (or s) for its colour's columns
+// and stores it (later sweeps read it back with KIND 0).  Thread m of row j owns column
+// i = 2m + ((j + colour) & 1); grid (ceil(nx/2 / W), nyl), dynamic smem 2*nz*W*sizeof(V).
+template <int MODE, int KIND, bool FIRST>
+__global__ void __launch_bounds__(128) k_sor_half(Geo g, Vecs<MODE> vv, const typename Prec<MODE>::V* __restrict__ fin,
+                                                  typename Prec<MODE>::V* __restrict__ x, int colour,
+                                                  double omega_d, int check_halt) {
+    using V = typename Prec<MODE>::V;
+    constexpr int KB = sizeof(V) == 4 ? 4 : 2;
+    constexpr int NA = 13;  // f, x(k), x(k+1) [own], xE, xW, xN, xS, E, W, N, S, U, D
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int W = blockDim.x, tid = threadIdx.x;
+    V* cps = reinterpret_cast<V*>(smraw);
+    V* ys = cps + g.nz * W;
+    V beta = 0, omega_b = 0, alpha = 0;
+    bool fresh = false;
+    if (KIND != 0) {
+        const DevState* st = vv.st;
+        if (st->halt != H_RUN) return;
+        if (KIND == 1) {
+            fresh = st->fresh != 0;
+            beta = (V)st->beta_v;
+            omega_b = (V)st->omega_v;
+        } else {
+            alpha = (V)st->alpha_v;
+        }
+    } else if (check_halt && vv.st->halt != H_RUN) {
+        return;
+    }
+    const V om = (V)omega_d, om1 = (V)(1.0 - omega_d);
+    const int nx = (int)g.nx, nz = (int)g.nz;
+    const int m = blockIdx.x * W + tid;
+    if (m >= nx / 2) return;
+    const int64_t jl = blockIdx.y, jg = g.j0 + jl;
+    const int i = 2 * m + (int)((jg + colour) & 1);
+    const int iE = (i + 1 == nx) ? 0 : i + 1, iW = (i == 0) ? nx - 1 : i - 1;
+    const int64_t rb = jl * g.row;
+    const V* __restrict__ xc = x + rb + i;
+    const V* __restrict__ xE = x + rb + iE;
+    const V* __restrict__ xW = x + rb + iW;
+    // at the poles the absent N / S neighbour (zero band) reads the E neighbour instead: it has the
+    // other colour, so it is already written even in the first sweep (the own column is not)
+    const V* __restrict__ xN = (jg < g.ny - 1) ? xc + g.row : xE;
+    const V* __restrict__ xS = (jg > 0) ? xc - g.row : xE;
+    const V* __restrict__ b4 = vv.B4 + 4 * (rb + i);
+    const V* __restrict__ b2 = vv.B2 + 2 * (rb + i);
+    const V* __restrict__ A0 = (KIND == 0 ? fin : vv.r) + rb + i;
+    const V* __restrict__ Pp = (KIND == 1 && fresh ? vv.r : vv.p) + rb + i;
+    const V* __restrict__ Vv = (KIND == 1 && fresh ? vv.r : vv.v) + rb + i;
+    if (KIND == 1 && fresh) beta = 0;
+    V* __restrict__ Fw = (KIND == 1 ? vv.p : vv.s) + rb + i;
+    V* __restrict__ Xw = x + rb + i;
+    const bool need_nbr = !(FIRST && colour == 0);
+    V cur[KB][NA], nxt[KB][NA];
+#pragma unroll
+    for (int e = 0; e < KB; ++e)
+#pragma unroll
+        for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a] = (V)0;
+    auto load = [&](int k0, V(&b)[KB][NA]) {
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const int k = min(k0 + e, nz - 1);
+            const int o = k * nx;
+            if (KIND == 1) b[e][0] = fma(beta, fma(-omega_b, Vv[o], Pp[o]), A0[o]);
+            else if (KIND == 2) b[e][0] = fma(-alpha, Vv[o], A0[o]);
+            else b[e][0] = A0[o];
+            if (!FIRST) {
+                b[e][1] = xc[o];
+                b[e][2] = xc[min(k + 1, nz - 1) * nx];
+            }
+            if (need_nbr) {
+                b[e][3] = xE[o]; b[e][4] = xW[o]; b[e][5] = xN[o]; b[e][6] = xS[o];
+                const VecN<V, 4> h4 = ldv<4>(b4 + 4 * o);
+                b[e][7] = h4.v[0]; b[e][8] = h4.v[1]; b[e][9] = h4.v[2]; b[e][10] = h4.v[3];
+            }
+            const VecN<V, 2> h2 = ldv<2>(b2 + 2 * o);
+            b[e][11] = h2.v[0]; b[e][12] = h2.v[1];
+        }
+    };
+    load(0, cur);
+    V cprev = 0, yprev = 0, xprev = 0;
+    for (int k0 = 0; k0 < nz; k0 += KB) {
+        if (k0 + KB < nz) load(k0 + KB, nxt);
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const int k = k0 + e;
+            if (k < nz) {
+                const V f = cur[e][0];
+                if (FIRST && KIND != 0) Fw[k * nx] = f;
+                V rhs;
+                V hx = 0;
+                if (need_nbr) {
+                    hx = cur[e][7] * cur[e][3];
+                    hx = fma(cur[e][8], cur[e][4], hx);
+                    hx = fma(cur[e][9], cur[e][5], hx);
+                    hx = fma(cur[e][10], cur[e][6], hx);
+                }
+                if (FIRST) {
+                    rhs = om * (f - hx);
+                } else {
+                    V tx = cur[e][1];
+                    tx = fma(cur[e][11], cur[e][2], tx);   // U x(k+1): U = 0 on the top level
+                    tx = fma(cur[e][12], xprev, tx);      // D x(k-1): D = 0 at k = 0
+                    rhs = fma(om1, tx, om * (f - hx));
+                    xprev = cur[e][1];
+                }
+                const V u = cur[e][11], d = cur[e][12];
+                V c, y;
+                if (k == 0) {
+                    c = u;
+                    y = rhs;
+                } else {
+                    const V inv = rcp_fast<V>(fma(-d, cprev, (V)1));
+                    c = u * inv;
+                    y = fma(-d, yprev, rhs) * inv;
+                }
+                cps[k * W + tid] = c;
+                ys[k * W + tid] = y;
+                cprev = c;
+                yprev = y;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < KB; ++e)
+#pragma unroll
+            for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a];
+    }
+    V zn = yprev;
+    Xw[(nz - 1) * nx] = zn;
+    for (int k = nz - 2; k >= 0; --k) {
+        zn = fma(-cps[k * W + tid], zn, ys[k * W + tid]);
+        Xw[k * nx] = zn;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // a4 / a7 / apply: y = Ahat z (unit diagonal + 6 bands; periodic i; absent neighbours contribute 0)
 // DOTS 0: none;  1: sigma = aux . y (aux = rhat0);  2: t.s, t.t, s.s (aux = s).
 // Thread per column walking k.  Loads of KB levels (B4, B2, z centre / E / W / N / S, aux) are

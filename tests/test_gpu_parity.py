@@ -29,6 +29,9 @@ def _vnp(mode):
 def _make(prob, mode):
     bands, b = gen.host(prob)
     bd = torch.from_numpy(bands).cuda()
+    # poison the caching allocator with NaN so that a read of an unwritten workspace element shows up
+    junk = torch.full((4 * 7 * prob.n + (1 << 20),), float("nan"), dtype=torch.float64, device="cuda")
+    del junk
     s = egs.Solver((prob.nx, prob.ny, prob.nz), bd, mode)
     return s, bands, b
 
@@ -244,3 +247,40 @@ def test_fused_phases_match_unfused_schedule(prob, mode, monkeypatch):
     s1.solve(bt, tol=0.0, maxit=3, flags=egs.EG_SOLVE_PROFILE)
     p = s1.profile()
     assert p["phase_A"][1] == 3 and p["phase_B"][1] == 3 and p["thomas_p"][1] == 0
+
+
+TRISOR_CASES = [gen.Problem(64, 48, 10, seed=0), gen.Problem(130, 9, 70, seed=10), gen.Problem(128, 37, 13, seed=11)]
+
+
+@pytest.mark.parametrize("prob", TRISOR_CASES, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("sweeps,omega", [(1, 1.0), (3, 1.5)])
+def test_trisor_precondition_parity(prob, mode, sweeps, omega):
+    """NEXT-1: the GPU red-black tri-SOR sweeps against the oracle's Eq. 7 sweeps."""
+    s, bands, _ = _make(prob, mode)
+    s.set_preconditioner("trisor", sweeps=sweeps, omega=omega)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, _ = oracle.scale(g, bands, mode)
+    f = np.random.default_rng(3).standard_normal(prob.n).astype(_vnp(mode))
+    z = s.precondition(torch.from_numpy(f).cuda()).cpu().numpy().astype(np.float64)
+    zo = oracle.trisor(g, "fp64", ahat, f.astype(np.float64), sweeps=sweeps, omega=omega)
+    assert _rel(z, zo) <= (1e-12 if mode == "fp64" else 1e-5)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_trisor_solve_parity(mode):
+    prob = gen.Problem(64, 48, 20, seed=46, cv=(5.0, 20.0), dl=(1e-3, 1e-2))
+    s, bands, b = _make(prob, mode)
+    s.set_preconditioner("trisor", sweeps=3, omega=1.5)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, diag = oracle.scale(g, bands, mode)
+    tol = 1e-4
+    xo, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=tol, maxit=200, sor_sweeps=3, sor_omega=1.5)
+    x, info, h = s.solve(torch.from_numpy(b).cuda(), tol=tol, maxit=200)
+    assert info.converged and io.converged and abs(info.iters - io.iters) <= 2 and info.true_R < tol
+    assert _rel(x.cpu().numpy(), xo) <= 10 * tol
+    s.set_preconditioner("tridiag")
+    _, info1, _ = s.solve(torch.from_numpy(b).cuda(), tol=tol, maxit=200)
+    assert info.iters < info1.iters      # the paper's preconditioner is the stronger one
+    with pytest.raises(egs.EgError):
+        _make(gen.Problem(65, 4, 4, seed=1), mode)[0].set_preconditioner("trisor")   # odd nx
