@@ -34,3 +34,9 @@ clean:
 	rm -rf $(BUILD) gen/libeggen.so oracle/liboracle.so $(PKG)/libegsolve.so
 
 .PHONY: all clean
+
+# debug build with per-CTA cycle accounting of the fused phase kernels (scripts/march_trace.py)
+trace: $(CSRC) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -DMA_TRACE -Iinclude -I$(NCCL_DIR)/include -shared -o $(BUILD)/libegsolve_trace.so $(PKG)/csrc/egsolve.cu -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib -lcudart 2> $(BUILD)/ptxas_trace.log || (cat $(BUILD)/ptxas_trace.log; false)
+
+.PHONY: trace

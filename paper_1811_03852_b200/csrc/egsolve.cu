@@ -17,7 +17,7 @@
 
 #include "egsolve.h"
 #include "kernels.cuh"
-#include "phase.cuh"
+#include "march.cuh"
 
 using namespace eg;
 
@@ -64,7 +64,7 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L) {
     L->off_xg = o;    o = align_up(o + 2 * row * 8, A);
     L->off_vec = o;   o = align_up(o + 6 * align_up(n * L->vsz, A), A);
     L->off_z = o;     o = align_up(o + 2 * align_up((n + 2 * row) * L->vsz, A), A);
-    L->off_pv = o;    o = align_up(o + (size_t)nyl * L->tiles * sizeof(int), A);  // wavefront ready flags
+    L->off_pv = o;    o = align_up(o + (size_t)nyl * L->tiles * sizeof(int), A);  // ready flags of the fused phases
     // reduction slots per row: 128-column tiles (unfused kernels) or 64-longitude strips (phases)
     L->off_slots = o; o = align_up(o + 3 * (size_t)nyl * L->tiles * 8, A);
     L->off_gsum = o;  o = align_up(o + 2 * 8 * 3 * 8, A);
@@ -97,9 +97,11 @@ struct eg_solver {
     double* xg = nullptr;  // [2][row] ghost rows of x (X-typed)
     void* vec[6]{};        // r, rh, p, v, s, t
     void* zext[2]{};       // ghosted z, zs (row -1 .. nyl)
-    int* wave_flags = nullptr;  // [nyl][tiles] ready flags of the wavefront phase kernels
-    bool use_wave = false;      // fused wavefront phases (fp32 working precision, one GPU)
-    int wave_ctas = 0;
+    int* ready_flags = nullptr;  // [nyl][tiles] ready flags of the fused (marching) phase kernels
+    bool use_march = false;     // fused phases (fp32 working precision, one GPU; march.cuh)
+    MarchGeo mg{};
+    MarchMaps maps{};
+    size_t smem_march = 0;
     int epoch_base = 1;         // first epoch of the next solve (flags are never reset)
     int precond = EG_PRECOND_TRIDIAG;  // NEXT-1: EG_PRECOND_TRISOR selects red-black tri-SOR
     int sor_sweeps = 3;
@@ -271,20 +273,22 @@ int finalize(eg_solver* s, int first, int tiles = 0) {
 }
 
 // -------- the iteration (rows a3-a10) --------
+// fused schedule: phase A (a3 + a4), phase B (a6 + a7), update (a9), three finalisers
 template <int MODE>
 int iteration_fused(eg_solver* s, void* x_it) {
     Vecs<MODE> v = vecs<MODE>(s, x_it);
     int rc;
     if constexpr (MODE != 0) {
+        const unsigned grid = (unsigned)(s->mg.strips * s->L.tiles);
         {
             ProfScope ps(s, KID_PHASE_A);
-            k_wave<MODE, 1><<<s->wave_ctas, WAVE_THREADS, s->smem_tm, s->st>>>(s->geo, v, s->wave_flags);
+            k_march<MODE, 1><<<grid, MA_THREADS, s->smem_march, s->st>>>(s->geo, v, s->mg, s->ready_flags, s->maps);
             CK(cudaGetLastError());
         }
         if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
         {
             ProfScope ps(s, KID_PHASE_B);
-            k_wave<MODE, 2><<<s->wave_ctas, WAVE_THREADS, s->smem_tm, s->st>>>(s->geo, v, s->wave_flags);
+            k_march<MODE, 2><<<grid, MA_THREADS, s->smem_march, s->st>>>(s->geo, v, s->mg, s->ready_flags, s->maps);
             CK(cudaGetLastError());
         }
         if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
@@ -356,7 +360,7 @@ template <int MODE>
 int iteration(eg_solver* s, void* x_it) {
     using V = typename Prec<MODE>::V;
     if (s->precond == EG_PRECOND_TRISOR) return iteration_trisor<MODE>(s, x_it);
-    if (s->use_wave) return iteration_fused<MODE>(s, x_it);
+    if (s->use_march) return iteration_fused<MODE>(s, x_it);
     Vecs<MODE> v = vecs<MODE>(s, x_it);
     const dim3 gt((unsigned)((s->grid.nx + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
@@ -511,10 +515,10 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     h->restart_every = prm->restart_every;
     h->eps_v = MODE == 0 ? 0x1.0p-53 : 0x1.0p-24;
     h->omega = h->omega_v = 1.0;
-    // wavefront flags are stamped with epochs that only ever grow: reserve this solve's range
+    // ready flags are stamped with epochs that only ever grow: reserve this solve's range
     // (at most ~5 finalisers per iteration) and wrap around with a flag reset well before overflow
     if (s->epoch_base > (1 << 30)) {
-        CK(cudaMemsetAsync(s->wave_flags, 0, (size_t)s->L.nyl * s->L.tiles * sizeof(int), s->st));
+        CK(cudaMemsetAsync(s->ready_flags, 0, (size_t)s->L.nyl * s->L.tiles * sizeof(int), s->st));
         s->epoch_base = 1;
     }
     h->epoch = s->epoch_base;
@@ -708,6 +712,39 @@ int set_thomas_smem(eg_solver* s) {
     return rc;
 }
 
+// TMA tensor maps of the arrays the fused phases stream ([nyl][nz][nx] views, 128 x MA_KB x 1 boxes)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool encode_map(EncodeTiledFn enc, CUtensorMap* m, void* base, int64_t inner, int64_t nz, int64_t nyl, int esz,
+                int box0) {
+    const cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)nz, (cuuint64_t)nyl};
+    const cuuint64_t strides[2] = {(cuuint64_t)(inner * esz), (cuuint64_t)(inner * nz * esz)};
+    const cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)MA_KB, 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_march_maps(eg_solver* s) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return false;
+    EncodeTiledFn enc = (EncodeTiledFn)fn;
+    const int64_t nx = s->grid.nx, nz = s->grid.nz, nyl = s->L.nyl;
+    bool ok = encode_map(enc, &s->maps.r, s->vec[0], nx, nz, nyl, 4, 128);
+    ok = ok && encode_map(enc, &s->maps.rh, s->vec[1], nx, nz, nyl, 4, 128);
+    ok = ok && encode_map(enc, &s->maps.p, s->vec[2], nx, nz, nyl, 4, 128);
+    ok = ok && encode_map(enc, &s->maps.v, s->vec[3], nx, nz, nyl, 4, 128);
+    ok = ok && encode_map(enc, &s->maps.b2, s->B2, nx, nz, nyl, 8, 128);       // (U, D) as one 8-byte element
+    ok = ok && encode_map(enc, &s->maps.b4, s->B4, 2 * nx, nz, nyl, 8, 256);   // (E, W), (N, S)
+    return ok;
+}
+
 bool valid_dist(const eg_grid* g, const eg_dist* d, int64_t* jb, int64_t* je, int* rank, int* nranks) {
     if (!d) { *jb = 0; *je = g->ny; *rank = 0; *nranks = 1; return true; }
     *jb = d->j_begin; *je = d->j_end; *rank = d->rank; *nranks = d->nranks;
@@ -777,7 +814,7 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     for (int d = 0; d < 6; ++d) s->vec[d] = s->ws + L.off_vec + (size_t)d * align_up(L.n * L.vsz, 256);
     for (int d = 0; d < 2; ++d)
         s->zext[d] = s->ws + L.off_z + (size_t)d * align_up((L.n + 2 * L.row) * L.vsz, 256);
-    s->wave_flags = (int*)(s->ws + L.off_pv);
+    s->ready_flags = (int*)(s->ws + L.off_pv);
     s->slots = (double*)(s->ws + L.off_slots);
     s->gsum = (double*)(s->ws + L.off_gsum);
     s->gall = s->gsum + 8 * 3;
@@ -823,28 +860,44 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         if (rc == EG_OK && r == ncclSuccess) r = ncclCommInitRank(&s->comm, s->nranks, id, s->rank);
         if (r != ncclSuccess) rc = fail(s, EG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
     }
-    if (rc == EG_OK) {  // fused wavefront phases: fp32 vectors, one GPU, TMEM Thomas available
-        // opt-in (EG_WAVE=1): on B200 it is slower than the tuned 5-kernel schedule because ~600
-        // resident 128x70-point work items stream ~130 MB between writing a z row and reading it
-        // back, more than L2 holds (DESIGN.md §Fused phases)
-        const char* wv = getenv("EG_WAVE");
+    if (rc == EG_OK) {  // fused marching phases (march.cuh): fp32 vectors, one GPU; EG_NO_FUSE=1 disables
         const char* nf = getenv("EG_NO_FUSE");
         int dev = 0, nsm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        s->wave_ctas = 4 * nsm;
-        // deadlock freedom needs more resident CTAs than tiles per row (phase.cuh)
-        s->use_wave = s->use_tm && s->comm == nullptr && 2 * s->L.tiles < s->wave_ctas && wv && wv[0] == '1' &&
-                      !(nf && nf[0] == '1');
-        if (s->use_wave) {
+        const int64_t nz8 = (grid->nz + MA_KB - 1) / MA_KB * MA_KB;
+        const size_t ring = 3 * (size_t)nz8 * MA_RING_W * sizeof(float);
+        const size_t budget = 227 * 1024 - 2048 - 128;  // dynamic + static shared memory per CTA
+        auto stages_for = [&](size_t stage_bytes) {
+            return (int)std::min<size_t>(MA_MAX_STAGES, ring < budget ? (budget - ring) / stage_bytes : 0);
+        };
+        const int sa = stages_for(ma_stage_bytes(1)), sb = stages_for(ma_stage_bytes(2));
+        s->use_march = s->use_tm && s->comm == nullptr && grid->nx % 4 == 0 && 7 * nz8 <= 512 &&
+                       s->L.tiles <= nsm && sa >= 3 && !(nf && nf[0] == '1');
+        if (s->use_march) {
+            s->mg.stages_a = sa;
+            s->mg.stages_b = sb;
+            s->mg.strips = (int)std::min<int64_t>(s->L.nyl, nsm / s->L.tiles);
+            const char* fs = getenv("EG_MARCH_STRIPS");  // tests: fewer, longer strips
+            if (fs && atoi(fs) >= 1) s->mg.strips = std::min(s->mg.strips, atoi(fs));
+            // at least ~116 KB so that exactly one CTA (and one 512-column TMEM allocation) fits an SM
+            s->smem_march = std::max<size_t>(std::max((size_t)sa * ma_stage_bytes(1), (size_t)sb * ma_stage_bytes(2)) + ring + 128,
+                                             116 * 1024);
             cudaError_t e1 = prec == EG_MIXED
-                ? cudaFuncSetAttribute(k_wave<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm)
-                : cudaFuncSetAttribute(k_wave<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm);
+                ? cudaFuncSetAttribute(k_march<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_march)
+                : cudaFuncSetAttribute(k_march<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_march);
             cudaError_t e2 = prec == EG_MIXED
-                ? cudaFuncSetAttribute(k_wave<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm)
-                : cudaFuncSetAttribute(k_wave<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm);
-            cudaError_t e3 = cudaMemsetAsync(s->wave_flags, 0, (size_t)s->L.nyl * s->L.tiles * sizeof(int), s->st);
-            if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) rc = fail(s, EG_ERR_CUDA, "wave setup");
+                ? cudaFuncSetAttribute(k_march<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_march)
+                : cudaFuncSetAttribute(k_march<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_march);
+            int occ = 0;
+            cudaError_t e3 = prec == EG_MIXED
+                ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_march<1, 2>, MA_THREADS, s->smem_march)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_march<2, 2>, MA_THREADS, s->smem_march);
+            cudaError_t e4 = cudaMemsetAsync(s->ready_flags, 0, (size_t)s->L.nyl * s->L.tiles * sizeof(int), s->st);
+            if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess)
+                rc = fail(s, EG_ERR_CUDA, "march setup: %s", cudaGetErrorString(cudaGetLastError()));
+            else if (occ != 1 || !make_march_maps(s))  // co-residency of every CTA makes the flag waits safe
+                s->use_march = false;
         }
     }
     if (rc == EG_OK)
@@ -978,6 +1031,13 @@ int eg_profile_get(const eg_solver* s, int kid, double* total_ms, int64_t* launc
     }
     return EG_OK;
 }
+
+#ifdef MA_TRACE
+// debug builds only (not declared in include/egsolve.h): per-CTA cycle counters of the last march
+int eg_debug_march_trace(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_ma_trace, (size_t)n * sizeof(unsigned long long)) == cudaSuccess ? 0 : EG_ERR_CUDA;
+}
+#endif
 
 int eg_profile_reset(eg_solver* s) {
     if (!s) return EG_ERR_ARG;

@@ -1079,7 +1079,7 @@ __global__ void __launch_bounds__(1024) k_fin(Geo g, const double* __restrict__ 
                                               double* __restrict__ gsum, int first) {
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
     const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
-    if (threadIdx.x == 0) { st->epoch += 1; st->wave_ctr = 0; }  // for the next wavefront launch
+    if (threadIdx.x == 0) { st->epoch += 1; }  // stamps the next fused phase launch
     if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;
     if (WHICH == W_C && st->sexit) {  // s-step exit: no sums needed
         if (threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gsum, st, first);
@@ -1103,7 +1103,7 @@ __global__ void __launch_bounds__(1024) k_fin_groups(Geo g, const double* __rest
 
 template <int MODE, int WHICH>
 __global__ void k_fin_logic(Geo g, const double* __restrict__ gall, DevState* st, int first) {
-    if (threadIdx.x == 0) { st->epoch += 1; st->wave_ctr = 0; }
+    if (threadIdx.x == 0) { st->epoch += 1; }
     if (threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gall, st, first);
 }
 

@@ -65,7 +65,7 @@ def test_precondition_parity(prob, mode):
     assert _rel(z, zo) <= (1e-12 if mode == "fp64" else 1e-5)
 
 
-FUSED_ODD = gen.Problem(128, 37, 13, seed=11)   # fused phase path (nx % 64 == 0), odd ny / nz
+FUSED_ODD = gen.Problem(128, 37, 13, seed=11)   # one 128-column tile, odd ny / nz
 FUSED_THIN = gen.Problem(192, 3, 70, seed=12)   # fewer rows than the per-CTA row ranges
 
 
@@ -224,29 +224,39 @@ def test_multirank_finaliser_path_bitwise_equal(mode, monkeypatch):
     assert torch.equal(y1, y2)
 
 
-@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], FUSED_ODD, FUSED_THIN, gen.CONFIGS["C2"]],
-                         ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+MARCH_CASES = [gen.CONFIGS["C1"], RAGGED, FUSED_ODD, FUSED_THIN, gen.CONFIGS["C2"],
+               gen.Problem(388, 23, 70, seed=13)]   # 4 tiles (last one 4 columns wide), nz = 70
+
+
+@pytest.mark.parametrize("prob", MARCH_CASES, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
 @pytest.mark.parametrize("mode", ["mixed", "fp32"])
-def test_fused_phases_match_unfused_schedule(prob, mode, monkeypatch):
-    """The opt-in fused wavefront phase kernels (EG_WAVE=1: Thomas + stencil per work item) compute
-    z, v, s, t with the same operations as the 5-kernel schedule and the same reduction slots, so
-    the solve is bitwise identical."""
+@pytest.mark.parametrize("strips", [None, 1, 2, 3])
+def test_fused_phases_match_unfused_schedule(prob, mode, strips, monkeypatch):
+    """The fused marching phase kernels (march.cuh: Thomas + stencil of a latitude strip per CTA,
+    the default for fp32 vectors on one GPU) compute z, v, s, t with the same operations as the
+    5-kernel schedule (EG_NO_FUSE=1) and write the same reduction slots, so the solve is bitwise
+    identical, whatever the number of strips (EG_MARCH_STRIPS: one-row strips, one strip per tile
+    column, odd counts whose strips alternate direction)."""
     bands, b = gen.host(prob)
     g = (prob.nx, prob.ny, prob.nz)
     bd = torch.from_numpy(bands).cuda()
     bt = torch.from_numpy(b).cuda()
-    monkeypatch.setenv("EG_WAVE", "1")
+    if strips is not None:
+        monkeypatch.setenv("EG_MARCH_STRIPS", str(strips))
     s1 = egs.Solver(g, bd, mode)
-    monkeypatch.delenv("EG_WAVE")
+    monkeypatch.delenv("EG_MARCH_STRIPS", raising=False)
+    monkeypatch.setenv("EG_NO_FUSE", "1")
     s2 = egs.Solver(g, bd, mode)
+    monkeypatch.delenv("EG_NO_FUSE")
     for tol, maxit in ((0.0, 8), (1e-5, 100)):
         x1, i1, h1 = s1.solve(bt, tol=tol, maxit=maxit)
         x2, i2, h2 = s2.solve(bt, tol=tol, maxit=maxit)
         assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
-    s1.profile_reset()
-    s1.solve(bt, tol=0.0, maxit=3, flags=egs.EG_SOLVE_PROFILE)
-    p = s1.profile()
-    assert p["phase_A"][1] == 3 and p["phase_B"][1] == 3 and p["thomas_p"][1] == 0
+    for s, fused in ((s1, True), (s2, False)):
+        s.profile_reset()
+        s.solve(bt, tol=0.0, maxit=3, flags=egs.EG_SOLVE_PROFILE)
+        p = s.profile()
+        assert (p["phase_A"][1], p["phase_B"][1], p["thomas_p"][1]) == ((3, 3, 0) if fused else (0, 0, 3))
 
 
 TRISOR_CASES = [gen.Problem(64, 48, 10, seed=0), gen.Problem(130, 9, 70, seed=10), gen.Problem(128, 37, 13, seed=11)]
