@@ -868,21 +868,23 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         const int64_t nz8 = (grid->nz + MA_KB - 1) / MA_KB * MA_KB;
         const size_t ring = 3 * (size_t)nz8 * MA_RING_W * sizeof(float);
         const size_t budget = 227 * 1024 - 2048 - 128;  // dynamic + static shared memory per CTA
-        auto stages_for = [&](size_t stage_bytes) {
-            return (int)std::min<size_t>(MA_MAX_STAGES, ring < budget ? (budget - ring) / stage_bytes : 0);
-        };
-        const int sa = stages_for(ma_stage_bytes(1)), sb = stages_for(ma_stage_bytes(2));
-        s->use_march = s->use_tm && s->comm == nullptr && grid->nx % 4 == 0 && 7 * nz8 <= 512 &&
-                       s->L.tiles <= nsm && sa >= 3 && !(nf && nf[0] == '1');
+        // two stage rings (elimination / stencil inputs) share what the z ring leaves
+        const int na = ring < budget ? (int)((budget - ring) / ma_stage_bytes(1)) : 0;
+        const int nb = ring < budget ? (int)((budget - ring) / ma_stage_bytes(2)) : 0;
+        s->use_march = s->use_tm && s->comm == nullptr && grid->nx % 4 == 0 && nz8 <= 8 * MA_MAX_CH &&
+                       7 * nz8 <= 512 && s->L.tiles <= nsm && na >= 4 && !(nf && nf[0] == '1');
         if (s->use_march) {
-            s->mg.stages_a = sa;
-            s->mg.stages_b = sb;
+            s->mg.fst_a = std::min(MA_MAX_STAGES, na - na / 2);
+            s->mg.sst_a = std::min(MA_MAX_STAGES, na / 2);
+            s->mg.fst_b = std::min(MA_MAX_STAGES, nb - nb / 2);
+            s->mg.sst_b = std::min(MA_MAX_STAGES, nb / 2);
             s->mg.strips = (int)std::min<int64_t>(s->L.nyl, nsm / s->L.tiles);
             const char* fs = getenv("EG_MARCH_STRIPS");  // tests: fewer, longer strips
             if (fs && atoi(fs) >= 1) s->mg.strips = std::min(s->mg.strips, atoi(fs));
             // at least ~116 KB so that exactly one CTA (and one 512-column TMEM allocation) fits an SM
-            s->smem_march = std::max<size_t>(std::max((size_t)sa * ma_stage_bytes(1), (size_t)sb * ma_stage_bytes(2)) + ring + 128,
-                                             116 * 1024);
+            const size_t st_a = (size_t)(s->mg.fst_a + s->mg.sst_a) * ma_stage_bytes(1);
+            const size_t st_b = (size_t)(s->mg.fst_b + s->mg.sst_b) * ma_stage_bytes(2);
+            s->smem_march = std::max<size_t>(std::max(st_a, st_b) + ring + 128, 116 * 1024);
             cudaError_t e1 = prec == EG_MIXED
                 ? cudaFuncSetAttribute(k_march<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_march)
                 : cudaFuncSetAttribute(k_march<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_march);

@@ -37,9 +37,9 @@ namespace eg {
 
 constexpr int MA_KB = 8;                               // levels per stage
 constexpr int MA_CONS = 128;                           // consumer threads: one column each
-constexpr int MA_THREADS = MA_CONS + 64;               // + a producer and a publisher warp
-// stage = one MA_KB-level chunk: phase A: r, p, v, (U,D) or (E,W,N,S), rhat0 (640 floats / level);
-// phase B: r, v, (U,D) or (E,W,N,S) (512 floats / level)
+constexpr int MA_THREADS = 2 * MA_CONS + 64;           // stencil + Thomas warps, producer, publisher
+// stage = one MA_KB-level chunk of one row.  Elimination ring: r, (p,) v, (U, D); stencil ring:
+// (E, W, N, S) (, rhat0): 640 floats / level in phase A, 512 in phase B, for both rings
 constexpr int ma_stage_floats(int kind) { return MA_KB * (kind == 1 ? 640 : 512); }
 constexpr int ma_stage_bytes(int kind) { return 4 * ma_stage_floats(kind); }
 constexpr int MA_MAX_STAGES = 8;
@@ -53,7 +53,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // stencil warps
 __device__ __forceinline__ int ld_volatile(const int* p) {
     int v;
     asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -178,27 +178,31 @@ __device__ unsigned long long g_ma_trace[1024 * 16];
 #endif
 
 struct MarchGeo {
-    int strips;            // latitude strips; grid = strips * tiles CTAs
-    int stages_a, stages_b;  // pipeline depth of phase A / phase B
+    int strips;                  // latitude strips; grid = strips * tiles CTAs
+    int fst_a, sst_a;            // phase A: stages of the elimination / stencil input rings
+    int fst_b, sst_b;            // phase B
 };
+constexpr int MA_MAX_CH = 9;     // chunks per column (nz <= 72)
 
-// KIND 1: phase A, KIND 2: phase B.  grid strips*tiles, block MA_THREADS (4 consumer warps, a TMA
-// producer warp, a publisher warp), dynamic shared memory stages*20 KB + 3*ceil8(nz)*130*4 B + 128 B
+// KIND 1: phase A, KIND 2: phase B.  grid strips*tiles, block MA_THREADS: warps 0-3 stencil (S),
+// warps 4-7 Thomas (F; warp 4+w shares TMEM lanes, i.e. columns, with S warp w), warp 8 TMA producer,
+// warp 9 publisher.  Dynamic shared memory: the two stage rings + 3*ceil8(nz)*130*4 B z ring + 128 B
 // of alignment slack (padded so that only one CTA fits an SM).
 //
-// Consumer schedule of a strip r_0, r_1, ..., r_{L-1} (r_{-1}, r_L: the neighbouring strips' rows):
-//   prologue:   T(r_0), T(r_1)                           T = forward elimination + back substitution
-//   step m:     for each MA_KB-level chunk: stencil(r_m) chunk, then elimination(r_{m+2}) chunk
-//               [the two are independent: the elimination's latency-bound recurrence interleaves
-//               with the stencil's streaming arithmetic]; back substitution of r_{m+2}
+// Schedule of a strip r_0, r_1, ..., r_{L-1} (r_{-1}, r_L: the neighbouring strips' rows):
+//   F: T(r_0), T(r_1), then per step m: elimination(r_{m+2}) chunk by chunk, back substitution
+//   S: per step m: [wait z(r_{m+1})] stencil(r_m) chunk by chunk, dot partials
+//   (T = forward elimination + back substitution)
 // Ring slot x % 3 holds z(r_x); TMEM slot x & 1 holds U, D (and s) of r_x.  The elimination of
-// r_{m+2} overwrites, level by level and in the same thread, exactly the ring entries (z(r_{m-1}),
-// own column) and TMEM entries (row r_m) that the stencil of r_m has just read.
+// r_{m+2} overwrites, level by level and column by column, exactly the ring entries (z(r_{m-1})) and
+// TMEM entries (row r_m) that the stencil of r_m reads in the same chunk: the F warps store a chunk
+// only after the S warps have read it (mbarrier sread[chunk], one phase per step).  The S warps
+// start step m+1 only when F has finished z(r_{m+2}) (mbarrier zready[x & 1]).
 // Levels are padded to a multiple of MA_KB: the TMA zero-fills levels >= nz, which the elimination
 // turns into c' = y = z = 0 (m = 1), so every chunk is branch-free; global stores are masked.
-// The publisher warp turns "z(r_x) stored" (an mbarrier the consumer warps arrive on) into the
-// ready flag with a gpu-scope release, keeping the fence latency off the consumers' path; halo
-// columns of r_{m+1} are fetched in the middle of step m, one step before they are needed.
+// The publisher warp turns "z(r_x) stored" (mbarrier zdone) into the ready flag with a gpu-scope
+// release, keeping the fence latency off the compute warps; halo columns of r_{m+1} are fetched
+// late in step m, one step before they are needed.
 template <int MODE, int KIND>
 __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, MarchGeo mg, int* __restrict__ flags,
                                                             const __grid_constant__ MarchMaps maps) {
@@ -206,8 +210,13 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     using V = float;
     constexpr int NQ = KIND == 1 ? 1 : 3;
     constexpr int KB = MA_KB;
+    constexpr int SF = ma_stage_floats(KIND);
+    constexpr int OFF_V = (KIND == 1 ? 2 : 1) * MA_KB * 128;   // v after r (, p)
+    constexpr int OFF_B2 = (KIND == 1 ? 3 : 2) * MA_KB * 128;  // (U, D) after r, (p,) v
     extern __shared__ __align__(128) unsigned char smraw[];
-    __shared__ __align__(8) uint64_t full[MA_MAX_STAGES], empty[MA_MAX_STAGES], zdone[2];
+    __shared__ __align__(8) uint64_t fullF[MA_MAX_STAGES], emptyF[MA_MAX_STAGES];
+    __shared__ __align__(8) uint64_t fullS[MA_MAX_STAGES], emptyS[MA_MAX_STAGES];
+    __shared__ __align__(8) uint64_t sread[MA_MAX_CH], zready[2], zdone[2];
     __shared__ uint32_t tm_slot;
     __shared__ double red[32 * 3];
     DevState* st = vv.st;
@@ -223,9 +232,8 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nx = (int)g.nx, nz = (int)g.nz, nyl = (int)g.nyl;
-    constexpr int SF = ma_stage_floats(KIND);
-    constexpr int OFF_B2 = (KIND == 1 ? 3 : 2) * MA_KB * 128;  // (U, D) after r, (p,) v
-    const int T = g.tiles, NS = KIND == 1 ? mg.stages_a : mg.stages_b;
+    const int T = g.tiles;
+    const int NSF = KIND == 1 ? mg.fst_a : mg.fst_b, NSS = KIND == 1 ? mg.sst_a : mg.sst_b;
     const int t = blockIdx.x % T, strip = blockIdx.x / T;
     const int ja = (int)((int64_t)strip * nyl / mg.strips), jb = (int)((int64_t)(strip + 1) * nyl / mg.strips);
     const int L = jb - ja;
@@ -236,14 +244,16 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     const int nch = (nz + KB - 1) / KB;
     const int NZ8 = nch * KB;
     // TMA destinations must be 128-byte aligned; the dynamic region follows the static one
-    float* stages = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
-    float* ring = stages + (size_t)NS * SF;  // [3][NZ8][130]
+    float* stF = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    float* stS = stF + (size_t)NSF * SF;
+    float* ring = stS + (size_t)NSS * SF;  // [3][NZ8][130]
     const int ring_slot = NZ8 * MA_RING_W;
 
     if (tid == 0) {
-        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MA_CONS / 32); }
-        mbar_init(&zdone[0], MA_CONS / 32);
-        mbar_init(&zdone[1], MA_CONS / 32);
+        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], 4); }
+        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], 4); }
+        for (int c = 0; c < MA_MAX_CH; ++c) mbar_init(&sread[c], 4);
+        for (int b = 0; b < 2; ++b) { mbar_init(&zready[b], 4); mbar_init(&zdone[b], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const uint32_t tbase = tm_alloc512(&tm_slot);  // contains __syncthreads()
@@ -254,37 +264,34 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     MA_CLK(t_all);
 
     // ------------------------------------------------------------------ producer warp
-    if (warp == MA_CONS / 32) {
+    if (warp == 8) {
         if (lane == 0 && L > 0) {
-            int slot = 0, round = 0;  // stage ring position (no runtime divisions in the loop)
-            auto acquire = [&](uint32_t bytes) -> float* {
-                MA_CLK(t0);
-                if (round > 0) mbar_wait_sleep(&empty[slot], (uint32_t)((round - 1) & 1), 32);
-                MA_ADD(9, t0);
-                mbar_expect_tx(&full[slot], bytes);
-                return stages + (size_t)slot * SF;
-            };
-            auto advance = [&]() {
-                if (++slot == NS) { slot = 0; ++round; }
-            };
+            int fslot = 0, fround = 0, sslot = 0, sround = 0;
             // elimination inputs of row jr, levels k0..k0+7: r, (p, v) or v, (U, D)
             auto fwd_stage = [&](int jr, int k0) {
-                const uint32_t bytes = (KIND == 1 ? (fresh ? 1u : 3u) : 2u) * MA_BOX_V + MA_BOX_B2;
-                float* sb = acquire(bytes);
-                uint64_t* fb = &full[slot];
+                MA_CLK(t0);
+                if (fround > 0) mbar_wait_sleep(&emptyF[fslot], (uint32_t)((fround - 1) & 1), 32);
+                MA_ADD(9, t0);
+                uint64_t* fb = &fullF[fslot];
+                mbar_expect_tx(fb, (KIND == 1 ? (fresh ? 1u : 3u) : 2u) * MA_BOX_V + MA_BOX_B2);
+                float* sb = stF + (size_t)fslot * SF;
                 tma3(sb, &maps.r, i0, k0, jr, fb);
                 if (KIND == 1 && !fresh) tma3(sb + KB * 128, &maps.p, i0, k0, jr, fb);
-                if (KIND == 2 || !fresh) tma3(sb + (KIND == 1 ? 2 : 1) * KB * 128, &maps.v, i0, k0, jr, fb);
+                if (KIND == 2 || !fresh) tma3(sb + OFF_V, &maps.v, i0, k0, jr, fb);
                 tma3(sb + OFF_B2, &maps.b2, i0, k0, jr, fb);
-                advance();
+                if (++fslot == NSF) { fslot = 0; ++fround; }
             };
             // stencil inputs of row jr: (E, W, N, S), rhat0 (phase A)
             auto sten_stage = [&](int jr, int k0) {
-                float* sb = acquire(MA_BOX_B4 + (KIND == 1 ? MA_BOX_V : 0u));
-                uint64_t* fb = &full[slot];
+                MA_CLK(t0);
+                if (sround > 0) mbar_wait_sleep(&emptyS[sslot], (uint32_t)((sround - 1) & 1), 32);
+                MA_ADD(9, t0);
+                uint64_t* fb = &fullS[sslot];
+                mbar_expect_tx(fb, MA_BOX_B4 + (KIND == 1 ? MA_BOX_V : 0u));
+                float* sb = stS + (size_t)sslot * SF;
                 tma3(sb, &maps.b4, 2 * i0, k0, jr, fb);
                 if (KIND == 1) tma3(sb + KB * 512, &maps.rh, i0, k0, jr, fb);
-                advance();
+                if (++sslot == NSS) { sslot = 0; ++sround; }
             };
             for (int c = 0; c < nch; ++c) fwd_stage(row_of(0), c * KB);
             if (L >= 2)
@@ -301,10 +308,10 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             for (int q = 9; q < 11; ++q) g_ma_trace[blockIdx.x * 16 + q] = tr[q];
         }
 #endif
-        return;  // the consumers keep the CTA (and its TMEM) alive until every stage has landed
+        return;  // the compute warps keep the CTA (and its TMEM) alive until every stage has landed
     }
     // ------------------------------------------------------------------ publisher warp
-    if (warp == MA_CONS / 32 + 1) {
+    if (warp == 9) {
         if (lane == 0)
             for (int x = 0; x < L; ++x) {
                 mbar_wait_sleep(&zdone[x & 1], (uint32_t)((x >> 1) & 1), 256);
@@ -313,292 +320,297 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
         return;
     }
 
-    // ------------------------------------------------------------------ consumer warps
-    const bool act = tid < w;
-    const bool uni = w == 128;  // every consumer lane owns a column (all tiles but a ragged last one)
-    const int i = i0 + (act ? tid : w - 1);  // inactive lanes compute on zero-filled data, never store
-    const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+    // ------------------------------------------------------------------ compute warps (S and F)
+    const bool isF = warp >= 4;
+    const int col = tid & 127;
+    const bool act = col < w;
+    const bool uni = w == 128;  // every lane owns a column (all tiles but a ragged last one)
+    const int i = i0 + (act ? col : w - 1);  // inactive lanes compute on zero-filled data, never store
+    const uint32_t tl = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     // TMEM column map (per lane = per column): c' | U(2 slots) | D(2 slots) | s(2 slots, phase B)
     auto tU = [&](int slot) { return tl + (uint32_t)(NZ8 + slot * 2 * NZ8); };
     auto tD = [&](int slot) { return tl + (uint32_t)(NZ8 + slot * 2 * NZ8 + NZ8); };
     auto tS = [&](int slot) { return tl + (uint32_t)(5 * NZ8 + slot * NZ8); };
-    V* __restrict__ Pw = KIND == 1 ? vv.p : vv.s;
     V* __restrict__ Zw = KIND == 1 ? vv.z : vv.zs;
-    V* __restrict__ Yw = KIND == 1 ? vv.v : vv.t;
-    const int64_t per_q = (int64_t)nyl * T;
-    const int iWg = (i0 == 0) ? nx - 1 : i0 - 1;       // W halo column (tile t-1, periodic)
-    const int iEg = (i0 + w == nx) ? 0 : i0 + w;        // E halo column (tile t+1, periodic)
-    const int tW = (t == 0) ? T - 1 : t - 1, tE = (t + 1 == T) ? 0 : t + 1;
     auto slot_ptr = [&](int x) { return ring + (size_t)(((x % 3) + 3) % 3) * ring_slot; };
-    int cslot = 0;
-    uint32_t cphase = 0;  // stage ring position of the consumers
-    auto stage_wait = [&](int& taken) -> const float* {
-        taken = cslot;
-        MA_CLK(t0);
-        mbar_wait(&full[cslot], cphase);
-        MA_ADD(2, t0);
-        const float* sb = stages + (size_t)cslot * SF;
-        if (++cslot == NS) { cslot = 0; cphase ^= 1u; }
-        return sb;
-    };
-    auto stage_release = [&](int taken) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[taken]);
-    };
 
-    // forward elimination of one chunk of row jr (inputs in stage sb): f = update, Thomas factors;
-    // y -> ring (own column), c' / U / D / s -> TMEM slot us, f -> HBM (p or s)
-    V cprev = 0.f, yprev = 0.f;
-    auto fwd_chunk = [&](const float* sb, int k0, float* zr, V* pw, int us) {
-        float rr[KB], pp[KB], vq[KB], uu[KB], dd[KB];
-#pragma unroll
-        for (int e = 0; e < KB; ++e) {
-            rr[e] = sb[e * 128 + tid];
-            if (KIND == 1) pp[e] = fresh ? rr[e] : sb[KB * 128 + e * 128 + tid];
-            vq[e] = (KIND == 1 && fresh) ? rr[e] : sb[(KIND == 1 ? 2 : 1) * KB * 128 + e * 128 + tid];
-            const float2 ud = *reinterpret_cast<const float2*>(sb + OFF_B2 + e * 256 + 2 * tid);
-            uu[e] = ud.x;
-            dd[e] = ud.y;
-        }
-        float cb[KB], yb[KB], fb[KB];
-#pragma unroll
-        for (int e = 0; e < KB; ++e) {
-            const int k = k0 + e;
-            const V f = KIND == 1 ? fmaf(beta, fmaf(-omega, vq[e], pp[e]), rr[e]) : fmaf(-alpha, vq[e], rr[e]);
-            const V inv = rcp_fast<V>(fmaf(-dd[e], cprev, 1.f));
-            const V c = k == 0 ? uu[e] : uu[e] * inv;
-            const V y = k == 0 ? f : fmaf(-dd[e], yprev, f) * inv;
-            cb[e] = c; yb[e] = y; fb[e] = f;
-            cprev = c;
-            yprev = y;
-        }
-        V* pk = pw + (int64_t)k0 * nx;
-        if (uni && k0 + KB <= nz) {  // warp-uniform: a full chunk of a full tile
-#pragma unroll
-            for (int e = 0; e < KB; ++e) pk[e * nx] = fb[e];
-        } else {
-#pragma unroll
-            for (int e = 0; e < KB; ++e)
-                if (act && k0 + e < nz) pk[e * nx] = fb[e];
-        }
-#pragma unroll
-        for (int e = 0; e < KB; ++e) zr[(k0 + e) * MA_RING_W] = yb[e];
-        tm_st8(tl + (uint32_t)k0, cb);
-        tm_st8(tU(us) + (uint32_t)k0, uu);
-        tm_st8(tD(us) + (uint32_t)k0, dd);
-        if (KIND == 2) tm_st8(tS(us) + (uint32_t)k0, fb);
-    };
-    // back substitution of the row whose y sits in ring row zr: z -> ring (in place) and HBM
-    auto back_row = [&](float* zr, V* zw) {
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        V zn = 0.f;  // z(NZ8) = 0; padded levels have c' = y = 0
-        for (int k0 = NZ8 - KB; k0 >= 0; k0 -= KB) {
-            float cb[KB], yb[KB];
-            tm_ld8_nw(tl + (uint32_t)k0, cb);
-#pragma unroll
-            for (int e = 0; e < KB; ++e) yb[e] = zr[(k0 + e) * MA_RING_W];
-            tm_wait_ld();
-#pragma unroll
-            for (int e = KB - 1; e >= 0; --e) {
-                zn = fmaf(-cb[e], zn, yb[e]);
-                yb[e] = zn;
-            }
-#pragma unroll
-            for (int e = 0; e < KB; ++e) zr[(k0 + e) * MA_RING_W] = yb[e];
-            V* zk = zw + (int64_t)k0 * nx;
-            if (uni && k0 + KB <= nz) {
-#pragma unroll
-                for (int e = 0; e < KB; ++e) zk[e * nx] = yb[e];
-            } else {
-#pragma unroll
-                for (int e = 0; e < KB; ++e)
-                    if (act && k0 + e < nz) zk[e * nx] = yb[e];
-            }
-        }
-    };
-    auto fwd_row = [&](int x) {  // prologue: elimination of r_x alone, then back substitution
-        const int jr = row_of(x);
-        float* zr = slot_ptr(x) + 1 + tid;
-        V* pw = Pw + (int64_t)jr * g.row + i;
-        cprev = yprev = 0.f;
-        for (int c = 0; c < nch; ++c) {
-            int g0;
-            const float* sb = stage_wait(g0);
-            fwd_chunk(sb, c * KB, zr, pw, x & 1);
-            stage_release(g0);
-        }
-        back_row(zr, Zw + (int64_t)jr * g.row + i);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&zdone[x & 1]);
-    };
-    // wait for flag(row, tile) == epoch (thread 0), then a consumer barrier
-    auto wait_flag = [&](int row, int tile) {
-        const int* f = flags + (int64_t)row * T + tile;
-        while (ld_acquire(f) != epoch) __nanosleep(40);
-    };
-    // a whole row of z from another strip (rows r_{-1}, r_L) into ring row dst (own column)
-    auto load_row = [&](float* dst, int row) {
-        const V* src = Zw + (int64_t)row * g.row + i;
-        for (int k = 0; k < nz; ++k) dst[k * MA_RING_W] = __ldcg(src + (int64_t)k * nx);
-    };
-
-    MA_CLK(t_pro);
-    fwd_row(0);
-    if (L >= 2) fwd_row(1);
-    MA_ADD(1, t_pro);
-    float hw = 0.f, he = 0.f;  // prefetched halo values of r_{m+1} (thread k = tid < nz)
-    for (int m = 0; m < L; ++m) {
-        const int j = row_of(m);
-        const int64_t jg = g.j0 + j;
-        const bool hasN = jg < g.ny - 1, hasS = jg > 0;
-        float* zC0 = slot_ptr(m);
-        // ring rows of j+1 and j-1: r_{m+1} (slot m+1) and r_{m-1} (slot m-1) in marching order
-        float* zN0 = hasN ? (dir > 0 ? slot_ptr(m + 1) : slot_ptr(m - 1)) : zC0;
-        float* zS0 = hasS ? (dir > 0 ? slot_ptr(m - 1) : slot_ptr(m + 1)) : zC0;
-        // ---- rows outside the strip (first / last step) and the first halo: synchronous ----
-        MA_CLK(t_sync);
-        const bool ld_prev = m == 0 && (dir > 0 ? hasS : hasN);       // r_{-1} exists
-        const bool ld_next = m == L - 1 && (dir > 0 ? hasN : hasS);   // r_L exists
-        if (m == 0 || ld_next) {
-            if (tid == 0) {
-                if (m == 0) { wait_flag(j, tW); wait_flag(j, tE); }
-                if (ld_prev) wait_flag(j - dir, t);
-                if (ld_next) wait_flag(j + dir, t);
-            }
-            cons_bar();
-            if (m == 0 && tid < nz) {
-                const V* zg = Zw + (int64_t)j * g.row + (int64_t)tid * nx;
-                zC0[tid * MA_RING_W] = __ldcg(zg + iWg);
-                zC0[tid * MA_RING_W + w + 1] = __ldcg(zg + iEg);
-            }
-            if (ld_prev) load_row(slot_ptr(m - 1) + 1 + tid, j - dir);
-            if (ld_next) load_row(slot_ptr(m + 1) + 1 + tid, j + dir);
-            cons_bar();
-        }
-        MA_ADD(4, t_sync);
-        // ---- combined pass: stencil(r_m) || elimination(r_{m+2}) ----
-        MA_CLK(t_comb);
-        const bool fw = m + 2 < L;
-        const int jf = fw ? row_of(m + 2) : j;
-        float* zrF = slot_ptr(m + 2) + 1 + tid;
-        V* pwF = Pw + (int64_t)jf * g.row + i;
-        const float* zC = zC0 + 1 + tid;
-        const float* zN = zN0 + 1 + tid;
-        const float* zS = zS0 + 1 + tid;
-        V* yw = Yw + (int64_t)j * g.row + i;
-        const int us = m & 1;
-        double acc[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-        V zprev = 0.f;
-        cprev = yprev = 0.f;
-        for (int c = 0; c < nch; ++c) {
-            const int k0 = c * KB;
-            if (c == nch / 2 && m + 1 < L) {  // halo of r_{m+1} (published during step m-1)
-                MA_CLK(t_h);
-                if (tid == 0) {
-                    const int jn = row_of(m + 1);
-                    wait_flag(jn, tW);
-                    wait_flag(jn, tE);
-                    // zdone[x & 1] may run at most one phase ahead of the publisher: it must have
-                    // published r_m before the consumers arrive for r_{m+2} on the same barrier
-                    if (m + 2 < L) wait_flag(j, t);
-                }
-                cons_bar();
-                if (tid < nz) {
-                    const V* zg = Zw + (int64_t)row_of(m + 1) * g.row + (int64_t)tid * nx;
-                    hw = __ldcg(zg + iWg);
-                    he = __ldcg(zg + iEg);
-                }
-                MA_ADD(4, t_h);
-            }
-            // stencil inputs: U, D (, s) of r_m from TMEM, bands / rhat0 from the stage, z from the ring
-            float ub[KB], db[KB], sv[KB];
-            tm_ld8_nw(tU(us) + (uint32_t)k0, ub);
-            tm_ld8_nw(tD(us) + (uint32_t)k0, db);
-            if (KIND == 2) tm_ld8_nw(tS(us) + (uint32_t)k0, sv);
-            int gS, gF = 0;
-            const float* sbS = stage_wait(gS);
-            const float* sbF = fw ? stage_wait(gF) : nullptr;
-            float4 b4[KB];
-            float ax[KB], zc[KB + 1], zE[KB], zW[KB], zNv[KB], zSv[KB], av[KB];
+    if (isF) {
+        // ============================ Thomas warps ============================
+        V* __restrict__ Pw = KIND == 1 ? vv.p : vv.s;
+        int cslot = 0;
+        uint32_t cphase = 0;
+        V cprev = 0.f, yprev = 0.f;
+        struct FwdIn { float rr[KB], pp[KB], vq[KB], uu[KB], dd[KB]; };
+        // one chunk of the elimination of row r_x: f = update, factors; y -> ring, c'/U/D/s -> TMEM,
+        // f -> HBM.  sync_step >= 0: wait until the S warps have read this chunk in step sync_step.
+        auto fwd_chunk = [&](int k0, int c, float* zr, V* pw, int us, int sync_step) {
+            MA_CLK(t0);
+            mbar_wait(&fullF[cslot], cphase);
+            MA_ADD(12, t0);
+            const float* sb = stF + (size_t)cslot * SF;
+            FwdIn in;
 #pragma unroll
             for (int e = 0; e < KB; ++e) {
-                const int ko = (k0 + e) * MA_RING_W;
-                b4[e] = *reinterpret_cast<const float4*>(sbS + e * 512 + 4 * tid);
-                if (KIND == 1) ax[e] = sbS[KB * 512 + e * 128 + tid];
-                zc[e] = zC[ko];
-                zE[e] = zC[ko + 1];
-                zW[e] = zC[ko - 1];
-                zNv[e] = zN[ko];
-                zSv[e] = zS[ko];
+                in.rr[e] = sb[e * 128 + col];
+                if (KIND == 1) in.pp[e] = fresh ? in.rr[e] : sb[KB * 128 + e * 128 + col];
+                in.vq[e] = (KIND == 1 && fresh) ? in.rr[e] : sb[OFF_V + e * 128 + col];
+                const float2 ud = *reinterpret_cast<const float2*>(sb + OFF_B2 + e * 256 + 2 * col);
+                in.uu[e] = ud.x;
+                in.dd[e] = ud.y;
             }
-            zc[KB] = zC[min(k0 + KB, nz - 1) * MA_RING_W];
-            tm_wait_ld();
-            if (KIND == 2) {
-#pragma unroll
-                for (int e = 0; e < KB; ++e) ax[e] = sv[e];
-            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&emptyF[cslot]);
+            if (++cslot == NSF) { cslot = 0; cphase ^= 1u; }
+            float cb[KB], yb[KB], fb[KB];
 #pragma unroll
             for (int e = 0; e < KB; ++e) {
                 const int k = k0 + e;
-                const V zp = (k + 1 < nz) ? zc[e + 1] : zc[e];  // multiplied by U = 0 on the top level
-                V a = zc[e];
-                a = fmaf(b4[e].x, zE[e], a);
-                a = fmaf(b4[e].y, zW[e], a);
-                a = fmaf(b4[e].z, zNv[e], a);
-                a = fmaf(b4[e].w, zSv[e], a);
-                a = fmaf(ub[e], zp, a);
-                a = fmaf(db[e], zprev, a);  // zprev = 0 at k = 0 (D = 0 there)
-                zprev = zc[e];
-                av[e] = a;
-                if (act && k < nz) {
-                    if (KIND == 1) {
-                        acc_dot<MODE>(acc[0], ax[e], a);
-                    } else {
-                        acc_dot<MODE>(acc[0], a, ax[e]);
-                        acc_dot<MODE>(acc[1], a, a);
-                        acc_dot<MODE>(acc[2], ax[e], ax[e]);
-                    }
-                }
+                const V f = KIND == 1 ? fmaf(beta, fmaf(-omega, in.vq[e], in.pp[e]), in.rr[e])
+                                      : fmaf(-alpha, in.vq[e], in.rr[e]);
+                const V inv = rcp_fast<V>(fmaf(-in.dd[e], cprev, 1.f));
+                const V cc = k == 0 ? in.uu[e] : in.uu[e] * inv;
+                const V y = k == 0 ? f : fmaf(-in.dd[e], yprev, f) * inv;
+                cb[e] = cc; yb[e] = y; fb[e] = f;
+                cprev = cc;
+                yprev = y;
             }
-            V* yk = yw + (int64_t)k0 * nx;
-            if (uni && k0 + KB <= nz) {
+            V* pk = pw + (int64_t)k0 * nx;
+            if (uni && k0 + KB <= nz) {  // warp-uniform: a full chunk of a full tile
 #pragma unroll
-                for (int e = 0; e < KB; ++e) yk[e * nx] = av[e];
+                for (int e = 0; e < KB; ++e) __stcg(pk + e * nx, fb[e]);
             } else {
 #pragma unroll
                 for (int e = 0; e < KB; ++e)
-                    if (act && k0 + e < nz) yk[e * nx] = av[e];
+                    if (act && k0 + e < nz) __stcg(pk + e * nx, fb[e]);
             }
-            if (fw) fwd_chunk(sbF, k0, zrF, pwF, us);
-            stage_release(gS);
-            if (fw) stage_release(gF);
-        }
-        MA_ADD(6, t_comb);
-        MA_CLK(t_red);
-        cons_sum_d<NQ>(acc, red, MODE == 2 ? 0x7u : 0x0u);  // contains cons_bar()
-        if (tid == 0) {
+            tm_st8(tl + (uint32_t)k0, cb);
+            if (sync_step >= 0) {  // the S warps read U, D, s (TMEM slot us) and z(r_{m-1}) of this chunk
+                MA_CLK(t1);
+                mbar_wait(&sread[c], (uint32_t)(sync_step & 1));
+                MA_ADD(13, t1);
+            }
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) vv.slots[q * per_q + (int64_t)j * T + t] = acc[q];
-        }
-        MA_ADD(8, t_red);
-        if (fw) {
-            MA_CLK(t_back);
-            back_row(zrF, Zw + (int64_t)jf * g.row + i);
+            for (int e = 0; e < KB; ++e) zr[(k0 + e) * MA_RING_W] = yb[e];
+            tm_st8(tU(us) + (uint32_t)k0, in.uu);
+            tm_st8(tD(us) + (uint32_t)k0, in.dd);
+            if (KIND == 2) tm_st8(tS(us) + (uint32_t)k0, fb);
+        };
+        // back substitution of row r_x (y in ring row zr): z -> ring (in place) and HBM
+        auto back_row = [&](float* zr, V* zw, int x) {
+            MA_CLK(t0);
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            V zn = 0.f;  // z(NZ8) = 0; padded levels have c' = y = 0
+            for (int k0 = NZ8 - KB; k0 >= 0; k0 -= KB) {
+                float cb[KB], yb[KB];
+                tm_ld8_nw(tl + (uint32_t)k0, cb);
+#pragma unroll
+                for (int e = 0; e < KB; ++e) yb[e] = zr[(k0 + e) * MA_RING_W];
+                tm_wait_ld();
+#pragma unroll
+                for (int e = KB - 1; e >= 0; --e) {
+                    zn = fmaf(-cb[e], zn, yb[e]);
+                    yb[e] = zn;
+                }
+#pragma unroll
+                for (int e = 0; e < KB; ++e) zr[(k0 + e) * MA_RING_W] = yb[e];
+                V* zk = zw + (int64_t)k0 * nx;
+                if (uni && k0 + KB <= nz) {
+#pragma unroll
+                    for (int e = 0; e < KB; ++e) __stcg(zk + e * nx, yb[e]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < KB; ++e)
+                        if (act && k0 + e < nz) __stcg(zk + e * nx, yb[e]);
+                }
+            }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&zdone[(m + 2) & 1]);
-            MA_ADD(3, t_back);
+            if (lane == 0) {
+                mbar_arrive(&zready[x & 1]);  // the S warps may read z(r_x) from the ring
+                mbar_arrive(&zdone[x & 1]);   // the publisher may release the ready flag
+            }
+            MA_ADD(14, t0);
+        };
+        auto T_row = [&](int x, int sync_step) {
+            const int jr = row_of(x);
+            float* zr = slot_ptr(x) + 1 + col;
+            V* pw = Pw + (int64_t)jr * g.row + i;
+            cprev = yprev = 0.f;
+            MA_CLK(t0);
+            for (int c = 0; c < nch; ++c) fwd_chunk(c * KB, c, zr, pw, x & 1, sync_step);
+            MA_ADD(15, t0);
+            back_row(zr, Zw + (int64_t)jr * g.row + i, x);
+        };
+        T_row(0, -1);
+        if (L >= 2) T_row(1, -1);
+        for (int m = 0; m + 2 < L; ++m) T_row(m + 2, m);
+    } else {
+        // ============================ stencil warps ============================
+        V* __restrict__ Yw = KIND == 1 ? vv.v : vv.t;
+        const int64_t per_q = (int64_t)nyl * T;
+        const int iWg = (i0 == 0) ? nx - 1 : i0 - 1;       // W halo column (tile t-1, periodic)
+        const int iEg = (i0 + w == nx) ? 0 : i0 + w;        // E halo column (tile t+1, periodic)
+        const int tW = (t == 0) ? T - 1 : t - 1, tE = (t + 1 == T) ? 0 : t + 1;
+        int cslot = 0;
+        uint32_t cphase = 0;
+        auto wait_flag = [&](int row, int tile) {
+            const int* f = flags + (int64_t)row * T + tile;
+            while (ld_acquire(f) != epoch) __nanosleep(40);
+        };
+        // a whole row of z from another strip (rows r_{-1}, r_L) into ring row dst (own column)
+        auto load_row = [&](float* dst, int row) {
+            const V* src = Zw + (int64_t)row * g.row + i;
+            for (int k = 0; k < nz; ++k) dst[k * MA_RING_W] = __ldcg(src + (int64_t)k * nx);
+        };
+        float hw = 0.f, he = 0.f;  // prefetched halo values of r_{m+1} (thread k = tid < nz)
+        for (int m = 0; m < L; ++m) {
+            const int j = row_of(m);
+            const int64_t jg = g.j0 + j;
+            const bool hasN = jg < g.ny - 1, hasS = jg > 0;
+            // ---- z(r_m), z(r_{m+1}) complete (F warps) ----
+            MA_CLK(t_z);
+            if (m == 0) mbar_wait(&zready[0], 0u);
+            if (m + 1 < L) mbar_wait(&zready[(m + 1) & 1], (uint32_t)(((m + 1) >> 1) & 1));
+            MA_ADD(5, t_z);
+            float* zC0 = slot_ptr(m);
+            float* zN0 = hasN ? (dir > 0 ? slot_ptr(m + 1) : slot_ptr(m - 1)) : zC0;
+            float* zS0 = hasS ? (dir > 0 ? slot_ptr(m - 1) : slot_ptr(m + 1)) : zC0;
+            // ---- rows outside the strip (first / last step) and the first halo: synchronous ----
+            MA_CLK(t_sync);
+            const bool ld_prev = m == 0 && (dir > 0 ? hasS : hasN);       // r_{-1} exists
+            const bool ld_next = m == L - 1 && (dir > 0 ? hasN : hasS);   // r_L exists
+            if (m == 0 || ld_next) {
+                if (tid == 0) {
+                    if (m == 0) { wait_flag(j, tW); wait_flag(j, tE); }
+                    if (ld_prev) wait_flag(j - dir, t);
+                    if (ld_next) wait_flag(j + dir, t);
+                }
+                cons_bar();
+                if (m == 0 && tid < nz) {
+                    const V* zg = Zw + (int64_t)j * g.row + (int64_t)tid * nx;
+                    zC0[tid * MA_RING_W] = __ldcg(zg + iWg);
+                    zC0[tid * MA_RING_W + w + 1] = __ldcg(zg + iEg);
+                }
+                if (ld_prev) load_row(slot_ptr(m - 1) + 1 + col, j - dir);
+                if (ld_next) load_row(slot_ptr(m + 1) + 1 + col, j + dir);
+                cons_bar();
+            }
+            MA_ADD(4, t_sync);
+            MA_CLK(t_st);
+            const float* zC = zC0 + 1 + col;
+            const float* zN = zN0 + 1 + col;
+            const float* zS = zS0 + 1 + col;
+            V* yw = Yw + (int64_t)j * g.row + i;
+            const int us = m & 1;
+            double acc[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+            V zprev = 0.f;
+            for (int c = 0; c < nch; ++c) {
+                const int k0 = c * KB;
+                if (c == (3 * nch) / 4 && m + 1 < L) {  // halo of r_{m+1} (published at the end of step m-1)
+                    MA_CLK(t_h);
+                    if (tid == 0) {
+                        const int jn = row_of(m + 1);
+                        wait_flag(jn, tW);
+                        wait_flag(jn, tE);
+                        // zdone[x & 1] may run at most one phase ahead of the publisher: it must have
+                        // published r_m before the F warps arrive for r_{m+2} (after sread of this step)
+                        if (m + 2 < L) wait_flag(j, t);
+                    }
+                    cons_bar();
+                    if (tid < nz) {
+                        const V* zg = Zw + (int64_t)row_of(m + 1) * g.row + (int64_t)tid * nx;
+                        hw = __ldcg(zg + iWg);
+                        he = __ldcg(zg + iEg);
+                    }
+                    MA_ADD(4, t_h);
+                }
+                // U, D (, s) of r_m from TMEM, bands / rhat0 from the stage, z from the ring
+                float ub[KB], db[KB], sv[KB];
+                tm_ld8_nw(tU(us) + (uint32_t)k0, ub);
+                tm_ld8_nw(tD(us) + (uint32_t)k0, db);
+                if (KIND == 2) tm_ld8_nw(tS(us) + (uint32_t)k0, sv);
+                MA_CLK(t0);
+                mbar_wait(&fullS[cslot], cphase);
+                MA_ADD(2, t0);
+                const float* sbS = stS + (size_t)cslot * SF;
+                float4 b4[KB];
+                float ax[KB], zc[KB + 1], zE[KB], zW[KB], zNv[KB], zSv[KB], av[KB];
+#pragma unroll
+                for (int e = 0; e < KB; ++e) {
+                    const int ko = (k0 + e) * MA_RING_W;
+                    b4[e] = *reinterpret_cast<const float4*>(sbS + e * 512 + 4 * col);
+                    if (KIND == 1) ax[e] = sbS[KB * 512 + e * 128 + col];
+                    zc[e] = zC[ko];
+                    zE[e] = zC[ko + 1];
+                    zW[e] = zC[ko - 1];
+                    zNv[e] = zN[ko];
+                    zSv[e] = zS[ko];
+                }
+                zc[KB] = zC[min(k0 + KB, nz - 1) * MA_RING_W];
+                tm_wait_ld();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&emptyS[cslot]);
+                    mbar_arrive(&sread[c]);  // the F warps may now overwrite this chunk
+                }
+                if (++cslot == NSS) { cslot = 0; cphase ^= 1u; }
+                if (KIND == 2) {
+#pragma unroll
+                    for (int e = 0; e < KB; ++e) ax[e] = sv[e];
+                }
+#pragma unroll
+                for (int e = 0; e < KB; ++e) {
+                    const int k = k0 + e;
+                    const V zp = (k + 1 < nz) ? zc[e + 1] : zc[e];  // multiplied by U = 0 on the top level
+                    V a = zc[e];
+                    a = fmaf(b4[e].x, zE[e], a);
+                    a = fmaf(b4[e].y, zW[e], a);
+                    a = fmaf(b4[e].z, zNv[e], a);
+                    a = fmaf(b4[e].w, zSv[e], a);
+                    a = fmaf(ub[e], zp, a);
+                    a = fmaf(db[e], zprev, a);  // zprev = 0 at k = 0 (D = 0 there)
+                    zprev = zc[e];
+                    av[e] = a;
+                    if (act && k < nz) {
+                        if (KIND == 1) {
+                            acc_dot<MODE>(acc[0], ax[e], a);
+                        } else {
+                            acc_dot<MODE>(acc[0], a, ax[e]);
+                            acc_dot<MODE>(acc[1], a, a);
+                            acc_dot<MODE>(acc[2], ax[e], ax[e]);
+                        }
+                    }
+                }
+                V* yk = yw + (int64_t)k0 * nx;
+                if (uni && k0 + KB <= nz) {
+#pragma unroll
+                    for (int e = 0; e < KB; ++e) __stcg(yk + e * nx, av[e]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < KB; ++e)
+                        if (act && k0 + e < nz) __stcg(yk + e * nx, av[e]);
+                }
+            }
+            MA_ADD(6, t_st);
+            MA_CLK(t_red);
+            cons_sum_d<NQ>(acc, red, MODE == 2 ? 0x7u : 0x0u);  // contains cons_bar()
+            if (tid == 0) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) vv.slots[q * per_q + (int64_t)j * T + t] = acc[q];
+            }
+            if (m + 1 < L && tid < nz) {
+                float* zn1 = slot_ptr(m + 1);
+                zn1[tid * MA_RING_W] = hw;
+                zn1[tid * MA_RING_W + w + 1] = he;
+            }
+            cons_bar();  // ring halo and `red` are rewritten by the next step
+            MA_ADD(8, t_red);
         }
-        if (m + 1 < L && tid < nz) {
-            float* zn1 = slot_ptr(m + 1);
-            zn1[tid * MA_RING_W] = hw;
-            zn1[tid * MA_RING_W + w + 1] = he;
-        }
-        cons_bar();  // ring rows / halo and `red` are rewritten by the next step
     }
+    // ---- all compute warps: release TMEM ----
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    cons_bar();
+    asm volatile("bar.sync 2, 256;" ::: "memory");
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase) : "memory");
@@ -607,6 +619,10 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     if (tid == 0) {
         MA_ADD(0, t_all);
         for (int q = 0; q < 9; ++q) g_ma_trace[blockIdx.x * 16 + q] = tr[q];
+    }
+    if (tid == 128) {
+        MA_ADD(11, t_all);
+        for (int q = 11; q < 16; ++q) g_ma_trace[blockIdx.x * 16 + q] = tr[q];
     }
 #endif
 }

@@ -34,8 +34,9 @@ assert egs.lib().eg_debug_march_trace(buf, 1024 * 16) == 0
 t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16).astype(np.float64)
 ncta = int((t[:, 0] > 0).sum())
 t = t[:ncta]
-names = ["total", "prologue T(r0),T(r1)", " all full-waits", "back subst", "flag/halo/boundary sync", "-", "combined pass",
-         "-", "reduce", "PRODUCER empty-wait", "PRODUCER total"]
+names = ["S total", "-", " S stage waits", "-", " S flag/halo/boundary sync", " S wait z(r_m+1) from F",
+         " S stencil pass", "-", " S reduce", "PRODUCER empty-wait", "PRODUCER total", "F total",
+         " F stage waits", " F wait sread (S behind)", " F back subst", " F elimination"]
 print(f"CTAs {ncta}; cycles per CTA (mean / min / max) of the last march launch (phase B)")
 for q, nm in enumerate(names):
     print(f"  {nm:22s} {t[:, q].mean():14.0f} {t[:, q].min():14.0f} {t[:, q].max():14.0f}  {100 * t[:, q].mean() / t[:, 0].mean():5.1f}%")
