@@ -712,7 +712,7 @@ int set_thomas_smem(eg_solver* s) {
     return rc;
 }
 
-// TMA tensor maps of the arrays the fused phases stream ([nyl][nz][nx] views, 128 x MA_KB x 1 boxes)
+// TMA tensor maps of the arrays the fused phases stream ([nyl][nz][nx] views, 128 x MA_KS x 1 boxes)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -721,7 +721,7 @@ bool encode_map(EncodeTiledFn enc, CUtensorMap* m, void* base, int64_t inner, in
                 int box0) {
     const cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)nz, (cuuint64_t)nyl};
     const cuuint64_t strides[2] = {(cuuint64_t)(inner * esz), (cuuint64_t)(inner * nz * esz)};
-    const cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)MA_KB, 1u};
+    const cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)MA_KS, 1u};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
     return enc(m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides,
                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

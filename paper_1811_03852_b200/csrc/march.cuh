@@ -40,9 +40,10 @@ constexpr int MA_CONS = 128;                           // consumer threads: one 
 constexpr int MA_THREADS = 2 * MA_CONS + 64;           // stencil + Thomas warps, producer, publisher
 // stage = one MA_KB-level chunk of one row.  Elimination ring: r, (p,) v, (U, D); stencil ring:
 // (E, W, N, S) (, rhat0): 640 floats / level in phase A, 512 in phase B, for both rings
-constexpr int ma_stage_floats(int kind) { return MA_KB * (kind == 1 ? 640 : 512); }
+constexpr int MA_KS = 4;  // levels per stage: a chunk of MA_KB levels is two stages (finer refill)
+constexpr int ma_stage_floats(int kind) { return MA_KS * (kind == 1 ? 640 : 512); }
 constexpr int ma_stage_bytes(int kind) { return 4 * ma_stage_floats(kind); }
-constexpr int MA_MAX_STAGES = 8;
+constexpr int MA_MAX_STAGES = 16;
 constexpr int MA_RING_W = 130;                         // W halo | 128 columns | E halo
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -115,12 +116,12 @@ __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, 
         : "memory");
 }
 
-// tensor maps of the streamed arrays, [nyl][nz][nx] views with 128 x MA_KB x 1 boxes; (U, D) and
+// tensor maps of the streamed arrays, [nyl][nz][nx] views with 128 x MA_KS x 1 boxes; (U, D) and
 // (E, W, N, S) are viewed as 8-byte elements: [nyl][nz][nx] and [nyl][nz][2 nx]
 struct MarchMaps {
     CUtensorMap r, p, v, rh, b2, b4;
 };
-constexpr uint32_t MA_BOX_V = 128 * MA_KB * 4;       // one fp32 array
+constexpr uint32_t MA_BOX_V = 128 * MA_KS * 4;       // one fp32 array
 constexpr uint32_t MA_BOX_B2 = 2 * MA_BOX_V;
 constexpr uint32_t MA_BOX_B4 = 4 * MA_BOX_V;
 
@@ -211,8 +212,11 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     constexpr int NQ = KIND == 1 ? 1 : 3;
     constexpr int KB = MA_KB;
     constexpr int SF = ma_stage_floats(KIND);
-    constexpr int OFF_V = (KIND == 1 ? 2 : 1) * MA_KB * 128;   // v after r (, p)
-    constexpr int OFF_B2 = (KIND == 1 ? 3 : 2) * MA_KB * 128;  // (U, D) after r, (p,) v
+    constexpr int KS = MA_KS;
+    constexpr int OFF_P = KS * 128;                          // p after r
+    constexpr int OFF_V = (KIND == 1 ? 2 : 1) * KS * 128;   // v after r (, p)
+    constexpr int OFF_B2 = (KIND == 1 ? 3 : 2) * KS * 128;  // (U, D) after r, (p,) v
+    constexpr int OFF_RH = KS * 512;                         // rhat0 after (E, W, N, S)
     extern __shared__ __align__(128) unsigned char smraw[];
     __shared__ __align__(8) uint64_t fullF[MA_MAX_STAGES], emptyF[MA_MAX_STAGES];
     __shared__ __align__(8) uint64_t fullS[MA_MAX_STAGES], emptyS[MA_MAX_STAGES];
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 mbar_expect_tx(fb, (KIND == 1 ? (fresh ? 1u : 3u) : 2u) * MA_BOX_V + MA_BOX_B2);
                 float* sb = stF + (size_t)fslot * SF;
                 tma3(sb, &maps.r, i0, k0, jr, fb);
-                if (KIND == 1 && !fresh) tma3(sb + KB * 128, &maps.p, i0, k0, jr, fb);
+                if (KIND == 1 && !fresh) tma3(sb + OFF_P, &maps.p, i0, k0, jr, fb);
                 if (KIND == 2 || !fresh) tma3(sb + OFF_V, &maps.v, i0, k0, jr, fb);
                 tma3(sb + OFF_B2, &maps.b2, i0, k0, jr, fb);
                 if (++fslot == NSF) { fslot = 0; ++fround; }
@@ -290,22 +294,22 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 mbar_expect_tx(fb, MA_BOX_B4 + (KIND == 1 ? MA_BOX_V : 0u));
                 float* sb = stS + (size_t)sslot * SF;
                 tma3(sb, &maps.b4, 2 * i0, k0, jr, fb);
-                if (KIND == 1) tma3(sb + KB * 512, &maps.rh, i0, k0, jr, fb);
+                if (KIND == 1) tma3(sb + OFF_RH, &maps.rh, i0, k0, jr, fb);
                 if (++sslot == NSS) { sslot = 0; ++sround; }
             };
-            for (int c = 0; c < nch; ++c) fwd_stage(row_of(0), c * KB);
+            for (int k0 = 0; k0 < NZ8; k0 += KS) fwd_stage(row_of(0), k0);
             if (L >= 2)
-                for (int c = 0; c < nch; ++c) fwd_stage(row_of(1), c * KB);
+                for (int k0 = 0; k0 < NZ8; k0 += KS) fwd_stage(row_of(1), k0);
             for (int m = 0; m < L; ++m)
-                for (int c = 0; c < nch; ++c) {
-                    sten_stage(row_of(m), c * KB);
-                    if (m + 2 < L) fwd_stage(row_of(m + 2), c * KB);
+                for (int k0 = 0; k0 < NZ8; k0 += KS) {
+                    sten_stage(row_of(m), k0);
+                    if (m + 2 < L) fwd_stage(row_of(m + 2), k0);
                 }
         }
 #ifdef MA_TRACE
         if (lane == 0) {
             MA_ADD(10, t_all);
-            for (int q = 9; q < 11; ++q) g_ma_trace[blockIdx.x * 16 + q] = tr[q];
+            for (int q = 9; q < 11; ++q) g_ma_trace[(KIND - 1) * 512 * 16 + blockIdx.x * 16 + q] = tr[q];
         }
 #endif
         return;  // the compute warps keep the CTA (and its TMEM) alive until every stage has landed
@@ -344,23 +348,27 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
         // one chunk of the elimination of row r_x: f = update, factors; y -> ring, c'/U/D/s -> TMEM,
         // f -> HBM.  sync_step >= 0: wait until the S warps have read this chunk in step sync_step.
         auto fwd_chunk = [&](int k0, int c, float* zr, V* pw, int us, int sync_step) {
-            MA_CLK(t0);
-            mbar_wait(&fullF[cslot], cphase);
-            MA_ADD(12, t0);
-            const float* sb = stF + (size_t)cslot * SF;
             FwdIn in;
 #pragma unroll
-            for (int e = 0; e < KB; ++e) {
-                in.rr[e] = sb[e * 128 + col];
-                if (KIND == 1) in.pp[e] = fresh ? in.rr[e] : sb[KB * 128 + e * 128 + col];
-                in.vq[e] = (KIND == 1 && fresh) ? in.rr[e] : sb[OFF_V + e * 128 + col];
-                const float2 ud = *reinterpret_cast<const float2*>(sb + OFF_B2 + e * 256 + 2 * col);
-                in.uu[e] = ud.x;
-                in.dd[e] = ud.y;
+            for (int h = 0; h < KB / KS; ++h) {  // the chunk's stages
+                MA_CLK(t0);
+                mbar_wait(&fullF[cslot], cphase);
+                MA_ADD(12, t0);
+                const float* sb = stF + (size_t)cslot * SF;
+#pragma unroll
+                for (int l = 0; l < KS; ++l) {
+                    const int e = h * KS + l;
+                    in.rr[e] = sb[l * 128 + col];
+                    if (KIND == 1) in.pp[e] = fresh ? in.rr[e] : sb[OFF_P + l * 128 + col];
+                    in.vq[e] = (KIND == 1 && fresh) ? in.rr[e] : sb[OFF_V + l * 128 + col];
+                    const float2 ud = *reinterpret_cast<const float2*>(sb + OFF_B2 + l * 256 + 2 * col);
+                    in.uu[e] = ud.x;
+                    in.dd[e] = ud.y;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyF[cslot]);
+                if (++cslot == NSF) { cslot = 0; cphase ^= 1u; }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&emptyF[cslot]);
-            if (++cslot == NSF) { cslot = 0; cphase ^= 1u; }
             float cb[KB], yb[KB], fb[KB];
 #pragma unroll
             for (int e = 0; e < KB; ++e) {
@@ -530,17 +538,26 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 tm_ld8_nw(tU(us) + (uint32_t)k0, ub);
                 tm_ld8_nw(tD(us) + (uint32_t)k0, db);
                 if (KIND == 2) tm_ld8_nw(tS(us) + (uint32_t)k0, sv);
-                MA_CLK(t0);
-                mbar_wait(&fullS[cslot], cphase);
-                MA_ADD(2, t0);
-                const float* sbS = stS + (size_t)cslot * SF;
                 float4 b4[KB];
                 float ax[KB], zc[KB + 1], zE[KB], zW[KB], zNv[KB], zSv[KB], av[KB];
+                int sl[KB / KS];
+#pragma unroll
+                for (int h = 0; h < KB / KS; ++h) {  // the chunk's stages
+                    MA_CLK(t0);
+                    mbar_wait(&fullS[cslot], cphase);
+                    MA_ADD(2, t0);
+                    const float* sbS = stS + (size_t)cslot * SF;
+#pragma unroll
+                    for (int l = 0; l < KS; ++l) {
+                        b4[h * KS + l] = *reinterpret_cast<const float4*>(sbS + l * 512 + 4 * col);
+                        if (KIND == 1) ax[h * KS + l] = sbS[OFF_RH + l * 128 + col];
+                    }
+                    sl[h] = cslot;
+                    if (++cslot == NSS) { cslot = 0; cphase ^= 1u; }
+                }
 #pragma unroll
                 for (int e = 0; e < KB; ++e) {
                     const int ko = (k0 + e) * MA_RING_W;
-                    b4[e] = *reinterpret_cast<const float4*>(sbS + e * 512 + 4 * col);
-                    if (KIND == 1) ax[e] = sbS[KB * 512 + e * 128 + col];
                     zc[e] = zC[ko];
                     zE[e] = zC[ko + 1];
                     zW[e] = zC[ko - 1];
@@ -551,10 +568,10 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 tm_wait_ld();
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(&emptyS[cslot]);
+#pragma unroll
+                    for (int h = 0; h < KB / KS; ++h) mbar_arrive(&emptyS[sl[h]]);
                     mbar_arrive(&sread[c]);  // the F warps may now overwrite this chunk
                 }
-                if (++cslot == NSS) { cslot = 0; cphase ^= 1u; }
                 if (KIND == 2) {
 #pragma unroll
                     for (int e = 0; e < KB; ++e) ax[e] = sv[e];
@@ -618,11 +635,11 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
 #ifdef MA_TRACE
     if (tid == 0) {
         MA_ADD(0, t_all);
-        for (int q = 0; q < 9; ++q) g_ma_trace[blockIdx.x * 16 + q] = tr[q];
+        for (int q = 0; q < 9; ++q) g_ma_trace[(KIND - 1) * 512 * 16 + blockIdx.x * 16 + q] = tr[q];
     }
     if (tid == 128) {
         MA_ADD(11, t_all);
-        for (int q = 11; q < 16; ++q) g_ma_trace[blockIdx.x * 16 + q] = tr[q];
+        for (int q = 11; q < 16; ++q) g_ma_trace[(KIND - 1) * 512 * 16 + blockIdx.x * 16 + q] = tr[q];
     }
 #endif
 }

@@ -31,12 +31,12 @@ x, info, hist = s.solve(b, tol=0.0, maxit=2, flags=egs.EG_SOLVE_NO_GRAPH)
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * (1024 * 16))()
 assert egs.lib().eg_debug_march_trace(buf, 1024 * 16) == 0
-t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16).astype(np.float64)
+t = np.frombuffer(buf, dtype=np.uint64).reshape(2, 512, 16).astype(np.float64)[0 if a.which == "A" else 1]
 ncta = int((t[:, 0] > 0).sum())
 t = t[:ncta]
 names = ["S total", "-", " S stage waits", "-", " S flag/halo/boundary sync", " S wait z(r_m+1) from F",
          " S stencil pass", "-", " S reduce", "PRODUCER empty-wait", "PRODUCER total", "F total",
          " F stage waits", " F wait sread (S behind)", " F back subst", " F elimination"]
-print(f"CTAs {ncta}; cycles per CTA (mean / min / max) of the last march launch (phase B)")
+print(f"CTAs {ncta}; cycles per CTA (mean / min / max) of the last phase {a.which} launch")
 for q, nm in enumerate(names):
     print(f"  {nm:22s} {t[:, q].mean():14.0f} {t[:, q].min():14.0f} {t[:, q].max():14.0f}  {100 * t[:, q].mean() / t[:, 0].mean():5.1f}%")
