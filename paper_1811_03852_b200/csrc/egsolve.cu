@@ -73,7 +73,7 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L) {
     return true;
 }
 
-struct PendingEv { int kid; cudaEvent_t a, b; };
+struct PendingEv { int kid; cudaEvent_t a, b; double bytes; };
 
 }  // namespace
 
@@ -126,7 +126,9 @@ struct eg_solver {
     std::vector<cudaEvent_t> evpool;
     std::vector<PendingEv> pending;
     double prof_ms[KID_COUNT]{};
+    double prof_bytes[KID_COUNT]{};  // algorithmic HBM bytes of the profiled launches
     int64_t prof_n[KID_COUNT]{};
+    bool next_fresh = false;         // the next iteration starts from p = v = 0 (reads r only)
     std::string err;
 };
 
@@ -172,11 +174,14 @@ cudaEvent_t take_event(eg_solver* s) {
     return e;
 }
 
+double alg_bytes(const eg_solver* s, int kid);
+
 struct ProfScope {
     eg_solver* s;
     int kid;
+    double bytes;
     cudaEvent_t a = nullptr;
-    ProfScope(eg_solver* s_, int k) : s(s_), kid(k) {
+    ProfScope(eg_solver* s_, int k, double b = -1.0) : s(s_), kid(k), bytes(b) {
         if (s->profiling) {
             a = take_event(s);
             cudaEventRecord(a, s->st);
@@ -186,7 +191,7 @@ struct ProfScope {
         if (s->profiling) {
             cudaEvent_t b = take_event(s);
             cudaEventRecord(b, s->st);
-            s->pending.push_back({kid, a, b});
+            s->pending.push_back({kid, a, b, bytes >= 0.0 ? bytes : alg_bytes(s, kid)});
         }
     }
 };
@@ -196,6 +201,7 @@ void drain_profile(eg_solver* s) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
             s->prof_ms[p.kid] += ms;
+            s->prof_bytes[p.kid] += p.bytes;
             s->prof_n[p.kid] += 1;
         }
         s->evpool.push_back(p.a);
@@ -281,7 +287,9 @@ int iteration_fused(eg_solver* s, void* x_it) {
     if constexpr (MODE != 0) {
         const unsigned grid = (unsigned)(s->mg.strips * s->L.tiles);
         {
-            ProfScope ps(s, KID_PHASE_A);
+            // the first iteration after a (re)start has p = v = 0: phase A then reads r only
+            ProfScope ps(s, KID_PHASE_A, s->next_fresh ? alg_bytes(s, KID_PHASE_A) - 2.0 * s->L.vsz * s->L.n : -1.0);
+            s->next_fresh = false;
             k_march<MODE, 1><<<grid, MA_THREADS, s->smem_march, s->st>>>(s->geo, v, s->mg, s->ready_flags, s->maps);
             CK(cudaGetLastError());
         }
@@ -427,6 +435,7 @@ int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero) {
         if ((rc = halo(s, x, s->xg, (unsigned char*)s->xg + s->L.row * 8, sizeof(X)))) return rc;
     }
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+    s->next_fresh = true;
     {
         ProfScope ps(s, KID_START);
         if (entry && xzero) k_start<MODE, true, true><<<gr, RW, 0, s->st>>>(s->geo, v, b);
@@ -763,6 +772,29 @@ bool valid_grid(const eg_grid* g) {
            g->ny < 65536 && g->nz < 65536;
 }
 
+// algorithmic HBM bytes of one launch, V = vector / band bytes, X = x bytes
+double alg_bytes(const eg_solver* s, int kid) {
+    const double V = (double)s->L.vsz, X = (double)s->L.xsz, n = (double)s->L.n;
+    double per = 0;
+    switch (kid) {
+        case KID_SCALE: per = 7 * 8 + 6 * V + 8; break;            // 7 fp64 in; 6 V + diag out
+        case KID_START: per = 8 + X + 6 * V + 2 * V; break;        // bhat, x, 6 bands; r, rhat0
+        case KID_THOMAS_P: per = 5 * V + 2 * V; break;             // r,p,v,U,D; p,z
+        case KID_STENCIL_A: per = 8 * V + V; break;                // z,6 bands,rhat0; v
+        case KID_THOMAS_S: per = 4 * V + 2 * V; break;             // r,v,U,D; s,z_s
+        case KID_STENCIL_B: per = 8 * V + V; break;                // z_s,6 bands,s; t
+        case KID_UPDATE: per = X + 5 * V + X + V; break;           // x,z,z_s,s,t,rhat0; x,r
+        case KID_APPLY: per = 7 * V + V; break;
+        case KID_PRECOND: per = 3 * V + V; break;
+        case KID_CONVERT: per = 12; break;
+        case KID_PHASE_A: per = 4 * V + 6 * V + 3 * V; break;      // r,p,v,rhat0 + B4,B2; p',z,v'
+        case KID_PHASE_B: per = 2 * V + 6 * V + 3 * V; break;      // r,v' + B4,B2; s,z_s,t
+        case KID_SOR: per = 0.5 * (V + V + 4 * V + 6 * V + V); break;  // half the points: f, x, 4 nbrs, bands; x
+        default: per = 0;
+    }
+    return per * n;
+}
+
 }  // namespace
 
 // =================================== C ABI ===================================
@@ -1009,28 +1041,8 @@ int eg_profile_get(const eg_solver* s, int kid, double* total_ms, int64_t* launc
     if (!s || kid < 0 || kid >= KID_COUNT) return EG_ERR_ARG;
     if (total_ms) *total_ms = s->prof_ms[kid];
     if (launches) *launches = s->prof_n[kid];
-    if (alg_bytes_per_launch) {
-        // algorithmic HBM bytes per point, V = vector / band bytes, X = x bytes
-        const double V = (double)s->L.vsz, X = (double)s->L.xsz, n = (double)s->L.n;
-        double per = 0;
-        switch (kid) {
-            case KID_SCALE: per = 7 * 8 + 6 * V + 8; break;            // 7 fp64 in; 6 V + diag out
-            case KID_START: per = 8 + X + 6 * V + 2 * V; break;        // bhat, x, 6 bands; r, rhat0
-            case KID_THOMAS_P: per = 5 * V + 2 * V; break;             // r,p,v,U,D; p,z
-            case KID_STENCIL_A: per = 8 * V + V; break;                // z,6 bands,rhat0; v
-            case KID_THOMAS_S: per = 4 * V + 2 * V; break;             // r,v,U,D; s,z_s
-            case KID_STENCIL_B: per = 8 * V + V; break;                // z_s,6 bands,s; t
-            case KID_UPDATE: per = X + 5 * V + X + V; break;           // x,z,z_s,s,t,rhat0; x,r
-            case KID_APPLY: per = 7 * V + V; break;
-            case KID_PRECOND: per = 3 * V + V; break;
-            case KID_CONVERT: per = 12; break;
-            case KID_PHASE_A: per = 4 * V + 6 * V + 3 * V; break;   // r,p,v,rhat0 + B4,B2; p',z,v'
-            case KID_PHASE_B: per = 2 * V + 6 * V + 3 * V; break;   // r,v' + B4,B2; s,z_s,t
-            case KID_SOR: per = 0.5 * (V + V + 4 * V + 6 * V + V); break;  // half the points: f, x, 4 nbrs, bands; x
-            default: per = 0;
-        }
-        *alg_bytes_per_launch = per * n;
-    }
+    if (alg_bytes_per_launch)  // the profiled launches' average, else the steady-state figure
+        *alg_bytes_per_launch = s->prof_n[kid] > 0 ? s->prof_bytes[kid] / (double)s->prof_n[kid] : alg_bytes(s, kid);
     return EG_OK;
 }
 
@@ -1043,7 +1055,7 @@ int eg_debug_march_trace(unsigned long long* out, int n) {
 
 int eg_profile_reset(eg_solver* s) {
     if (!s) return EG_ERR_ARG;
-    for (int k = 0; k < KID_COUNT; ++k) { s->prof_ms[k] = 0; s->prof_n[k] = 0; }
+    for (int k = 0; k < KID_COUNT; ++k) { s->prof_ms[k] = 0; s->prof_bytes[k] = 0; s->prof_n[k] = 0; }
     return EG_OK;
 }
 

@@ -47,6 +47,10 @@ for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         key = "thomas_s"
     elif k.startswith("eg::k_scale"):
         key = "scale"
+    elif k.startswith("eg::k_march<1, 1>"):
+        key = "phase_A"
+    elif k.startswith("eg::k_march<1, 2>"):
+        key = "phase_B"
     if key:
         traffic[key] = b / n
 open(out_txt, "w").write("\n".join(lines) + "\n")
