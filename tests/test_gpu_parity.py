@@ -225,7 +225,9 @@ def test_multirank_finaliser_path_bitwise_equal(mode, monkeypatch):
 
 
 MARCH_CASES = [gen.CONFIGS["C1"], RAGGED, FUSED_ODD, FUSED_THIN, gen.CONFIGS["C2"],
-               gen.Problem(388, 23, 70, seed=13)]   # 4 tiles (last one 4 columns wide), nz = 70
+               gen.Problem(388, 23, 70, seed=13),   # 4 tiles (last one 4 columns wide), nz = 70
+               gen.Problem(8, 5, 1, seed=14),       # one level: the Thomas solve is the identity
+               gen.Problem(132, 6, 72, seed=15)]    # the deepest column the fused kernels take
 
 
 @pytest.mark.parametrize("prob", MARCH_CASES, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
@@ -248,15 +250,28 @@ def test_fused_phases_match_unfused_schedule(prob, mode, strips, monkeypatch):
     monkeypatch.setenv("EG_NO_FUSE", "1")
     s2 = egs.Solver(g, bd, mode)
     monkeypatch.delenv("EG_NO_FUSE")
-    for tol, maxit in ((0.0, 8), (1e-5, 100)):
-        x1, i1, h1 = s1.solve(bt, tol=tol, maxit=maxit)
-        x2, i2, h2 = s2.solve(bt, tol=tol, maxit=maxit)
-        assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
+    # fixed iterations; to tolerance; with a restart every 3 iterations (fresh phase A each time)
+    for tol, maxit, rs in ((0.0, 8, 150), (1e-5, 100, 150), (0.0, 10, 3)):
+        x1, i1, h1 = s1.solve(bt, tol=tol, maxit=maxit, restart_every=rs)
+        x2, i2, h2 = s2.solve(bt, tol=tol, maxit=maxit, restart_every=rs)
+        assert i1.iters == i2.iters and i1.restarts == i2.restarts
+        assert np.array_equal(h1, h2) and torch.equal(x1, x2)
     for s, fused in ((s1, True), (s2, False)):
         s.profile_reset()
         s.solve(bt, tol=0.0, maxit=3, flags=egs.EG_SOLVE_PROFILE)
         p = s.profile()
         assert (p["phase_A"][1], p["phase_B"][1], p["thomas_p"][1]) == ((3, 3, 0) if fused else (0, 0, 3))
+
+
+@pytest.mark.parametrize("prob", [gen.Problem(130, 9, 70, seed=10), gen.Problem(64, 8, 73, seed=16)],
+                         ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+def test_fused_phases_fall_back_outside_their_domain(prob):
+    """nx % 4 != 0 (16-byte TMA strides) or nz > 72 (TMEM columns): the 5-kernel schedule runs."""
+    s, _, b = _make(prob, "mixed")
+    s.profile_reset()
+    s.solve(torch.from_numpy(b).cuda(), tol=0.0, maxit=2, flags=egs.EG_SOLVE_PROFILE)
+    p = s.profile()
+    assert p["phase_A"][1] == 0 and p["thomas_p"][1] == 2
 
 
 TRISOR_CASES = [gen.Problem(64, 48, 10, seed=0), gen.Problem(130, 9, 70, seed=10), gen.Problem(128, 37, 13, seed=11)]
