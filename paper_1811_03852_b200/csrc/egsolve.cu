@@ -98,7 +98,7 @@ struct eg_solver {
     void* vec[6]{};        // r, rh, p, v, s, t
     void* zext[2]{};       // ghosted z, zs (row -1 .. nyl)
     int* ready_flags = nullptr;  // [nyl][tiles] ready flags of the fused (marching) phase kernels
-    bool use_march = false;     // fused phases (fp32 working precision, one GPU; march.cuh)
+    bool use_march = false;     // fused phases (fp32 working precision; march.cuh)
     MarchGeo mg{};
     MarchMaps maps{};
     size_t smem_march = 0;
@@ -286,6 +286,12 @@ int iteration_fused(eg_solver* s, void* x_it) {
     int rc;
     if constexpr (MODE != 0) {
         const unsigned grid = (unsigned)(s->mg.strips * s->L.tiles);
+        const dim3 gedge((unsigned)s->L.tiles, 2u);
+        if (s->comm) {  // latitude bands: z of the band's edge rows -> the neighbours' ghost rows
+            k_edge_rows<MODE, 1><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.z);
+            CK(cudaGetLastError());
+            if ((rc = halo_ghosted(s, v.z))) return rc;
+        }
         {
             // the first iteration after a (re)start has p = v = 0: phase A then reads r only
             ProfScope ps(s, KID_PHASE_A, s->next_fresh ? alg_bytes(s, KID_PHASE_A) - 2.0 * s->L.vsz * s->L.n : -1.0);
@@ -294,6 +300,11 @@ int iteration_fused(eg_solver* s, void* x_it) {
             CK(cudaGetLastError());
         }
         if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
+        if (s->comm) {
+            k_edge_rows<MODE, 2><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.zs);
+            CK(cudaGetLastError());
+            if ((rc = halo_ghosted(s, v.zs))) return rc;
+        }
         {
             ProfScope ps(s, KID_PHASE_B);
             k_march<MODE, 2><<<grid, MA_THREADS, s->smem_march, s->st>>>(s->geo, v, s->mg, s->ready_flags, s->maps);
@@ -716,6 +727,8 @@ int set_thomas_smem(eg_solver* s) {
             CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
             CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
             CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
+            CK(cudaFuncSetAttribute(k_edge_rows<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
+            CK(cudaFuncSetAttribute(k_edge_rows<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
         }
     }
     return rc;
@@ -903,7 +916,7 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         // two stage rings (elimination / stencil inputs) share what the z ring leaves
         const int na = ring < budget ? (int)((budget - ring) / ma_stage_bytes(1)) : 0;
         const int nb = ring < budget ? (int)((budget - ring) / ma_stage_bytes(2)) : 0;
-        s->use_march = s->use_tm && s->comm == nullptr && grid->nx % 4 == 0 && nz8 <= 8 * MA_MAX_CH &&
+        s->use_march = s->use_tm && grid->nx % 4 == 0 && nz8 <= 8 * MA_MAX_CH &&
                        7 * nz8 <= 512 && s->L.tiles <= nsm && na >= 4 && !(nf && nf[0] == '1');
         if (s->use_march) {
             s->mg.fst_a = std::min(MA_MAX_STAGES, na - na / 2);

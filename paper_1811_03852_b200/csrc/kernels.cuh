@@ -463,7 +463,7 @@ __device__ __forceinline__ void tm_free128(uint32_t base) {
 // One 128-column tile of one latitude row: f = update(inputs), z = T^-1 f, with c'_k in this
 // thread's TMEM lane and y_k in shared memory ys[k][128].  All 128 threads of the CTA call it
 // (warp-collective TMEM access); `act` masks columns beyond nx.  KIND as in k_thomas.
-template <int MODE, int KIND>
+template <int MODE, int KIND, bool WRITE_F = true>
 __device__ __forceinline__ void thomas_tm_tile(const Geo& g, const Vecs<MODE>& vv, int64_t row_base, int i,
                                                bool act, uint32_t taddr, float* ys, float beta, float omega,
                                                float alpha, bool fresh, const float* __restrict__ fin,
@@ -523,7 +523,7 @@ __device__ __forceinline__ void thomas_tm_tile(const Geo& g, const Vecs<MODE>& v
                 if (KIND == 0) f = ca[e];
                 else if (KIND == 1) f = fmaf(beta, fmaf(-omega, cv[e], cp[e]), ca[e]);
                 else f = fmaf(-alpha, cv[e], ca[e]);
-                if (KIND != 0 && act) Pw[k * nx] = f;
+                if (KIND != 0 && WRITE_F && act) Pw[k * nx] = f;
                 const V u = cu[e].v[0], d = cu[e].v[1];
                 V c, y;
                 if (k == 0) {
@@ -588,6 +588,39 @@ __global__ void __launch_bounds__(128, 4) k_thomas_tm(Geo g, Vecs<MODE> vv, cons
     const int i = act ? i_raw : nx - 1;  // inactive lanes read a valid column, never store
     thomas_tm_tile<MODE, KIND>(g, vv, (int64_t)blockIdx.y * g.row, i, act, base + ((uint32_t)(warp * 32) << 16),
                                reinterpret_cast<float*>(smraw), beta, omega, alpha, fresh, fin, zout);
+    tm_free128(base);
+}
+
+// Multi-GPU fused schedule: z of the band's first and last local rows (those with a neighbouring
+// rank) ahead of the phase kernel, so that the rows can be exchanged into the neighbours' ghost
+// rows before it runs.  Same arithmetic as the phase kernel's elimination (which recomputes these
+// rows bitwise identically); p / s are not written here (phase A updates p in place).
+// grid (ceil(nx/128), 2): blockIdx.y 0 -> local row 0, 1 -> local row nyl-1.
+template <int MODE, int KIND>
+__global__ void __launch_bounds__(128, 4) k_edge_rows(Geo g, Vecs<MODE> vv, float* __restrict__ zout) {
+    static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ uint32_t tm_base;
+    const DevState* st = vv.st;
+    if (st->halt != H_RUN) return;
+    float beta = 0.f, omega = 0.f, alpha = 0.f;
+    bool fresh = false;
+    if (KIND == 1) {
+        fresh = st->fresh != 0;
+        beta = (float)st->beta_v;
+        omega = (float)st->omega_v;
+    } else {
+        alpha = (float)st->alpha_v;
+    }
+    const uint32_t base = tm_alloc128(&tm_base);
+    const int warp = threadIdx.x >> 5;
+    const int nx = (int)g.nx;
+    const int i_raw = blockIdx.x * 128 + threadIdx.x;
+    const bool act = i_raw < nx;
+    const int i = act ? i_raw : nx - 1;
+    const int64_t row = blockIdx.y == 0 ? 0 : g.nyl - 1;
+    thomas_tm_tile<MODE, KIND, false>(g, vv, row * g.row, i, act, base + ((uint32_t)(warp * 32) << 16),
+                                      reinterpret_cast<float*>(smraw), beta, omega, alpha, fresh, nullptr, zout);
     tm_free128(base);
 }
 

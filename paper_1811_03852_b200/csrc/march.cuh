@@ -28,6 +28,8 @@
 // work, so with all CTAs co-resident (grid <= #SMs, one CTA per SM) the march cannot deadlock.
 // The producer issues one TMA box (128 columns x MA_KB levels) per array per stage.
 // Requires: nx % 4 == 0 (16-byte TMA strides), 7 * ceil8(nz) <= 512 TMEM columns, tiles <= #SMs.
+// Multi-GPU: the band's first / last rows' neighbours are the ghost rows -1 / nyl of z, which the
+// host fills (k_edge_rows + NCCL) before the launch.
 #pragma once
 #include <cuda.h>  // CUtensorMap (the host encodes the maps through cudaGetDriverEntryPointByVersion)
 
@@ -489,8 +491,10 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             if (m == 0 || ld_next) {
                 if (tid == 0) {
                     if (m == 0) { wait_flag(j, tW); wait_flag(j, tE); }
-                    if (ld_prev) wait_flag(j - dir, t);
-                    if (ld_next) wait_flag(j + dir, t);
+                    // rows of a neighbouring rank sit in the ghost rows -1 / nyl, exchanged before
+                    // the launch: no flag
+                    if (ld_prev && j - dir >= 0 && j - dir < nyl) wait_flag(j - dir, t);
+                    if (ld_next && j + dir >= 0 && j + dir < nyl) wait_flag(j + dir, t);
                 }
                 cons_bar();
                 if (m == 0 && tid < nz) {

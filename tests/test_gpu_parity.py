@@ -219,6 +219,10 @@ def test_multirank_finaliser_path_bitwise_equal(mode, monkeypatch):
     monkeypatch.delenv("EG_FORCE_NCCL")
     x2, i2, h2 = s2.solve(torch.from_numpy(b).cuda(), tol=1e-6, maxit=100)
     assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
+    if mode == "mixed":  # the fused phases run on the multi-rank path too (edge rows + ghost rows)
+        s2.profile_reset()
+        s2.solve(torch.from_numpy(b).cuda(), tol=0.0, maxit=2, flags=egs.EG_SOLVE_PROFILE)
+        assert s2.profile()["phase_A"][1] == 2
     y1 = s1.apply(torch.ones(prob.n, dtype=s1.vdtype, device="cuda"))
     y2 = s2.apply(torch.ones(prob.n, dtype=s2.vdtype, device="cuda"))
     assert torch.equal(y1, y2)
