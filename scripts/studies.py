@@ -6,6 +6,9 @@
   timestep  NEXT-4: time-varying operator workflow: per "time step" the
             operator is rebuilt (a new seed) and 4 solves follow, each warm-started from the previous
             solution with a perturbed right-hand side.
+  trisor    NEXT-1 measured: iterations, time-to-solution and per-iteration cost of the red-black
+            tri-SOR preconditioner (sweeps, omega) against C^-1 = T^-1, on the C5 operator and on a
+            harder operator (the NEXT-2 knob) at C4 size; per-kernel times and algorithmic GB/s.
   precision NEXT-2: deep-convergence precision study: R_i histories of
             fp32 / mixed / fp64 run without a halting criterion (tol = 0) on a harder operator, with
             and without the mandatory restart.
@@ -138,6 +141,64 @@ def timestep(args):
             "mean_set_operator_ms": statistics.mean(r["set_operator_ms"] for r in rows if r["solve"] == 0)}
 
 
+def trisor(args):
+    cases = {
+        "C5": gen.CONFIGS["C5"],
+        "C4-hard": gen.CONFIGS["C4"].with_(cv=(args.cv_lo, args.cv_hi), dl=(args.dl_lo, args.dl_hi)),
+    }
+    pcs = [("tridiag", 0, 0.0), ("trisor", 1, 1.0), ("trisor", 2, 1.5), ("trisor", 3, 1.5)]
+    out = {"study": "NEXT-1 tri-SOR measured", "precision": args.precision,
+           "knob": f"C4-hard: c_v ~ U({args.cv_lo}, {args.cv_hi}), delta ~ U({args.dl_lo}, {args.dl_hi}) "
+                   "(not from the paper)", "cases": {}}
+    st = torch.cuda.Stream()
+    dev = torch.device("cuda")
+    for name, prob in cases.items():
+        rows = []
+        with torch.cuda.stream(st):
+            bands = torch.empty((7, prob.n), dtype=torch.float64, device=dev)
+            b = torch.empty(prob.n, dtype=torch.float64, device=dev)
+            x = torch.empty(prob.n, dtype=torch.float64, device=dev)
+            gen.device(prob, bands, b, stream=st)
+            s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, args.precision, stream=st)
+            for kind, sweeps, omega in pcs:
+                if kind == "tridiag":
+                    s.set_preconditioner("tridiag")
+                else:
+                    s.set_preconditioner("trisor", sweeps=sweeps, omega=omega)
+                row = {"precond": kind, "sweeps": sweeps, "omega": omega}
+                for tol in (1e-4, 1e-6):
+                    s.solve(b, tol=tol, maxit=args.maxit, out=x)  # warm-up (graph capture)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    torch.cuda.synchronize()
+                    e0.record(st)
+                    s.set_operator(bands)
+                    _, info, _ = s.solve(b, tol=tol, maxit=args.maxit, out=x)
+                    e1.record(st)
+                    torch.cuda.synchronize()
+                    row[f"{tol:g}"] = {"iters": info.iters, "ms": e0.elapsed_time(e1), "true_R": info.true_R,
+                                       "converged": info.converged, "restarts": info.restarts}
+                # per-iteration cost: fixed 8 iterations, per-kernel CUDA events
+                s.profile_reset()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(st)
+                _, info, _ = s.solve(b, tol=0.0, maxit=8, flags=egs.EG_SOLVE_PROFILE, out=x)
+                e1.record(st)
+                torch.cuda.synchronize()
+                prof = s.profile()
+                row["fixed8_ms"] = e0.elapsed_time(e1)
+                row["kernels"] = {k: {"launches": v[1], "avg_ms": v[0] / v[1],
+                                      "alg_GBps": v[2] / (v[0] / v[1] / 1e3) / 1e9}
+                                  for k, v in prof.items() if v[1] > 0}
+                per_it = sum(v[0] for k, v in prof.items() if k not in ("start",)) / 8
+                row["ms_per_iteration"] = per_it
+                rows.append(row)
+        out["cases"][name] = {"grid": [prob.nx, prob.ny, prob.nz], "rows": rows}
+        del s, bands, b, x
+        torch.cuda.empty_cache()
+    return out
+
+
 def precision(args):
     """Deep convergence without a halting criterion on a harder operator
     (knob, not from the paper: c_v ~ U(cv_lo, cv_hi), delta ~ U(dl_lo, dl_hi)).  For each mode and
@@ -180,7 +241,7 @@ def precision(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("study", choices=["table1", "timestep", "precision"])
+    ap.add_argument("study", choices=["table1", "timestep", "precision", "trisor"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--dates", type=int, default=11)
     ap.add_argument("--seed0", type=int, default=4)
@@ -198,7 +259,7 @@ def main():
     ap.add_argument("--true-stride", type=int, default=2)
     a = ap.parse_args()
     t0 = time.time()
-    out = {"table1": table1, "timestep": timestep, "precision": precision}[a.study](a)
+    out = {"table1": table1, "timestep": timestep, "precision": precision, "trisor": trisor}[a.study](a)
     out["wall_s"] = time.time() - t0
     out["device"] = torch.cuda.get_device_name()
     print(json.dumps(out))
