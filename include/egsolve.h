@@ -101,6 +101,17 @@ typedef struct {
  * band and precision (PyTorch owns all device memory).  Returns EG_OK or EG_ERR_ARG. */
 int eg_workspace_bytes(const eg_grid* grid, const eg_dist* dist, eg_precision prec, size_t* bytes);
 
+/* Same, for a solver that will also use optional features.  features: bit mask of
+ *   EG_FEATURE_TRISOR: room for colour-split copies of the scaled bands and of the preconditioner's
+ *     right-hand side (7 working-precision values per point), which the red-black tri-SOR sweeps
+ *     (EG_PRECOND_TRISOR) read instead of every other value of the natural-order arrays.  A solver
+ *     whose workspace is at least this size uses them; a smaller workspace still runs tri-SOR, on
+ *     the natural-order arrays (same results, bitwise).
+ * features = 0 gives eg_workspace_bytes.  Returns EG_OK or EG_ERR_ARG. */
+#define EG_FEATURE_TRISOR 1u
+int eg_workspace_bytes_ex(const eg_grid* grid, const eg_dist* dist, eg_precision prec, uint32_t features,
+                          size_t* bytes);
+
 /* a1 — create a solver: scales the operator "outside the solver" (Eq. 5):
  * Ahat_d = a_d / a_C (binary64 IEEE division, then rounded to the working precision), the fp64
  * diagonal kept for scaling b.  bands[7]: DEVICE fp64 arrays of the local rows (layout above);

@@ -20,11 +20,12 @@ _SO = os.environ.get("EGSOLVE_LIB") or os.path.join(_HERE, "libegsolve.so")  # o
 EG_FP64, EG_MIXED, EG_FP32 = 0, 1, 2
 PRECISIONS = {"fp64": EG_FP64, "mixed": EG_MIXED, "fp32": EG_FP32}
 EG_SOLVE_NO_GRAPH, EG_SOLVE_PROFILE = 1, 2
+EG_FEATURE_TRISOR = 1
 STATUS = {0: "EG_OK", 1: "EG_ERR_ARG", 2: "EG_ERR_SINGULAR_DIAG", 3: "EG_ERR_DEGENERATE_RHS",
           4: "EG_ERR_BREAKDOWN", 5: "EG_ERR_NONFINITE", 6: "EG_ERR_CUDA", 7: "EG_ERR_NCCL",
           8: "EG_ERR_WORKSPACE"}
 # symbols declared in include/egsolve.h (tests check the library exports all of them)
-ABI_SYMBOLS = ("eg_workspace_bytes", "eg_solver_create", "eg_solver_set_operator",
+ABI_SYMBOLS = ("eg_workspace_bytes", "eg_workspace_bytes_ex", "eg_solver_create", "eg_solver_set_operator",
                "eg_solver_set_preconditioner", "eg_apply_operator", "eg_precondition",
                "eg_solve", "eg_solver_destroy", "eg_last_error", "eg_status_str",
                "eg_nccl_unique_id", "eg_num_kernels", "eg_kernel_name", "eg_profile_get",
@@ -83,6 +84,8 @@ def lib():
         vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
         L.eg_workspace_bytes.argtypes = [ctypes.POINTER(_Grid), ctypes.POINTER(_Dist), i32,
                                          ctypes.POINTER(ctypes.c_size_t)]
+        L.eg_workspace_bytes_ex.argtypes = [ctypes.POINTER(_Grid), ctypes.POINTER(_Dist), i32,
+                                            ctypes.c_uint32, ctypes.POINTER(ctypes.c_size_t)]
         L.eg_solver_create.argtypes = [ctypes.POINTER(_Grid), ctypes.POINTER(_Dist),
                                        ctypes.POINTER(vp), i32, vp, ctypes.c_size_t, vp,
                                        ctypes.POINTER(vp)]
@@ -144,7 +147,9 @@ class Solver:
     torch.distributed process group for a latitude-band decomposition (one rank per GPU).
     """
 
-    def __init__(self, grid, bands, precision="mixed", group=None, stream=None):
+    def __init__(self, grid, bands, precision="mixed", group=None, stream=None, trisor=False):
+        """trisor=True sizes the workspace for the colour-split tri-SOR copies (EG_FEATURE_TRISOR);
+        set_preconditioner("trisor") works either way, faster with them."""
         import torch
         self.grid = tuple(int(v) for v in grid)
         nx, ny, nz = self.grid
@@ -177,9 +182,10 @@ class Solver:
         assert tuple(bands.shape) == (7, self.n_local), (tuple(bands.shape), self.n_local)
         self._grid = _Grid(nx, ny, nz)
         nbytes = ctypes.c_size_t()
-        rc = lib().eg_workspace_bytes(ctypes.byref(self._grid), dptr, self.mode, ctypes.byref(nbytes))
+        rc = lib().eg_workspace_bytes_ex(ctypes.byref(self._grid), dptr, self.mode,
+                                         EG_FEATURE_TRISOR if trisor else 0, ctypes.byref(nbytes))
         if rc:
-            raise EgError(rc, "eg_workspace_bytes")
+            raise EgError(rc, "eg_workspace_bytes_ex")
         self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
         ptrs = (ctypes.c_void_p * 7)(*[bands[d].data_ptr() for d in range(7)])
         h = ctypes.c_void_p()

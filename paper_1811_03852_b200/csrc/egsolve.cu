@@ -35,7 +35,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
     size_t off_bands, off_diag, off_bhat, off_x64, off_x32, off_xg, off_vec, off_z, off_pv, off_slots,
-        off_gsum, off_state, total;
+        off_gsum, off_state, base_total, off_split, total;
     size_t vsz;      // sizeof(V)
     size_t xsz;      // sizeof(X)
     int64_t n, row, nyl;
@@ -45,7 +45,7 @@ struct Layout {
 int vsize(int mode) { return mode == EG_FP64 ? 8 : 4; }
 int xsize(int mode) { return mode == EG_FP32 ? 4 : 8; }
 
-bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L) {
+bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t features = 0) {
     const size_t A = 256;
     L->row = g->nx * g->nz;
     L->nyl = nyl;
@@ -69,6 +69,9 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L) {
     L->off_slots = o; o = align_up(o + 3 * (size_t)nyl * L->tiles * 8, A);
     L->off_gsum = o;  o = align_up(o + 2 * 8 * 3 * 8, A);
     L->off_state = o; o = align_up(o + sizeof(DevState), A);
+    L->base_total = o;
+    // EG_FEATURE_TRISOR: colour-split (E,W,N,S), (U,D) and f for the red-black tri-SOR sweeps
+    L->off_split = o; if (features & EG_FEATURE_TRISOR) o = align_up(o + 7 * n * L->vsz, A);
     L->total = o;
     return true;
 }
@@ -104,6 +107,8 @@ struct eg_solver {
     size_t smem_march = 0;
     int epoch_base = 1;         // first epoch of the next solve (flags are never reset)
     int precond = EG_PRECOND_TRIDIAG;  // NEXT-1: EG_PRECOND_TRISOR selects red-black tri-SOR
+    void* split = nullptr;             // colour-split B4 | B2 | f for tri-SOR (NULL: not available)
+    bool split_valid = false;          // the split bands match the current operator
     int sor_sweeps = 3;
     double sor_omega = 1.5;
     double* slots = nullptr;
@@ -175,6 +180,7 @@ cudaEvent_t take_event(eg_solver* s) {
 }
 
 double alg_bytes(const eg_solver* s, int kid);
+double sor_alg_bytes(const eg_solver* s, int kind, int sweep, int colour);
 
 struct ProfScope {
     eg_solver* s;
@@ -331,15 +337,27 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
     const dim3 gs((unsigned)((s->grid.nx / 2 + s->wth - 1) / s->wth), (unsigned)s->L.nyl);
     const V* fsrc = KIND == 0 ? fin : (KIND == 1 ? v.p : v.s);
     int rc;
+    Split<V> sp{nullptr, nullptr, nullptr};
+    if (s->split) {  // colour-split bands (refreshed after every set_operator) and f
+        V* b4s = (V*)s->split;
+        V* b2s = b4s + 4 * s->L.n;
+        if (!s->split_valid) {
+            const dim3 grid((unsigned)((s->grid.nx + 255) / 256), (unsigned)s->grid.nz, (unsigned)s->L.nyl);
+            k_split_bands<V><<<grid, 256, 0, s->st>>>(s->geo, v.B4, v.B2, b4s, b2s);
+            CK(cudaGetLastError());
+            s->split_valid = true;
+        }
+        sp = Split<V>{b4s, b2s, b2s + 2 * s->L.n};
+    }
     for (int sw = 0; sw < s->sor_sweeps; ++sw)
         for (int colour = 0; colour < 2; ++colour) {
             {
-                ProfScope ps(s, KID_SOR);
+                ProfScope ps(s, KID_SOR, sor_alg_bytes(s, KIND, sw, colour));
                 if (sw == 0)
-                    k_sor_half<MODE, KIND, true><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, colour, s->sor_omega, 0);
+                    k_sor_half<MODE, KIND, true><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, colour, s->sor_omega, 0, sp);
                 else
                     k_sor_half<MODE, 0, false><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fsrc, z, colour, s->sor_omega,
-                                                                                   KIND != 0);
+                                                                                   KIND != 0, sp);
                 CK(cudaGetLastError());
             }
             if ((rc = halo_ghosted(s, z))) return rc;
@@ -643,6 +661,7 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
 template <int MODE>
 int create_impl(eg_solver* s, const double* const bands[7]) {
     using V = typename Prec<MODE>::V;
+    s->split_valid = false;  // the colour-split bands are re-derived on the next tri-SOR sweep
     Bands7 in;
     for (int d = 0; d < 7; ++d) in.b[d] = bands[d];
     int* err = (int*)&s->dstate->err;
@@ -785,6 +804,18 @@ bool valid_grid(const eg_grid* g) {
            g->ny < 65536 && g->nz < 65536;
 }
 
+// algorithmic HBM bytes of one red-black tri-SOR half-sweep, per grid point in units
+// of V: the colour's f (or the inputs of its update) and bands, the values of x it reads, the
+// colour's x (and p / s, and the colour-split f) it writes.  Layout independent: the colour-split
+// copies change how much of each loaded sector is used, not what the sweep needs.
+double sor_alg_bytes(const eg_solver* s, int kind, int sweep, int colour) {
+    const double V = (double)s->L.vsz, n = (double)s->L.n;
+    if (sweep > 0) return 5 * V * n;                                   // f, 6 bands / 2; x; x / 2
+    const double fin = kind == 0 ? 0.5 : (kind == 1 ? 1.5 : 1.0);     // fin | r, p, v | r, v (one colour)
+    const double out = 0.5 + (kind != 0 ? 0.5 : 0.0) + (s->split ? 0.5 : 0.0);  // x, p / s, f split
+    return (fin + (colour == 0 ? 1.0 : 3.0 + 0.5) + out) * V * n;      // red: (U,D) only; black: + (E,W,N,S), red x
+}
+
 // algorithmic HBM bytes of one launch, V = vector / band bytes, X = x bytes
 double alg_bytes(const eg_solver* s, int kid) {
     const double V = (double)s->L.vsz, X = (double)s->L.xsz, n = (double)s->L.n;
@@ -802,7 +833,7 @@ double alg_bytes(const eg_solver* s, int kid) {
         case KID_CONVERT: per = 12; break;
         case KID_PHASE_A: per = 4 * V + 6 * V + 3 * V; break;      // r,p,v,rhat0 + B4,B2; p',z,v'
         case KID_PHASE_B: per = 2 * V + 6 * V + 3 * V; break;      // r,v' + B4,B2; s,z_s,t
-        case KID_SOR: per = 0.5 * (V + V + 4 * V + 6 * V + V); break;  // half the points: f, x, 4 nbrs, bands; x
+        case KID_SOR: per = 5 * V; break;  // a later sweep's half: f, bands of one colour; all of x; x of one colour
         default: per = 0;
     }
     return per * n;
@@ -825,6 +856,19 @@ int eg_workspace_bytes(const eg_grid* grid, const eg_dist* dist, eg_precision pr
     return EG_OK;
 }
 
+int eg_workspace_bytes_ex(const eg_grid* grid, const eg_dist* dist, eg_precision prec, uint32_t features,
+                          size_t* bytes) {
+    int64_t jb, je;
+    int rank, nranks;
+    if (!valid_grid(grid) || !bytes || prec < EG_FP64 || prec > EG_FP32 || (features & ~EG_FEATURE_TRISOR))
+        return EG_ERR_ARG;
+    if (!valid_dist(grid, dist, &jb, &je, &rank, &nranks)) return EG_ERR_ARG;
+    Layout L;
+    make_layout(grid, je - jb, prec, &L, features);
+    *bytes = L.total;
+    return EG_OK;
+}
+
 int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* const bands[7],
                      eg_precision prec, void* workspace, size_t workspace_bytes, void* stream,
                      eg_solver** out) {
@@ -842,8 +886,9 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         delete s;
         return EG_ERR_ARG;
     }
-    make_layout(grid, s->j_end - s->j_begin, prec, &s->L);
-    if (workspace_bytes < s->L.total || ((uintptr_t)workspace & 255)) {
+    make_layout(grid, s->j_end - s->j_begin, prec, &s->L, EG_FEATURE_TRISOR);
+    const bool room_split = workspace_bytes >= s->L.total && grid->nx % 2 == 0;
+    if (workspace_bytes < s->L.base_total || ((uintptr_t)workspace & 255)) {
         delete s;
         return EG_ERR_WORKSPACE;
     }
@@ -860,6 +905,7 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     for (int d = 0; d < 2; ++d)
         s->zext[d] = s->ws + L.off_z + (size_t)d * align_up((L.n + 2 * L.row) * L.vsz, 256);
     s->ready_flags = (int*)(s->ws + L.off_pv);
+    s->split = room_split ? (void*)(s->ws + L.off_split) : nullptr;
     s->slots = (double*)(s->ws + L.off_slots);
     s->gsum = (double*)(s->ws + L.off_gsum);
     s->gall = s->gsum + 8 * 3;

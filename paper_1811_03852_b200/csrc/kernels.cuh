@@ -635,10 +635,32 @@ __global__ void __launch_bounds__(128, 4) k_edge_rows(Geo g, Vecs<MODE> vv, floa
 // (rhs = omega f); with KIND 1 / 2 the first sweep also forms f = p (or s) for its colour's columns
 // and stores it (later sweeps read it back with KIND 0).  Thread m of row j owns column
 // i = 2m + ((j + colour) & 1); grid (ceil(nx/2 / W), nyl), dynamic smem 2*nz*W*sizeof(V).
+// Colour-split copies (EG_FEATURE_TRISOR): split[c] holds, per (row, level), the nx/2 values of
+// the columns of colour c in order, so a half-sweep thread m reads split + (jl*nz*nx +
+// c*nx/2 + m) + k*nx: every loaded sector is used, where the natural arrays waste half of each.
+template <class V>
+struct Split {
+    const V* b4;  // (E, W, N, S) per point, colour-split
+    const V* b2;  // (U, D)
+    V* f;         // the sweep's right-hand side (written by the first sweep, read by the others)
+};
+
+template <class V>
+__global__ void __launch_bounds__(256) k_split_bands(Geo g, const V* __restrict__ B4, const V* __restrict__ B2,
+                                                     V* __restrict__ B4s, V* __restrict__ B2s) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.nx) return;
+    const int64_t k = blockIdx.y, jl = blockIdx.z, jg = g.j0 + jl;
+    const int64_t q = jl * g.row + k * g.nx + i;
+    const int64_t qs = jl * g.row + k * g.nx + ((i + jg) & 1) * (g.nx / 2) + (i >> 1);
+    stv<4>(B4s + 4 * qs, ldv<4>(B4 + 4 * q));
+    stv<2>(B2s + 2 * qs, ldv<2>(B2 + 2 * q));
+}
+
 template <int MODE, int KIND, bool FIRST>
 __global__ void __launch_bounds__(128) k_sor_half(Geo g, Vecs<MODE> vv, const typename Prec<MODE>::V* __restrict__ fin,
                                                   typename Prec<MODE>::V* __restrict__ x, int colour,
-                                                  double omega_d, int check_halt) {
+                                                  double omega_d, int check_halt, Split<typename Prec<MODE>::V> sp) {
     using V = typename Prec<MODE>::V;
     constexpr int KB = sizeof(V) == 4 ? 4 : 2;
     constexpr int NA = 13;  // f, x(k), x(k+1) [own], xE, xW, xN, xS, E, W, N, S, U, D
@@ -676,13 +698,16 @@ __global__ void __launch_bounds__(128) k_sor_half(Geo g, Vecs<MODE> vv, const ty
     // other colour, so it is already written even in the first sweep (the own column is not)
     const V* __restrict__ xN = (jg < g.ny - 1) ? xc + g.row : xE;
     const V* __restrict__ xS = (jg > 0) ? xc - g.row : xE;
-    const V* __restrict__ b4 = vv.B4 + 4 * (rb + i);
-    const V* __restrict__ b2 = vv.B2 + 2 * (rb + i);
-    const V* __restrict__ A0 = (KIND == 0 ? fin : vv.r) + rb + i;
+    const bool split = sp.b4 != nullptr;  // uniform
+    const int64_t qs = rb + (int64_t)colour * (nx / 2) + m;  // colour-split index (per-level stride nx)
+    const V* __restrict__ b4 = split ? sp.b4 + 4 * qs : vv.B4 + 4 * (rb + i);
+    const V* __restrict__ b2 = split ? sp.b2 + 2 * qs : vv.B2 + 2 * (rb + i);
+    const V* __restrict__ A0 = (!FIRST && split) ? sp.f + qs : (KIND == 0 ? fin : vv.r) + rb + i;
     const V* __restrict__ Pp = (KIND == 1 && fresh ? vv.r : vv.p) + rb + i;
     const V* __restrict__ Vv = (KIND == 1 && fresh ? vv.r : vv.v) + rb + i;
     if (KIND == 1 && fresh) beta = 0;
     V* __restrict__ Fw = (KIND == 1 ? vv.p : vv.s) + rb + i;
+    V* __restrict__ Fs = split ? sp.f + qs : nullptr;
     V* __restrict__ Xw = x + rb + i;
     const bool need_nbr = !(FIRST && colour == 0);
     V cur[KB][NA], nxt[KB][NA];
@@ -721,6 +746,7 @@ __global__ void __launch_bounds__(128) k_sor_half(Geo g, Vecs<MODE> vv, const ty
             if (k < nz) {
                 const V f = cur[e][0];
                 if (FIRST && KIND != 0) Fw[k * nx] = f;
+                if (FIRST && split) Fs[k * nx] = f;  // the later sweeps read f colour-split
                 V rhs;
                 V hx = 0;
                 if (need_nbr) {

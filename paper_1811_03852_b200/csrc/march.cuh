@@ -180,6 +180,16 @@ __device__ unsigned long long g_ma_trace[1024 * 16];
 #define MA_ADD(slot, t0)
 #endif
 
+// tcgen05 accesses of one warp role are ordered against the other role's through the mbarriers
+// only with these fences (a run-to-run race at full size without them: scripts/stress_march.py)
+#ifdef MA_NO_TMEM_FENCE
+#define MA_TFENCE_BEFORE()
+#define MA_TFENCE_AFTER()
+#else
+#define MA_TFENCE_BEFORE() asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory")
+#define MA_TFENCE_AFTER() asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory")
+#endif
+
 struct MarchGeo {
     int strips;                  // latitude strips; grid = strips * tiles CTAs
     int fst_a, sst_a;            // phase A: stages of the elimination / stencil input rings
@@ -397,6 +407,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             if (sync_step >= 0) {  // the S warps read U, D, s (TMEM slot us) and z(r_{m-1}) of this chunk
                 MA_CLK(t1);
                 mbar_wait(&sread[c], (uint32_t)(sync_step & 1));
+                MA_TFENCE_AFTER();
                 MA_ADD(13, t1);
             }
 #pragma unroll
@@ -433,10 +444,14 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                         if (act && k0 + e < nz) __stcg(zk + e * nx, yb[e]);
                 }
             }
+            // TMEM writes of this row (U, D, s) are ordered before the S warps' reads by the fence
+            MA_TFENCE_BEFORE();
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&zready[x & 1]);  // the S warps may read z(r_x) from the ring
-                mbar_arrive(&zdone[x & 1]);   // the publisher may release the ready flag
+                // the publisher may release the ready flag: this arrival (release, CTA scope) and
+                // its wait (acquire) order these z stores before its gpu-scope release of the flag
+                mbar_arrive(&zdone[x & 1]);
             }
             MA_ADD(14, t0);
         };
@@ -480,6 +495,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             MA_CLK(t_z);
             if (m == 0) mbar_wait(&zready[0], 0u);
             if (m + 1 < L) mbar_wait(&zready[(m + 1) & 1], (uint32_t)(((m + 1) >> 1) & 1));
+            MA_TFENCE_AFTER();
             MA_ADD(5, t_z);
             float* zC0 = slot_ptr(m);
             float* zN0 = hasN ? (dir > 0 ? slot_ptr(m + 1) : slot_ptr(m - 1)) : zC0;
@@ -570,6 +586,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 }
                 zc[KB] = zC[min(k0 + KB, nz - 1) * MA_RING_W];
                 tm_wait_ld();
+                MA_TFENCE_BEFORE();
                 __syncwarp();
                 if (lane == 0) {
 #pragma unroll

@@ -159,7 +159,7 @@ def trisor(args):
             b = torch.empty(prob.n, dtype=torch.float64, device=dev)
             x = torch.empty(prob.n, dtype=torch.float64, device=dev)
             gen.device(prob, bands, b, stream=st)
-            s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, args.precision, stream=st)
+            s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, args.precision, stream=st, trisor=True)
             for kind, sweeps, omega in pcs:
                 if kind == "tridiag":
                     s.set_preconditioner("tridiag")

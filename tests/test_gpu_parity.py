@@ -285,15 +285,19 @@ TRISOR_CASES = [gen.Problem(64, 48, 10, seed=0), gen.Problem(130, 9, 70, seed=10
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("sweeps,omega", [(1, 1.0), (3, 1.5)])
 def test_trisor_precondition_parity(prob, mode, sweeps, omega):
-    """NEXT-1: the GPU red-black tri-SOR sweeps against the oracle's Eq. 7 sweeps."""
+    """NEXT-1: the GPU red-black tri-SOR sweeps against the oracle's Eq. 7 sweeps, on the natural
+    arrays and on the colour-split copies (EG_FEATURE_TRISOR), which give bitwise the same z."""
     s, bands, _ = _make(prob, mode)
     s.set_preconditioner("trisor", sweeps=sweeps, omega=omega)
     g = (prob.nx, prob.ny, prob.nz)
     ahat, _ = oracle.scale(g, bands, mode)
     f = np.random.default_rng(3).standard_normal(prob.n).astype(_vnp(mode))
-    z = s.precondition(torch.from_numpy(f).cuda()).cpu().numpy().astype(np.float64)
+    z = s.precondition(torch.from_numpy(f).cuda())
     zo = oracle.trisor(g, "fp64", ahat, f.astype(np.float64), sweeps=sweeps, omega=omega)
-    assert _rel(z, zo) <= (1e-12 if mode == "fp64" else 1e-5)
+    assert _rel(z.cpu().numpy().astype(np.float64), zo) <= (1e-12 if mode == "fp64" else 1e-5)
+    st = egs.Solver(g, torch.from_numpy(bands).cuda(), mode, trisor=True)
+    st.set_preconditioner("trisor", sweeps=sweeps, omega=omega)
+    assert torch.equal(st.precondition(torch.from_numpy(f).cuda()), z)
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -308,8 +312,36 @@ def test_trisor_solve_parity(mode):
     x, info, h = s.solve(torch.from_numpy(b).cuda(), tol=tol, maxit=200)
     assert info.converged and io.converged and abs(info.iters - io.iters) <= 2 and info.true_R < tol
     assert _rel(x.cpu().numpy(), xo) <= 10 * tol
+    st = egs.Solver(g, torch.from_numpy(bands).cuda(), mode, trisor=True)   # colour-split copies
+    st.set_preconditioner("trisor", sweeps=3, omega=1.5)
+    xs, infos, hs = st.solve(torch.from_numpy(b).cuda(), tol=tol, maxit=200)
+    assert infos.iters == info.iters and np.array_equal(hs, h) and torch.equal(xs, x)
+    st.set_operator(torch.from_numpy(bands).cuda() * 2.0)   # new operator -> split copies refreshed
+    xs2, infos2, _ = st.solve(torch.from_numpy(b).cuda() * 2.0, tol=tol, maxit=200)
+    assert infos2.iters == info.iters and torch.equal(xs2, x)  # (2A) x = 2b: same scaled system
     s.set_preconditioner("tridiag")
     _, info1, _ = s.solve(torch.from_numpy(b).cuda(), tol=tol, maxit=200)
     assert info.iters < info1.iters      # the paper's preconditioner is the stronger one
     with pytest.raises(egs.EgError):
         _make(gen.Problem(65, 4, 4, seed=1), mode)[0].set_preconditioner("trisor")   # odd nx
+
+
+def test_fused_phases_repeatable_at_scale(monkeypatch):
+    """Race check of the fused phase kernels on a multi-strip grid (C3: 5 tiles x 29 strips of
+    ~17 rows): repeated solves, each with a new output buffer (so the iteration graph is
+    re-captured), are bitwise identical to one another and to the 5-kernel schedule."""
+    prob = gen.CONFIGS["C3"]
+    bands = torch.empty((7, prob.n), dtype=torch.float64, device="cuda")
+    b = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    gen.device(prob, bands, b)
+    g = (prob.nx, prob.ny, prob.nz)
+    monkeypatch.setenv("EG_NO_FUSE", "1")
+    ref = egs.Solver(g, bands, "mixed")
+    monkeypatch.delenv("EG_NO_FUSE")
+    x0, i0, h0 = ref.solve(b, tol=1e-6, maxit=200)
+    s = egs.Solver(g, bands, "mixed")
+    keep = []
+    for _ in range(6):
+        x, info, h = s.solve(b, tol=1e-6, maxit=200)
+        keep.append(x)
+        assert info.iters == i0.iters and np.array_equal(h, h0) and torch.equal(x, x0)
