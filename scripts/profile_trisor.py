@@ -23,8 +23,8 @@ with torch.cuda.stream(st):
     bands = torch.empty((7, prob.n), dtype=torch.float64, device="cuda")
     b = torch.empty(prob.n, dtype=torch.float64, device="cuda")
     gen.device(prob, bands, b, stream=st)
-    s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, "mixed", stream=st)
-    s.set_preconditioner("trisor", sweeps=a.sweeps, omega=a.omega)
+    s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, "mixed", stream=st, trisor=True)
+    s.set_preconditioner("trisor", sweeps=a.sweeps, omega=a.omega)  # (colour-split copies: trisor=True)
     x, info, hist = s.solve(b, tol=0.0, maxit=a.maxit, flags=egs.EG_SOLVE_NO_GRAPH)
 torch.cuda.synchronize()
 print("iters", info.iters, "hist", list(hist))
