@@ -284,6 +284,32 @@ int finalize(eg_solver* s, int first, int tiles = 0) {
     return EG_OK;
 }
 
+#ifdef MA_VERIFY
+// debug builds: after every fused phase kernel, recompute its outputs with the 5-kernel kernels on
+// copies and count bitwise mismatches per array (0 z, 1 p, 2 v, 3 s, 4 z_s, 5 t, 6 slots)
+__device__ unsigned long long g_vfy_cnt[8];
+__device__ long long g_vfy_rec[256];
+__device__ int g_vfy_nrec;
+template <class T>
+__global__ void k_vfy_cmp(const T* __restrict__ a, const T* __restrict__ b, int64_t n, int id) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const bool same = sizeof(T) == 4 ? __float_as_uint((float)a[q]) == __float_as_uint((float)b[q])
+                                         : __double_as_longlong((double)a[q]) == __double_as_longlong((double)b[q]);
+        if (!same) {
+            atomicAdd(&g_vfy_cnt[id], 1ull);
+            const int r = atomicAdd(&g_vfy_nrec, 1);
+            if (r < 64) {
+                g_vfy_rec[4 * r] = id; g_vfy_rec[4 * r + 1] = q;
+                g_vfy_rec[4 * r + 2] = __double_as_longlong((double)a[q]);
+                g_vfy_rec[4 * r + 3] = __double_as_longlong((double)b[q]);
+            }
+        }
+    }
+}
+struct VfyBufs { float *p, *v, *z, *s, *zs, *t; double* slots; int64_t n; };
+VfyBufs g_vfy{};
+#endif
+
 // -------- the iteration (rows a3-a10) --------
 // fused schedule: phase A (a3 + a4), phase B (a6 + a7), update (a9), three finalisers
 template <int MODE>
@@ -298,6 +324,15 @@ int iteration_fused(eg_solver* s, void* x_it) {
             CK(cudaGetLastError());
             if ((rc = halo_ghosted(s, v.z))) return rc;
         }
+#ifdef MA_VERIFY
+        const int64_t n = s->L.n;
+        if (g_vfy.n != n) return fail(s, EG_ERR_CUDA, "MA_VERIFY buffers not allocated for this size");
+        CK(cudaMemcpyAsync(g_vfy.p, v.p, n * 4, cudaMemcpyDeviceToDevice, s->st));
+        CK(cudaMemcpyAsync(g_vfy.v, v.v, n * 4, cudaMemcpyDeviceToDevice, s->st));
+        const dim3 gtm_((unsigned)((s->grid.nx + 127) / 128), (unsigned)s->L.nyl);
+        const dim3 gr_((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+        const int64_t nsl = (int64_t)s->L.nyl * s->L.tiles;
+#endif
         {
             // the first iteration after a (re)start has p = v = 0: phase A then reads r only
             ProfScope ps(s, KID_PHASE_A, s->next_fresh ? alg_bytes(s, KID_PHASE_A) - 2.0 * s->L.vsz * s->L.n : -1.0);
@@ -305,6 +340,19 @@ int iteration_fused(eg_solver* s, void* x_it) {
             k_march<MODE, 1><<<grid, MA_THREADS, s->smem_march, s->st>>>(s->geo, v, s->mg, s->ready_flags, s->maps);
             CK(cudaGetLastError());
         }
+#ifdef MA_VERIFY
+        {
+            Vecs<MODE> w = v;
+            w.p = (typename Prec<MODE>::V*)g_vfy.p; w.v = (typename Prec<MODE>::V*)g_vfy.v; w.slots = g_vfy.slots;
+            k_thomas_tm<MODE, 1><<<gtm_, 128, s->smem_tm, s->st>>>(s->geo, w, nullptr, (typename Prec<MODE>::V*)g_vfy.z);
+            k_stencil<MODE, 1><<<gr_, RW, 0, s->st>>>(s->geo, w, (typename Prec<MODE>::V*)g_vfy.z, w.v, w.rh);
+            k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.z, g_vfy.z, n, 0);
+            k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.p, g_vfy.p, n, 1);
+            k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.v, g_vfy.v, n, 2);
+            k_vfy_cmp<double><<<64, 256, 0, s->st>>>(v.slots, g_vfy.slots, nsl, 6);
+            CK(cudaGetLastError());
+        }
+#endif
         if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
         if (s->comm) {
             k_edge_rows<MODE, 2><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.zs);
@@ -316,6 +364,20 @@ int iteration_fused(eg_solver* s, void* x_it) {
             k_march<MODE, 2><<<grid, MA_THREADS, s->smem_march, s->st>>>(s->geo, v, s->mg, s->ready_flags, s->maps);
             CK(cudaGetLastError());
         }
+#ifdef MA_VERIFY
+        {
+            Vecs<MODE> w = v;
+            w.s = (typename Prec<MODE>::V*)g_vfy.s; w.slots = g_vfy.slots;
+            k_thomas_tm<MODE, 2><<<gtm_, 128, s->smem_tm, s->st>>>(s->geo, w, nullptr, (typename Prec<MODE>::V*)g_vfy.zs);
+            k_stencil<MODE, 2><<<gr_, RW, 0, s->st>>>(s->geo, w, (typename Prec<MODE>::V*)g_vfy.zs,
+                                                     (typename Prec<MODE>::V*)g_vfy.t, w.s);
+            k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.s, g_vfy.s, n, 3);
+            k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.zs, g_vfy.zs, n, 4);
+            k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.t, g_vfy.t, n, 5);
+            k_vfy_cmp<double><<<64, 256, 0, s->st>>>(v.slots, g_vfy.slots, 3 * nsl, 6);
+            CK(cudaGetLastError());
+        }
+#endif
         if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
         const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
         {
@@ -993,6 +1055,16 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
                 s->use_march = false;
         }
     }
+#ifdef MA_VERIFY
+    if (rc == EG_OK && g_vfy.n != s->L.n) {
+        const int64_t n = s->L.n;
+        g_vfy.n = n;
+        if (cudaMalloc(&g_vfy.p, 6 * n * sizeof(float)) != cudaSuccess ||
+            cudaMalloc(&g_vfy.slots, 3 * s->L.nyl * s->L.tiles * sizeof(double)) != cudaSuccess)
+            rc = EG_ERR_CUDA;
+        g_vfy.v = g_vfy.p + n; g_vfy.z = g_vfy.v + n; g_vfy.s = g_vfy.z + n; g_vfy.zs = g_vfy.s + n; g_vfy.t = g_vfy.zs + n;
+    }
+#endif
     if (rc == EG_OK)
         rc = prec == EG_FP64 ? create_impl<0>(s, bands) : prec == EG_MIXED ? create_impl<1>(s, bands) : create_impl<2>(s, bands);
     if (rc != EG_OK) {
@@ -1111,6 +1183,22 @@ int eg_debug_march_trace(unsigned long long* out, int n) {
     return cudaMemcpyFromSymbol(out, g_ma_trace, (size_t)n * sizeof(unsigned long long)) == cudaSuccess ? 0 : EG_ERR_CUDA;
 }
 #endif
+
+
+#ifdef MA_VERIFY
+int eg_debug_verify(unsigned long long* cnt8, long long* rec128, int* nrec) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(cnt8, g_vfy_cnt, 8 * sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(rec128, g_vfy_rec, 256 * sizeof(long long));
+    cudaMemcpyFromSymbol(nrec, g_vfy_nrec, sizeof(int));
+    unsigned long long z8[8] = {0};
+    int z = 0;
+    cudaMemcpyToSymbol(g_vfy_cnt, z8, sizeof(z8));
+    cudaMemcpyToSymbol(g_vfy_nrec, &z, sizeof(z));
+    return EG_OK;
+}
+#endif
+
 
 int eg_profile_reset(eg_solver* s) {
     if (!s) return EG_ERR_ARG;

@@ -102,6 +102,12 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, int ns) {
     while (!mbar_test(b, parity)) __nanosleep(ns);
 }
+// a consumer's generic-proxy reads of a stage must be ordered before the TMA (async proxy) that
+// refills it: without this fence the refill can land before the reads are performed (observed as a
+// rare run-to-run difference at full size; scripts/repro_t1.py)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
@@ -179,6 +185,19 @@ __device__ unsigned long long g_ma_trace[1024 * 16];
 #define MA_CLK(v)
 #define MA_ADD(slot, t0)
 #endif
+
+// -DMA_JITTER (debug builds): pseudo-random delays at the synchronisation points, to expose races
+#ifdef MA_JITTER
+__device__ __forceinline__ void ma_jitter(uint32_t salt) {
+    uint32_t h = (uint32_t)clock() * 2654435761u ^ (salt * 40503u) ^ (blockIdx.x * 2246822519u) ^ threadIdx.x;
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    if ((h & 7u) == 0u) __nanosleep(h >> 20 & 2047u);
+}
+#define MA_J(salt) ma_jitter(salt)
+#else
+#define MA_J(salt)
+#endif
+
 
 // tcgen05 accesses of one warp role are ordered against the other role's through the mbarriers
 // only with these fences (a run-to-run race at full size without them: scripts/stress_march.py)
@@ -266,10 +285,12 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     const int ring_slot = NZ8 * MA_RING_W;
 
     if (tid == 0) {
-        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], 4); }
-        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], 4); }
-        for (int c = 0; c < MA_MAX_CH; ++c) mbar_init(&sread[c], 4);
-        for (int b = 0; b < 2; ++b) { mbar_init(&zready[b], 4); mbar_init(&zdone[b], 4); }
+        // consumer-side barriers count every thread of a role (128): each thread releases its own
+        // shared / global / TMEM accesses, nothing relies on a warp-level hand-off to lane 0
+        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], MA_CONS); }
+        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], MA_CONS); }
+        for (int c = 0; c < MA_MAX_CH; ++c) mbar_init(&sread[c], MA_CONS);
+        for (int b = 0; b < 2; ++b) { mbar_init(&zready[b], MA_CONS); mbar_init(&zdone[b], MA_CONS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const uint32_t tbase = tm_alloc512(&tm_slot);  // contains __syncthreads()
@@ -289,6 +310,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 if (fround > 0) mbar_wait_sleep(&emptyF[fslot], (uint32_t)((fround - 1) & 1), 32);
                 MA_ADD(9, t0);
                 uint64_t* fb = &fullF[fslot];
+                MA_J(1);
                 mbar_expect_tx(fb, (KIND == 1 ? (fresh ? 1u : 3u) : 2u) * MA_BOX_V + MA_BOX_B2);
                 float* sb = stF + (size_t)fslot * SF;
                 tma3(sb, &maps.r, i0, k0, jr, fb);
@@ -303,6 +325,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 if (sround > 0) mbar_wait_sleep(&emptyS[sslot], (uint32_t)((sround - 1) & 1), 32);
                 MA_ADD(9, t0);
                 uint64_t* fb = &fullS[sslot];
+                MA_J(2);
                 mbar_expect_tx(fb, MA_BOX_B4 + (KIND == 1 ? MA_BOX_V : 0u));
                 float* sb = stS + (size_t)sslot * SF;
                 tma3(sb, &maps.b4, 2 * i0, k0, jr, fb);
@@ -331,6 +354,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
         if (lane == 0)
             for (int x = 0; x < L; ++x) {
                 mbar_wait_sleep(&zdone[x & 1], (uint32_t)((x >> 1) & 1), 256);
+                MA_J(3);
                 st_release(flags + (int64_t)row_of(x) * T + t, epoch);  // gpu-scope release: z(r_x)
             }
         return;
@@ -366,6 +390,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 MA_CLK(t0);
                 mbar_wait(&fullF[cslot], cphase);
                 MA_ADD(12, t0);
+                MA_J(4);
                 const float* sb = stF + (size_t)cslot * SF;
 #pragma unroll
                 for (int l = 0; l < KS; ++l) {
@@ -377,8 +402,8 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                     in.uu[e] = ud.x;
                     in.dd[e] = ud.y;
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyF[cslot]);
+                fence_proxy_async_smem();
+                mbar_arrive(&emptyF[cslot]);
                 if (++cslot == NSF) { cslot = 0; cphase ^= 1u; }
             }
             float cb[KB], yb[KB], fb[KB];
@@ -408,6 +433,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 MA_CLK(t1);
                 mbar_wait(&sread[c], (uint32_t)(sync_step & 1));
                 MA_TFENCE_AFTER();
+                MA_J(5);
                 MA_ADD(13, t1);
             }
 #pragma unroll
@@ -446,13 +472,10 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             }
             // TMEM writes of this row (U, D, s) are ordered before the S warps' reads by the fence
             MA_TFENCE_BEFORE();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&zready[x & 1]);  // the S warps may read z(r_x) from the ring
-                // the publisher may release the ready flag: this arrival (release, CTA scope) and
-                // its wait (acquire) order these z stores before its gpu-scope release of the flag
-                mbar_arrive(&zdone[x & 1]);
-            }
+            mbar_arrive(&zready[x & 1]);  // the S warps may read z(r_x) from the ring
+            // the publisher may release the ready flag: these arrivals (release, CTA scope) and its
+            // wait (acquire) order every thread's z stores before its gpu-scope release of the flag
+            mbar_arrive(&zdone[x & 1]);
             MA_ADD(14, t0);
         };
         auto T_row = [&](int x, int sync_step) {
@@ -496,6 +519,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             if (m == 0) mbar_wait(&zready[0], 0u);
             if (m + 1 < L) mbar_wait(&zready[(m + 1) & 1], (uint32_t)(((m + 1) >> 1) & 1));
             MA_TFENCE_AFTER();
+            MA_J(6);
             MA_ADD(5, t_z);
             float* zC0 = slot_ptr(m);
             float* zN0 = hasN ? (dir > 0 ? slot_ptr(m + 1) : slot_ptr(m - 1)) : zC0;
@@ -566,6 +590,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                     MA_CLK(t0);
                     mbar_wait(&fullS[cslot], cphase);
                     MA_ADD(2, t0);
+                    MA_J(7);
                     const float* sbS = stS + (size_t)cslot * SF;
 #pragma unroll
                     for (int l = 0; l < KS; ++l) {
@@ -587,12 +612,11 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 zc[KB] = zC[min(k0 + KB, nz - 1) * MA_RING_W];
                 tm_wait_ld();
                 MA_TFENCE_BEFORE();
-                __syncwarp();
-                if (lane == 0) {
+                MA_J(8);
+                fence_proxy_async_smem();
 #pragma unroll
-                    for (int h = 0; h < KB / KS; ++h) mbar_arrive(&emptyS[sl[h]]);
-                    mbar_arrive(&sread[c]);  // the F warps may now overwrite this chunk
-                }
+                for (int h = 0; h < KB / KS; ++h) mbar_arrive(&emptyS[sl[h]]);
+                mbar_arrive(&sread[c]);  // the F warps may now overwrite this chunk
                 if (KIND == 2) {
 #pragma unroll
                     for (int e = 0; e < KB; ++e) ax[e] = sv[e];

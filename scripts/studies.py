@@ -45,6 +45,8 @@ def _problem(base, seed):
 
 def table1(args):
     base = gen.CONFIGS[args.config]
+    if args.hard:  # the NEXT-2 knob (not from the paper): iteration counts near the paper's tens
+        base = base.with_(cv=(args.cv_lo, args.cv_hi), dl=(args.dl_lo, args.dl_hi))
     st = torch.cuda.Stream()
     dev = torch.device("cuda")
     # "mixed" runs the default fused schedule; "mixed_5k" the 5-kernel schedule (EG_NO_FUSE=1), the
@@ -61,8 +63,11 @@ def table1(args):
         for m in modes:
             if m == "mixed_5k":
                 os.environ["EG_NO_FUSE"] = "1"
-            solvers[m] = egs.Solver((base.nx, base.ny, base.nz), bands, "mixed" if m == "mixed_5k" else m, stream=st)
+            solvers[m] = egs.Solver((base.nx, base.ny, base.nz), bands, "mixed" if m == "mixed_5k" else m,
+                                    stream=st, trisor=args.precond == "trisor")
             os.environ.pop("EG_NO_FUSE", None)
+            if args.precond == "trisor":  # the UM's preconditioner: 3 sweeps, omega = 1.5
+                solvers[m].set_preconditioner("trisor", sweeps=3, omega=1.5)
         for d in range(args.dates):
             prob = _problem(base, args.seed0 + d)
             gen.device(prob, bands, b, stream=st)
@@ -82,6 +87,7 @@ def table1(args):
                     if tol == 1e-4:
                         first_R[m].append(float(hist[1]))
     out = {"study": "NEXT-3 Table 1 analogue", "config": args.config, "grid": [base.nx, base.ny, base.nz],
+           "precond": args.precond,
            "dates": args.dates, "seeds": [args.seed0 + d for d in range(args.dates)],
            "paper": {"1e-3": {"mixed": [8.4, 0.346], "fp64": [8.4, 0.592]},
                      "1e-4": {"mixed": [29.3, 1.18], "fp64": [29.3, 2.06]},
@@ -249,6 +255,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--tol", type=float, default=1e-4)
     ap.add_argument("--precision", default="mixed")
+    ap.add_argument("--precond", default="tridiag", choices=["tridiag", "trisor"])
     ap.add_argument("--nx", type=int, default=192)
     ap.add_argument("--ny", type=int, default=144)
     ap.add_argument("--nz", type=int, default=70)
@@ -257,6 +264,7 @@ def main():
     ap.add_argument("--dl-lo", type=float, default=1e-4)
     ap.add_argument("--dl-hi", type=float, default=1e-3)
     ap.add_argument("--true-stride", type=int, default=2)
+    ap.add_argument("--hard", action="store_true", help="table1: harder operator (NEXT-2 knob)")
     a = ap.parse_args()
     t0 = time.time()
     out = {"table1": table1, "timestep": timestep, "precision": precision, "trisor": trisor}[a.study](a)

@@ -345,3 +345,30 @@ def test_fused_phases_repeatable_at_scale(monkeypatch):
         x, info, h = s.solve(b, tol=1e-6, maxit=200)
         keep.append(x)
         assert info.iters == i0.iters and np.array_equal(h, h0) and torch.equal(x, x0)
+
+
+def test_fused_phases_repeatable_table1_sequence():
+    """Regression test for a stage-refill race (fixed with fence.proxy.async before each stage
+    release): two fused solvers driven like the Table 1 study (set_operator + solve at 1e-3, then
+    at 1e-4, per date) on the hard operator at C4 size must agree bitwise.  Before the fix about one
+    solve in six differed."""
+    base = gen.CONFIGS["C4"].with_(cv=(5.0, 20.0), dl=(1e-4, 1e-3))
+    g = (base.nx, base.ny, base.nz)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        bands = torch.empty((7, base.n), dtype=torch.float64, device="cuda")
+        b = torch.empty(base.n, dtype=torch.float64, device="cuda")
+        x = torch.empty(base.n, dtype=torch.float64, device="cuda")
+        gen.device(base, bands, b, stream=st)
+        sv = [egs.Solver(g, bands, "mixed", stream=st) for _ in range(2)]
+        for d in range(6):
+            gen.device(base.with_(seed=4 + d), bands, b, stream=st)
+            out = {}
+            for si, s in enumerate(sv):
+                for tol in (1e-3, 1e-4):
+                    s.set_operator(bands)
+                    _, info, h = s.solve(b, tol=tol, maxit=200, out=x)
+                    out[(si, tol)] = (x.clone(), info.iters, h)
+            for tol in (1e-3, 1e-4):
+                (x0, i0, h0), (x1, i1, h1) = out[(0, tol)], out[(1, tol)]
+                assert i0 == i1 and np.array_equal(h0, h1) and torch.equal(x0, x1), (d, tol)
