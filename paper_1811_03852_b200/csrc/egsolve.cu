@@ -18,6 +18,7 @@
 #include "egsolve.h"
 #include "kernels.cuh"
 #include "march.cuh"
+#include "sor_tma.cuh"
 
 using namespace eg;
 
@@ -104,6 +105,9 @@ struct eg_solver {
     bool use_march = false;     // fused phases (fp32 working precision; march.cuh)
     MarchGeo mg{};
     MarchMaps maps{};
+    SorMaps sor_maps[2]{};  // TMA maps of the tri-SOR sweeps writing into z / z_s
+    bool sor_tma = false;   // later tri-SOR sweeps on k_sor_tma (fp32, colour-split copies)
+    int nsm = 148;
     size_t smem_march = 0;
     int epoch_base = 1;         // first epoch of the next solve (flags are never reset)
     int precond = EG_PRECOND_TRIDIAG;  // NEXT-1: EG_PRECOND_TRISOR selects red-black tri-SOR
@@ -411,16 +415,26 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
         }
         sp = Split<V>{b4s, b2s, b2s + 2 * s->L.n};
     }
+    const int zi = (void*)z == (void*)v.zs ? 1 : 0;
     for (int sw = 0; sw < s->sor_sweeps; ++sw)
         for (int colour = 0; colour < 2; ++colour) {
             {
                 ProfScope ps(s, KID_SOR, sor_alg_bytes(s, KIND, sw, colour));
+                if constexpr (MODE != 0) {
+                    if (sw > 0 && s->sor_tma && s->split) {
+                        k_sor_tma<MODE><<<2 * s->nsm, SO_THREADS, SO_STAGES * SO_STAGE_FLOATS * 4 + 128, s->st>>>(
+                            s->geo, v, (float*)z, colour, s->sor_omega, KIND != 0, s->sor_maps[zi]);
+                        CK(cudaGetLastError());
+                        goto launched;
+                    }
+                }
                 if (sw == 0)
                     k_sor_half<MODE, KIND, true><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, colour, s->sor_omega, 0, sp);
                 else
                     k_sor_half<MODE, 0, false><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fsrc, z, colour, s->sor_omega,
                                                                                    KIND != 0, sp);
                 CK(cudaGetLastError());
+            launched:;
             }
             if ((rc = halo_ghosted(s, z))) return rc;
         }
@@ -820,15 +834,20 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-bool encode_map(EncodeTiledFn enc, CUtensorMap* m, void* base, int64_t inner, int64_t nz, int64_t nyl, int esz,
-                int box0) {
+bool encode_map_box(EncodeTiledFn enc, CUtensorMap* m, void* base, int64_t inner, int64_t nz, int64_t nyl, int esz,
+                    int box0, int box1) {
     const cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)nz, (cuuint64_t)nyl};
     const cuuint64_t strides[2] = {(cuuint64_t)(inner * esz), (cuuint64_t)(inner * nz * esz)};
-    const cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)MA_KS, 1u};
+    const cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)box1, 1u};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
     return enc(m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides,
                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool encode_map(EncodeTiledFn enc, CUtensorMap* m, void* base, int64_t inner, int64_t nz, int64_t nyl, int esz,
+                int box0) {
+    return encode_map_box(enc, m, base, inner, nz, nyl, esz, box0, MA_KS);
 }
 
 bool make_march_maps(eg_solver* s) {
@@ -845,6 +864,31 @@ bool make_march_maps(eg_solver* s) {
     ok = ok && encode_map(enc, &s->maps.v, s->vec[3], nx, nz, nyl, 4, 128);
     ok = ok && encode_map(enc, &s->maps.b2, s->B2, nx, nz, nyl, 8, 128);       // (U, D) as one 8-byte element
     ok = ok && encode_map(enc, &s->maps.b4, s->B4, 2 * nx, nz, nyl, 8, 256);   // (E, W), (N, S)
+    return ok;
+}
+
+bool make_sor_maps(eg_solver* s) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn || !s->split)
+        return false;
+    EncodeTiledFn enc = (EncodeTiledFn)fn;
+    const int64_t nx = s->grid.nx, nz = s->grid.nz, nyl = s->L.nyl;
+    float* b4s = (float*)s->split;
+    float* b2s = b4s + 4 * s->L.n;
+    float* fs = b2s + 2 * s->L.n;
+    bool ok = true;
+    for (int zi = 0; zi < 2; ++zi) {
+        void* zg = s->zext[zi];  // the ghosted array from its row -1: x rows are addressed as jl + 1
+        SorMaps& m = s->sor_maps[zi];
+        ok = ok && encode_map_box(enc, &m.x6, zg, nx, nz, nyl + 2, 4, 256, SO_KS + 2);
+        ok = ok && encode_map_box(enc, &m.xh, zg, nx, nz, nyl + 2, 4, 4, SO_KS + 2);
+        ok = ok && encode_map_box(enc, &m.x4, zg, nx, nz, nyl + 2, 4, 256, SO_KS);
+        ok = ok && encode_map_box(enc, &m.f, fs, nx, nz, nyl, 4, 128, SO_KS);
+        ok = ok && encode_map_box(enc, &m.b4, b4s, 2 * nx, nz, nyl, 8, 256, SO_KS);
+        ok = ok && encode_map_box(enc, &m.b2, b2s, nx, nz, nyl, 8, 128, SO_KS);
+    }
     return ok;
 }
 
@@ -1054,6 +1098,18 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
             else if (occ != 1 || !make_march_maps(s))  // co-residency of every CTA makes the flag waits safe
                 s->use_march = false;
         }
+    }
+    if (rc == EG_OK && s->split && prec != EG_FP64 && grid->nx % 4 == 0 && grid->nz <= SO_MAX_NZ8 && s->use_tm) {
+        // later tri-SOR sweeps on the TMA-fed kernel (EG_NO_SOR_TMA=1 keeps k_sor_half)
+        const char* ns = getenv("EG_NO_SOR_TMA");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&s->nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int smem = SO_STAGES * SO_STAGE_FLOATS * 4 + 128;
+        cudaError_t e1 = prec == EG_MIXED
+            ? cudaFuncSetAttribute(k_sor_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+            : cudaFuncSetAttribute(k_sor_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        s->sor_tma = e1 == cudaSuccess && !(ns && ns[0] == '1') && make_sor_maps(s);
     }
 #ifdef MA_VERIFY
     if (rc == EG_OK && g_vfy.n != s->L.n) {

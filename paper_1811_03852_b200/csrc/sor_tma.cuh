@@ -1,0 +1,218 @@
+// sor_tma.cuh — TMA-fed, persistent red-black tri-SOR half-sweep (NEXT-1, Eq. 7), fp32 vectors.
+//
+// One half-sweep updates the columns (i, j) with (i + j) % 2 == colour:
+//   rhs_k = (1 - omega) (T x_old)_k + omega (f_k - (E x_E + W x_W + N x_N + S x_S)_k),  x_col = T^-1 rhs
+// (k_sor_half in kernels.cuh has the same arithmetic, operation for operation, so both give bitwise
+// the same x).  Every value a half-sweep reads from x has the other colour or is the updated
+// column's own old value, so CTAs never depend on one another.
+//
+// This kernel serves the sweeps after the first (f = the colour-split right-hand side written by the
+// first sweep).  Work item = (latitude row, 256-column tile): the 128 columns of the sweep's colour,
+// one per consumer thread.  A producer warp streams, per 4-level stage, with 3-D TMA boxes:
+//   x of the row (levels k0-1 .. k0+4, the 256 columns and one 4-wide halo box on each side),
+//   x of the rows j-1 and j+1 (levels k0 .. k0+3), and the colour-split f, (E,W,N,S), (U,D),
+// so every loaded sector is used (the natural-order rows hold the updated column's old value and its
+// E / W neighbours; the N / S rows are shared with the neighbouring rows' items through L2).
+// The Thomas factors c' and y live in TMEM (thread = lane); x_new is written in natural order.
+// Persistent grid (2 CTAs / SM); stage release is ordered before the TMA refill by
+// fence.proxy.async (see march.cuh).
+#pragma once
+#include "march.cuh"
+
+namespace eg {
+
+constexpr int SO_KS = 4;                  // levels per stage
+constexpr int SO_CONS = 128;              // consumer threads (columns of one colour per item)
+constexpr int SO_THREADS = SO_CONS + 32;  // + the producer warp
+constexpr int SO_TILE = 256;              // natural columns per item
+// stage layout (floats; every TMA destination 128-byte aligned)
+constexpr int SO_XJ = 0;                              // [KS+2][256]
+constexpr int SO_XHW = SO_XJ + (SO_KS + 2) * 256;      // [KS+2][4]
+constexpr int SO_XHE = SO_XHW + 32;                    // [KS+2][4]
+constexpr int SO_XN = SO_XHE + 32;                     // [KS][256]
+constexpr int SO_XS = SO_XN + SO_KS * 256;             // [KS][256]
+constexpr int SO_F = SO_XS + SO_KS * 256;              // [KS][128]
+constexpr int SO_B4 = SO_F + SO_KS * 128;              // [KS][512]
+constexpr int SO_B2 = SO_B4 + SO_KS * 512;             // [KS][256]
+constexpr int SO_STAGE_FLOATS = SO_B2 + SO_KS * 256;
+constexpr int SO_STAGES = 3;
+constexpr int SO_MAX_NZ8 = 72;
+constexpr uint32_t SO_BOX_XJ = (SO_KS + 2) * 256 * 4, SO_BOX_XH = (SO_KS + 2) * 4 * 4, SO_BOX_XR = SO_KS * 256 * 4;
+constexpr uint32_t SO_BOX_F = SO_KS * 128 * 4, SO_BOX_B4 = SO_KS * 512 * 4, SO_BOX_B2 = SO_KS * 256 * 4;
+
+// tensor maps: x natural with (256, KS+2), (4, KS+2) and (256, KS) boxes; f split (128, KS);
+// (E,W,N,S) split as u64 (256, KS); (U,D) split as u64 (128, KS)
+struct SorMaps {
+    CUtensorMap x6, xh, x4, f, b4, b2;
+};
+
+// grid: persistent (2 CTAs / SM), block SO_THREADS, dynamic smem SO_STAGES * SO_STAGE_FLOATS * 4 + 128.
+// x: the ghosted array's row 0 (updated in place, own colour only).
+template <int MODE>
+__global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv, float* __restrict__ x, int colour,
+                                                            double omega_d, int check_halt,
+                                                            const __grid_constant__ SorMaps maps) {
+    static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
+    using V = float;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    __shared__ __align__(8) uint64_t full[SO_STAGES], empty[SO_STAGES];
+    __shared__ uint32_t tm_slot;
+    if (check_halt && vv.st->halt != H_RUN) return;  // uniform
+    const V om = (V)omega_d, om1 = (V)(1.0 - omega_d);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nx = (int)g.nx, nz = (int)g.nz, nyl = (int)g.nyl;
+    const int tiles = (nx + SO_TILE - 1) / SO_TILE;
+    const int64_t items = (int64_t)tiles * nyl;
+    const int NZ8 = (nz + 7) / 8 * 8;  // levels padded to whole 8-level TMEM chunks
+    float* stages = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    if (tid == 0) {
+        for (int s = 0; s < SO_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], SO_CONS); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // 256 TMEM columns: c' [0, 72), y [72, 144)
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&tm_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = tm_slot;
+    const int nstage = NZ8 / SO_KS;  // even
+
+    if (warp == SO_CONS / 32) {  // ------------------------------------------------ producer
+        if (lane == 0) {
+            int slot = 0, round = 0;
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+                const int jl = (int)(it / tiles), t = (int)(it % tiles);
+                const int64_t jg = g.j0 + jl;
+                const int i0 = t * SO_TILE;
+                const int w = min(SO_TILE, nx - i0);
+                const int iWb = (i0 == 0 ? nx - 1 : i0 - 1) - 3;  // W halo box: its last element
+                const int iEb = (i0 + w == nx) ? 0 : i0 + w;      // E halo box: its first element
+                const int cs = colour * (nx / 2) + t * (SO_TILE / 2);  // colour-split column of the tile
+                const bool hasN = jg < g.ny - 1, hasS = jg > 0;
+                for (int st = 0; st < nstage; ++st) {
+                    const int k0 = st * SO_KS;
+                    if (round > 0) mbar_wait_sleep(&empty[slot], (uint32_t)((round - 1) & 1), 32);
+                    uint64_t* fb = &full[slot];
+                    const uint32_t bytes = SO_BOX_XJ + 2 * SO_BOX_XH + (hasN ? SO_BOX_XR : 0u) +
+                                           (hasS ? SO_BOX_XR : 0u) + SO_BOX_F + SO_BOX_B4 + SO_BOX_B2;
+                    mbar_expect_tx(fb, bytes);
+                    float* sb = stages + (size_t)slot * SO_STAGE_FLOATS;
+                    // x maps span the ghosted rows -1 .. nyl: local row r is coordinate r + 1
+                    tma3(sb + SO_XJ, &maps.x6, i0, k0 - 1, jl + 1, fb);
+                    tma3(sb + SO_XHW, &maps.xh, iWb, k0 - 1, jl + 1, fb);
+                    tma3(sb + SO_XHE, &maps.xh, iEb, k0 - 1, jl + 1, fb);
+                    if (hasN) tma3(sb + SO_XN, &maps.x4, i0, k0, jl + 2, fb);
+                    if (hasS) tma3(sb + SO_XS, &maps.x4, i0, k0, jl, fb);
+                    tma3(sb + SO_F, &maps.f, cs, k0, jl, fb);
+                    tma3(sb + SO_B4, &maps.b4, 2 * cs, k0, jl, fb);
+                    tma3(sb + SO_B2, &maps.b2, cs, k0, jl, fb);
+                    if (++slot == SO_STAGES) { slot = 0; ++round; }
+                }
+            }
+        }
+    } else {  // ------------------------------------------------------------------ consumers
+        const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+        int slot = 0;
+        uint32_t phase = 0;
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+            const int jl = (int)(it / tiles), t = (int)(it % tiles);
+            const int64_t jg = g.j0 + jl;
+            const int i0 = t * SO_TILE;
+            const int w = min(SO_TILE, nx - i0);
+            const bool hasN = jg < g.ny - 1, hasS = jg > 0;
+            const int par = (int)((jg + colour) & 1);
+            const int li = 2 * tid + par;  // natural column within the tile
+            const bool act = li < w;
+            const bool eh = li + 1 >= w, wh = li == 0;  // E / W neighbour in the halo boxes
+            V cprev = 0.f, yprev = 0.f;
+            for (int k8 = 0; k8 < NZ8; k8 += 8) {  // two stages = one 8-level TMEM chunk
+                float cb[8], yb[8];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int k0 = k8 + h * SO_KS;
+                    mbar_wait(&full[slot], phase);
+                    const float* sb = stages + (size_t)slot * SO_STAGE_FLOATS;
+                    float xm[SO_KS], xc[SO_KS], xp[SO_KS], xE[SO_KS], xW[SO_KS], xN[SO_KS], xS[SO_KS], f[SO_KS];
+                    float4 b4[SO_KS];
+                    float2 b2[SO_KS];
+#pragma unroll
+                    for (int l = 0; l < SO_KS; ++l) {
+                        const float* xr = sb + SO_XJ + (l + 1) * 256;  // level k0 + l
+                        xm[l] = xr[li - 256];
+                        xc[l] = xr[li];
+                        xp[l] = xr[li + 256];
+                        xE[l] = eh ? sb[SO_XHE + (l + 1) * 4] : xr[li + 1];
+                        xW[l] = wh ? sb[SO_XHW + (l + 1) * 4 + 3] : xr[li - 1];
+                        xN[l] = hasN ? sb[SO_XN + l * 256 + li] : xE[l];  // poles: the zero N / S band reads x_E
+                        xS[l] = hasS ? sb[SO_XS + l * 256 + li] : xE[l];
+                        f[l] = sb[SO_F + l * 128 + tid];
+                        b4[l] = *reinterpret_cast<const float4*>(sb + SO_B4 + l * 512 + 4 * tid);
+                        b2[l] = *reinterpret_cast<const float2*>(sb + SO_B2 + l * 256 + 2 * tid);
+                    }
+                    fence_proxy_async_smem();
+                    mbar_arrive(&empty[slot]);
+                    if (++slot == SO_STAGES) { slot = 0; phase ^= 1u; }
+#pragma unroll
+                    for (int l = 0; l < SO_KS; ++l) {
+                        const int k = k0 + l;
+                        V hx = b4[l].x * xE[l];
+                        hx = fmaf(b4[l].y, xW[l], hx);
+                        hx = fmaf(b4[l].z, xN[l], hx);
+                        hx = fmaf(b4[l].w, xS[l], hx);
+                        const V xup = k + 1 < nz ? xp[l] : xc[l];  // U = 0 on the top level
+                        V tx = xc[l];
+                        tx = fmaf(b2[l].x, xup, tx);
+                        tx = fmaf(b2[l].y, xm[l], tx);  // D = 0 (and x(-1) = 0) at k = 0
+                        const V rhs = fmaf(om1, tx, om * (f[l] - hx));
+                        const V u = b2[l].x, d = b2[l].y;
+                        V c, y;
+                        if (k == 0) {
+                            c = u;
+                            y = rhs;
+                        } else {
+                            const V inv = rcp_fast<V>(fmaf(-d, cprev, 1.f));
+                            c = u * inv;
+                            y = fmaf(-d, yprev, rhs) * inv;
+                        }
+                        cb[h * SO_KS + l] = c;
+                        yb[h * SO_KS + l] = y;
+                        cprev = c;
+                        yprev = y;
+                    }
+                }
+                tm_st8(tl + (uint32_t)k8, cb);
+                tm_st8(tl + (uint32_t)(SO_MAX_NZ8 + k8), yb);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            // back substitution from the top (padded levels: c' = y = 0 as in the march kernels)
+            V zn = 0.f;
+            V* xo = x + (int64_t)jl * g.row + (i0 + (act ? li : 0));
+            for (int k8 = NZ8 - 8; k8 >= 0; k8 -= 8) {
+                float cc[8], yy[8];
+                tm_ld8_nw(tl + (uint32_t)k8, cc);
+                tm_ld8_nw(tl + (uint32_t)(SO_MAX_NZ8 + k8), yy);
+                tm_wait_ld();
+#pragma unroll
+                for (int e = 7; e >= 0; --e) {
+                    const int k = k8 + e;
+                    zn = (k == nz - 1) ? yy[e] : fmaf(-cc[e], zn, yy[e]);
+                    if (k >= nz) zn = 0.f;
+                    if (act && k < nz) xo[(int64_t)k * nx] = zn;
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tbase) : "memory");
+    }
+}
+
+}  // namespace eg
