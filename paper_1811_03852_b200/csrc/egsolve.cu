@@ -421,9 +421,17 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
             {
                 ProfScope ps(s, KID_SOR, sor_alg_bytes(s, KIND, sw, colour));
                 if constexpr (MODE != 0) {
-                    if (sw > 0 && s->sor_tma && s->split) {
-                        k_sor_tma<MODE><<<2 * s->nsm, SO_THREADS, SO_STAGES * SO_STAGE_FLOATS * 4 + 128, s->st>>>(
-                            s->geo, v, (float*)z, colour, s->sor_omega, KIND != 0, s->sor_maps[zi]);
+                    if (s->sor_tma && s->split) {
+                        const int so_smem = SO_STAGES * SO_STAGE_FLOATS * 4 + 128;
+                        if (sw == 0 && colour == 0)  // red half + f of both colours
+                            k_sor_first_red<MODE, KIND><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, (const float*)fin,
+                                                                                         (float*)z, s->sor_omega, sp);
+                        else if (sw == 0)
+                            k_sor_tma<MODE, true><<<2 * s->nsm, SO_THREADS, so_smem, s->st>>>(
+                                s->geo, v, (float*)z, colour, s->sor_omega, KIND != 0, s->sor_maps[zi]);
+                        else
+                            k_sor_tma<MODE, false><<<2 * s->nsm, SO_THREADS, so_smem, s->st>>>(
+                                s->geo, v, (float*)z, colour, s->sor_omega, KIND != 0, s->sor_maps[zi]);
                         CK(cudaGetLastError());
                         goto launched;
                     }
@@ -1106,9 +1114,19 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&s->nsm, cudaDevAttrMultiProcessorCount, dev);
         const int smem = SO_STAGES * SO_STAGE_FLOATS * 4 + 128;
-        cudaError_t e1 = prec == EG_MIXED
-            ? cudaFuncSetAttribute(k_sor_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
-            : cudaFuncSetAttribute(k_sor_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e1 = cudaSuccess;
+        auto attr = [&](const void* f, int bytes) {
+            if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        };
+        if (prec == EG_MIXED) {
+            attr((const void*)k_sor_tma<1, true>, smem); attr((const void*)k_sor_tma<1, false>, smem);
+            attr((const void*)k_sor_first_red<1, 0>, (int)s->smem_th); attr((const void*)k_sor_first_red<1, 1>, (int)s->smem_th);
+            attr((const void*)k_sor_first_red<1, 2>, (int)s->smem_th);
+        } else {
+            attr((const void*)k_sor_tma<2, true>, smem); attr((const void*)k_sor_tma<2, false>, smem);
+            attr((const void*)k_sor_first_red<2, 0>, (int)s->smem_th); attr((const void*)k_sor_first_red<2, 1>, (int)s->smem_th);
+            attr((const void*)k_sor_first_red<2, 2>, (int)s->smem_th);
+        }
         s->sor_tma = e1 == cudaSuccess && !(ns && ns[0] == '1') && make_sor_maps(s);
     }
 #ifdef MA_VERIFY

@@ -48,7 +48,9 @@ struct SorMaps {
 
 // grid: persistent (2 CTAs / SM), block SO_THREADS, dynamic smem SO_STAGES * SO_STAGE_FLOATS * 4 + 128.
 // x: the ghosted array's row 0 (updated in place, own colour only).
-template <int MODE>
+// FIRST: the black half of the first sweep (x_old = 0: rhs = omega (f - H x), the red neighbours
+// just written by k_sor_first_red, which also wrote the black columns' f colour-split).
+template <int MODE, bool FIRST>
 __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv, float* __restrict__ x, int colour,
                                                             double omega_d, int check_halt,
                                                             const __grid_constant__ SorMaps maps) {
@@ -163,11 +165,16 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
                         hx = fmaf(b4[l].y, xW[l], hx);
                         hx = fmaf(b4[l].z, xN[l], hx);
                         hx = fmaf(b4[l].w, xS[l], hx);
-                        const V xup = k + 1 < nz ? xp[l] : xc[l];  // U = 0 on the top level
-                        V tx = xc[l];
-                        tx = fmaf(b2[l].x, xup, tx);
-                        tx = fmaf(b2[l].y, xm[l], tx);  // D = 0 (and x(-1) = 0) at k = 0
-                        const V rhs = fmaf(om1, tx, om * (f[l] - hx));
+                        V rhs;
+                        if (FIRST) {
+                            rhs = om * (f[l] - hx);
+                        } else {
+                            const V xup = k + 1 < nz ? xp[l] : xc[l];  // U = 0 on the top level
+                            V tx = xc[l];
+                            tx = fmaf(b2[l].x, xup, tx);
+                            tx = fmaf(b2[l].y, xm[l], tx);  // D = 0 (and x(-1) = 0) at k = 0
+                            rhs = fmaf(om1, tx, om * (f[l] - hx));
+                        }
                         const V u = b2[l].x, d = b2[l].y;
                         V c, y;
                         if (k == 0) {
@@ -212,6 +219,115 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tbase) : "memory");
+    }
+}
+
+// The red half of the first sweep (x = 0 before it: rhs = omega f) fused with forming f for BOTH
+// colours: thread m owns the natural column pair (2m, 2m+1) of a row, reads r, p, v (or fin) for
+// both with 8-byte loads, writes p / s (KIND 1 / 2) for both and f colour-split for both, and solves
+// the pair's red column.  The black half then reads f colour-split (k_sor_tma<FIRST>), so r, p, v are
+// read once per application instead of once per colour.  Arithmetic as k_sor_half<KIND, true>.
+// grid (ceil(nx/2 / 128), nyl), block 128, dynamic smem 2 * nz * 128 * 4.
+template <int MODE, int KIND>
+__global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, const float* __restrict__ fin,
+                                                       float* __restrict__ x, double omega_d, Split<float> sp) {
+    using V = float;
+    constexpr int KB = 4;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int W = blockDim.x, tid = threadIdx.x;
+    V* cps = reinterpret_cast<V*>(smraw);
+    V* ys = cps + g.nz * W;
+    V beta = 0, omega_b = 0, alpha = 0;
+    bool fresh = false;
+    if (KIND != 0) {
+        const DevState* st = vv.st;
+        if (st->halt != H_RUN) return;
+        if (KIND == 1) {
+            fresh = st->fresh != 0;
+            beta = (V)st->beta_v;
+            omega_b = (V)st->omega_v;
+        } else {
+            alpha = (V)st->alpha_v;
+        }
+    }
+    const V om = (V)omega_d;
+    const int nx = (int)g.nx, nz = (int)g.nz;
+    const int m = blockIdx.x * W + tid;
+    if (m >= nx / 2) return;
+    const int64_t jl = blockIdx.y, jg = g.j0 + jl;
+    const int red = (int)(jg & 1);  // which of the pair (2m, 2m+1) is red: (i + jg) % 2 == 0
+    const int64_t rb = jl * g.row;
+    const int64_t q0 = rb + 2 * m;  // natural index of the pair
+    const V* __restrict__ A0 = (KIND == 0 ? fin : vv.r) + q0;
+    const V* __restrict__ Pp = (KIND == 1 && fresh ? vv.r : vv.p) + q0;
+    const V* __restrict__ Vv = (KIND == 1 && fresh ? vv.r : vv.v) + q0;
+    if (KIND == 1 && fresh) beta = 0;
+    V* __restrict__ Fw = (KIND == 1 ? vv.p : vv.s) + q0;
+    V* __restrict__ Fr = sp.f + rb + m;                           // colour 0 (red) half of the row
+    V* __restrict__ Fb = sp.f + rb + nx / 2 + m;                  // colour 1 (black)
+    const V* __restrict__ b2 = sp.b2 + 2 * (rb + m);              // red colour-split (U, D)
+    V* __restrict__ Xw = x + q0 + red;
+    VecN<V, 2> ca[KB], cp[KB], cv[KB], na[KB], np[KB], nv[KB];
+    VecN<V, 2> cu[KB], nu[KB];
+#pragma unroll
+    for (int e = 0; e < KB; ++e)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) ca[e].v[c] = cp[e].v[c] = cv[e].v[c] = na[e].v[c] = np[e].v[c] = nv[e].v[c] =
+            cu[e].v[c] = nu[e].v[c] = 0.f;
+    auto load = [&](int k0, VecN<V, 2>(&a)[KB], VecN<V, 2>(&p)[KB], VecN<V, 2>(&v)[KB], VecN<V, 2>(&u)[KB]) {
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const int o = min(k0 + e, nz - 1) * nx;
+            a[e] = ldv<2>(A0 + o);
+            if (KIND == 1) { p[e] = ldv<2>(Pp + o); v[e] = ldv<2>(Vv + o); }
+            if (KIND == 2) v[e] = ldv<2>(Vv + o);
+            u[e] = ldv<2>(b2 + 2 * o);
+        }
+    };
+    load(0, ca, cp, cv, cu);
+    V cprev = 0, yprev = 0;
+    for (int k0 = 0; k0 < nz; k0 += KB) {
+        if (k0 + KB < nz) load(k0 + KB, na, np, nv, nu);
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const int k = k0 + e;
+            if (k < nz) {
+                VecN<V, 2> f;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    if (KIND == 1) f.v[c] = fmaf(beta, fmaf(-omega_b, cv[e].v[c], cp[e].v[c]), ca[e].v[c]);
+                    else if (KIND == 2) f.v[c] = fmaf(-alpha, cv[e].v[c], ca[e].v[c]);
+                    else f.v[c] = ca[e].v[c];
+                }
+                if (KIND != 0) stv<2>(Fw + k * nx, f);
+                Fr[k * nx] = f.v[red];
+                Fb[k * nx] = f.v[red ^ 1];
+                const V hx = 0;
+                const V rhs = om * (f.v[red] - hx);
+                const V u = cu[e].v[0], d = cu[e].v[1];
+                V c, y;
+                if (k == 0) {
+                    c = u;
+                    y = rhs;
+                } else {
+                    const V inv = rcp_fast<V>(fmaf(-d, cprev, 1.f));
+                    c = u * inv;
+                    y = fmaf(-d, yprev, rhs) * inv;
+                }
+                cps[k * W + tid] = c;
+                ys[k * W + tid] = y;
+                cprev = c;
+                yprev = y;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < KB; ++e) { ca[e] = na[e]; cp[e] = np[e]; cv[e] = nv[e]; cu[e] = nu[e]; }
+    }
+    V zn = yprev;
+    Xw[(nz - 1) * nx] = zn;
+    for (int k = nz - 2; k >= 0; --k) {
+        zn = fmaf(-cps[k * W + tid], zn, ys[k * W + tid]);
+        Xw[k * nx] = zn;
     }
 }
 
