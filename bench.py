@@ -297,6 +297,37 @@ def run_ours(args, prob, ws, rank, local):
     torch.cuda.synchronize(dev)
     tts = ev0.elapsed_time(ev1)
 
+    # the paper's own preconditioner (NEXT-1): red-black tri-SOR, 3 sweeps, omega = 1.5,
+    # same step and timing; reported beside the headline, which uses C^-1 = T^-1 (reading A-3)
+    tri = None
+    if not args.no_trisor:
+        with torch.cuda.stream(stream):
+            st_ = egs.Solver((prob.nx, prob.ny, prob.nz), bands, args.precision, group=group, stream=stream,
+                             trisor=True)
+            st_.set_preconditioner("trisor", sweeps=3, omega=1.5)
+        s_main = s
+        s = st_
+        step(0)
+        ms_t, infos_t = timed(args.steps, 0)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        st_.set_operator(bands)
+        _, tinfo_t, _ = st_.solve(b, tol=1e-4, maxit=200, out=x)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        tri = {"preconditioner": "red-black tri-SOR, 3 sweeps, omega 1.5 (P:243-258)",
+               "value": sum(i.iters for i in infos_t) / (ms_t / 1000.0), "unit": "iter/s",
+               "ms_per_step": ms_t / args.steps,
+               "restarts_in_timed_region": int(sum(i.restarts for i in infos_t)),
+               "note": "fixed 8 iterations per step; with this preconditioner R falls below the fp32 floor "
+                       "within the step, so restarts (r recomputed in fp64) are part of the timed work",
+               "time_to_solution": {"tol": 1e-4, "ms": ev0.elapsed_time(ev1), "iters": tinfo_t.iters,
+                                    "true_R": tinfo_t.true_R}}
+        s = s_main
+        del st_
+        torch.cuda.empty_cache()
+
     if rank != 0:
         return
     n = prob.n
@@ -321,6 +352,7 @@ def run_ours(args, prob, ws, rank, local):
         "time_to_solution": {"tol": 1e-4, "ms": tts, "iters": tinfo.iters, "converged": tinfo.converged,
                              "true_R": tinfo.true_R, "history": [float(v) for v in thist],
                              "includes": "set_operator + solve (a1-a11)"},
+        "trisor": tri,
         "gpu_launches": int(launches),
         "restarts_in_timed_region": int(sum(i.restarts for i in infos)),
         "clocks": clk.summary(),
@@ -341,6 +373,7 @@ def main():
     ap.add_argument("--precision", default="mixed", choices=["mixed", "fp64", "fp32"])
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-trisor", action="store_true", help="skip the tri-SOR preconditioner block")
     args = ap.parse_args()
     subprocess.check_call(["make", "-s", "all"], cwd=ROOT, stdout=subprocess.DEVNULL)
     import gen
