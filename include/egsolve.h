@@ -28,7 +28,10 @@
  * A band at an absent neighbour (N at j = ny-1, S at j = 0, U at k = nz-1, D at k = 0) must be 0.
  *
  * THREADING.  One handle is not thread-safe; separate handles are independent.  All device work
- * is ordered on the stream given to eg_solver_create.
+ * is ordered on the stream given to eg_solver_create.  The fused phase kernels keep
+ * one CTA per SM and synchronise CTAs through ready flags, which needs every CTA of a launch
+ * resident: do not run two handles' solves concurrently on different streams of the same GPU
+ * (serialise them, or create the handles with EG_NO_FUSE=1 in the environment).
  */
 #ifndef EGSOLVE_H
 #define EGSOLVE_H

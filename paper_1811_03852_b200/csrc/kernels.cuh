@@ -996,7 +996,7 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
 
 // ---------------------------------------------------------------------------------------------
 // Finalisers.  fin_groups: warp w sums quantity (w % NQ) of local group (w / NQ): lane l sums the
-// group's (row, tile) slots l, l+32, l+64, ... in four fixed chains, then a fixed shuffle tree.
+// group's (row, tile) slots l, l+32, l+64, ... in 16 fixed chains, then a fixed shuffle tree.
 // fin_logic (thread 0): groups in order -> totals -> BiCGStab scalars and control flags.
 enum Which { W_START = 0, W_A = 1, W_B = 2, W_C = 3, W_VERIFY = 4 };
 
@@ -1011,27 +1011,40 @@ __device__ __forceinline__ void fin_groups(const Geo& g, const double* __restric
     const int64_t L = (re - rb) * g.tiles;
     const double* src = slots + (int64_t)qq * g.nyl * g.tiles + rb * g.tiles;
     const bool f = (r32 >> qq) & 1u;
-    // lane l sums slots l + 32 m for m = 0, 1, 2, ... into four chains (m mod 4), combined in
-    // fixed order: coalesced, latency-tolerant, and the same tree for any launch / rank count
-    double a4[4] = {0.0, 0.0, 0.0, 0.0};
-    int64_t e = lane;
-    for (; e + 96 < L; e += 128) {
+    // lane l sums slots l + 32 m for m = 0, 1, 2, ... into FC chains (m mod FC; the FC loads of a
+    // round are independent, so a round costs one L2 latency), combined by a fixed pairwise tree:
+    // coalesced, latency-tolerant, and the same tree for any launch / rank count
+    constexpr int FC = 16;
+    double ac[FC];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            a4[c] += src[e + 32 * c];
-            if (f) a4[c] = (double)(float)a4[c];
+    for (int c = 0; c < FC; ++c) ac[c] = 0.0;
+    int64_t e = lane;
+    for (; e + 32 * (FC - 1) < L; e += 32 * FC) {
+        double v[FC];
+#pragma unroll
+        for (int c = 0; c < FC; ++c) v[c] = src[e + 32 * c];
+#pragma unroll
+        for (int c = 0; c < FC; ++c) {
+            ac[c] += v[c];
+            if (f) ac[c] = (double)(float)ac[c];
         }
     }
-    for (int c = 0; e < L; e += 32, ++c) {
-        a4[c] += src[e];
-        if (f) a4[c] = (double)(float)a4[c];
+#pragma unroll
+    for (int c = 0; c < FC; ++c) {  // the last partial round
+        if (e + 32 * c < L) {
+            ac[c] += src[e + 32 * c];
+            if (f) ac[c] = (double)(float)ac[c];
+        }
     }
-    double s = (a4[0] + a4[1]);
-    if (f) s = (double)(float)s;
-    double s2 = (a4[2] + a4[3]);
-    if (f) s2 = (double)(float)s2;
-    s += s2;
-    if (f) s = (double)(float)s;
+#pragma unroll
+    for (int h = FC / 2; h > 0; h >>= 1) {
+#pragma unroll
+        for (int c = 0; c < h; ++c) {
+            ac[c] += ac[c + h];
+            if (f) ac[c] = (double)(float)ac[c];
+        }
+    }
+    double s = ac[0];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         s += __shfl_down_sync(0xffffffffu, s, o);
