@@ -328,6 +328,7 @@ def run_ours(args, prob, ws, rank, local):
         del st_
         torch.cuda.empty_cache()
 
+
     if rank != 0:
         return
     n = prob.n

@@ -138,6 +138,7 @@ struct eg_solver {
     double prof_bytes[KID_COUNT]{};  // algorithmic HBM bytes of the profiled launches
     int64_t prof_n[KID_COUNT]{};
     bool next_fresh = false;         // the next iteration starts from p = v = 0 (reads r only)
+    bool next_xzero = false;         // the next update starts from x = 0 (does not read x)
     std::string err;
 };
 
@@ -385,7 +386,8 @@ int iteration_fused(eg_solver* s, void* x_it) {
         if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
         const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
         {
-            ProfScope ps(s, KID_UPDATE);
+            ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - (double)s->L.xsz * s->L.n : -1.0);
+            s->next_xzero = false;
             if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
             else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
             CK(cudaGetLastError());
@@ -469,7 +471,8 @@ int iteration_trisor(eg_solver* s, void* x_it) {
     }
     if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
     {
-        ProfScope ps(s, KID_UPDATE);
+        ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - (double)s->L.xsz * s->L.n : -1.0);
+        s->next_xzero = false;
         if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
         else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
         CK(cudaGetLastError());
@@ -527,7 +530,8 @@ int iteration(eg_solver* s, void* x_it) {
     }
     if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
     {
-        ProfScope ps(s, KID_UPDATE);
+        ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - (double)s->L.xsz * s->L.n : -1.0);
+        s->next_xzero = false;
         if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
         else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
         CK(cudaGetLastError());
@@ -549,8 +553,10 @@ int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero) {
     }
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     s->next_fresh = true;
+    s->next_xzero = entry && xzero;
     {
-        ProfScope ps(s, KID_START);
+        // entry from x = 0 reads b, diag and writes bhat, r, rhat0 only (x is not stored)
+        ProfScope ps(s, KID_START, entry && xzero ? (24.0 + 2.0 * s->L.vsz) * s->L.n : -1.0);
         if (entry && xzero) k_start<MODE, true, true><<<gr, RW, 0, s->st>>>(s->geo, v, b);
         else if (entry) k_start<MODE, true, false><<<gr, RW, 0, s->st>>>(s->geo, v, b);
         else k_start<MODE, false, false><<<gr, RW, 0, s->st>>>(s->geo, v, b);
@@ -592,6 +598,17 @@ bool is_device_ptr(const void* p) {
         return false;
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// x = 0 not stored yet (DevState.xzero, no update since an x0 = 0 entry): store it before anything
+// else reads x (restart, verification, the output)
+template <int MODE>
+int materialise_x0(eg_solver* s, void* x_it) {
+    if (!s->hstate->xzero) return EG_OK;
+    CK(cudaMemsetAsync(x_it, 0, (size_t)s->L.n * sizeof(typename Prec<MODE>::X), s->st));
+    CK(cudaMemsetAsync(&s->dstate->xzero, 0, sizeof(int), s->st));
+    s->hstate->xzero = 0;
+    return EG_OK;
 }
 
 template <int MODE>
@@ -637,6 +654,7 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     h->restart_every = prm->restart_every;
     h->eps_v = MODE == 0 ? 0x1.0p-53 : 0x1.0p-24;
     h->omega = h->omega_v = 1.0;
+    h->xzero = x0 == nullptr ? 1 : 0;  // entry from x = 0 does not store x (the first update starts from 0)
     // ready flags are stamped with epochs that only ever grow: reserve this solve's range
     // (at most ~5 finalisers per iteration) and wrap around with a flag reset well before overflow
     if (s->epoch_base > (1 << 30)) {
@@ -705,6 +723,7 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
         // H_RESTART / breakdown / failed verification -> restart: r = round(bhat - Ahat x) with fp64
         // accumulation (A-11), which re-checks R_true < tol itself.
         if (halt == H_CONVERGED || halt == H_MAXIT) {
+            if ((rc = materialise_x0<MODE>(s, x_it))) return rc;
             if ((rc = verify<MODE>(s, x_it))) return rc;
             if ((rc = read_state(s))) return rc;
             if (h->halt == H_NONFINITE) { rc = EG_ERR_NONFINITE; break; }
@@ -713,12 +732,17 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
             if (h->iter >= h->maxit) break;
         }
         inf.restarts++;  // counted before the restart re-checks R_true (as the oracle does)
+        if ((rc = materialise_x0<MODE>(s, x_it))) return rc;
         if ((rc = start<MODE>(s, x_it, bdev, 0, 0))) return rc;
         if ((rc = read_state(s))) return rc;
         if (h->halt == H_START_CONVERGED) { inf.converged = 1; break; }
         if (h->halt == H_START_MAXIT) break;
     }
 
+    if (rc == EG_OK || rc == EG_ERR_BREAKDOWN || rc == EG_ERR_NONFINITE) {
+        const int rc0 = materialise_x0<MODE>(s, x_it);
+        if (rc0) return rc0;
+    }
     // ---- output x (fp64) ----
     if (MODE == 2) {
         double* dst = xdev ? x : s->x64;

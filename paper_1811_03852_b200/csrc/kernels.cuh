@@ -241,8 +241,7 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
                     }
                     double res;
                     if (XZERO) {
-                        res = bh;
-                        if (ENTRY) xo[o] = (X)0;
+                        res = bh;  // x = 0 is not stored: DevState.xzero (the first update starts from 0)
                     } else {
                         const double xm = e == 0 ? xprev : cur[e - 1][8];
                         const double xp = e + 1 < KB ? (k + 1 < nz ? cur[e + 1][8] : 0.0) : xup_c;
@@ -912,6 +911,7 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
     const DevState* st = vv.st;
     if (st->halt != H_RUN) return;
     const bool sexit = st->sexit != 0;
+    const bool xz = st->xzero != 0;  // x = 0 (not stored): the first update after an x0 = 0 entry
     const X alpha = (X)st->alpha, omega = (X)st->omega;
     const V omega_v = (V)st->omega_v;
     double acc[2] = {0.0, 0.0};
@@ -928,7 +928,10 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
         V* __restrict__ rp = vv.r + base;
         if (sexit) {
             for (int k = 0; k < nz; ++k) {
-                XC xv = ldv<CPT>(xp + k * nx);
+                XC xv;
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) xv.v[c] = (X)0;
+                if (!xz) xv = ldv<CPT>(xp + k * nx);
                 const VC zv = ldv<CPT>(zp + k * nx);
 #pragma unroll
                 for (int c = 0; c < CPT; ++c) xv.v[c] = fma(alpha, (X)zv.v[c], xv.v[c]);
@@ -951,7 +954,8 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
 #pragma unroll
                 for (int e = 0; e < KB; ++e) {
                     const int o = min(k0 + e, nz - 1) * nx;  // tail levels re-read the last one
-                    x_[e] = ldv<CPT>(xp + o); z_[e] = ldv<CPT>(zp + o); zs_[e] = ldv<CPT>(zsp + o);
+                    if (!xz) x_[e] = ldv<CPT>(xp + o);  // else stays 0
+                    z_[e] = ldv<CPT>(zp + o); zs_[e] = ldv<CPT>(zsp + o);
                     s_[e] = ldv<CPT>(sp + o); t_[e] = ldv<CPT>(tp + o); rh_[e] = ldv<CPT>(rhp + o);
                     if (UP_PF > 0 && k0 + e + UP_PF < nz) {  // warp-uniform
                         const int of = (k0 + e + UP_PF) * nx;
@@ -1117,6 +1121,7 @@ __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict
     } else {  // W_C
         const int it = st->iter + 1;
         st->iter = it;
+        st->xzero = 0;  // the update has stored x
         if (st->sexit) {
             st->hist[it % HIST_CAP] = st->Rs;
             st->final_R = st->Rs;
