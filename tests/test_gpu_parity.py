@@ -144,6 +144,27 @@ def test_warm_start_and_zero_iterations():
     assert info2.iters == 0 and info2.converged and torch.equal(x2, x)
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_solution_stays_zero_without_iterations(mode):
+    """From x0 = 0 the entry does not store x (the first update starts from 0): a solve that stops
+    before any update must still return exactly x = 0 in a NaN-poisoned output buffer (converged at
+    the start with tol > R_0 = 1, or maxit = 0), and the host-buffer path must agree."""
+    prob = gen.CONFIGS["C1"]
+    s, bands, b = _make(prob, mode)
+    bt = torch.from_numpy(b).cuda()
+    for tol, maxit in ((2.0, 200), (1e-6, 0)):
+        out = torch.full((prob.n,), float("nan"), dtype=torch.float64, device="cuda")
+        x, info, h = s.solve(bt, tol=tol, maxit=maxit, out=out)
+        assert info.iters == 0 and bool(torch.all(x == 0.0)), (tol, maxit)
+        xh = np.full(prob.n, np.nan)
+        xh, info_h, _ = s.solve(b, tol=tol, maxit=maxit, out=xh)
+        assert info_h.iters == 0 and np.all(xh == 0.0)
+    # one iteration from x0 = 0 equals one iteration from an explicit zero x0
+    x1, i1, h1 = s.solve(bt, tol=0.0, maxit=1)
+    x2, i2, h2 = s.solve(bt, x0=torch.zeros(prob.n, dtype=torch.float64, device="cuda"), tol=0.0, maxit=1)
+    assert np.array_equal(h1, h2) and torch.equal(x1, x2)
+
+
 def test_power_of_two_scaling_bitwise():
     prob = RAGGED
     s, bands, b = _make(prob, "mixed")
