@@ -112,6 +112,9 @@ int eg_workspace_bytes(const eg_grid* grid, const eg_dist* dist, eg_precision pr
  *     the natural-order arrays (same results, bitwise).
  * features = 0 gives eg_workspace_bytes.  Returns EG_OK or EG_ERR_ARG. */
 #define EG_FEATURE_TRISOR 1u
+/*   EG_FEATURE_BATCH: room for two device staging buffers each of b and x (4 fp64 values per point)
+ *     used by eg_solve_batch. */
+#define EG_FEATURE_BATCH 2u
 int eg_workspace_bytes_ex(const eg_grid* grid, const eg_dist* dist, eg_precision prec, uint32_t features,
                           size_t* bytes);
 
@@ -167,6 +170,23 @@ int eg_precondition(eg_solver* s, const void* r, void* z);
  * EG_ERR_NCCL; info / history / x stay valid up to the failure point. */
 int eg_solve(eg_solver* s, const double* b, const double* x0, const eg_solve_params* params,
              double* x, double* history, eg_solve_info* info);
+
+/* A sequence of `count` solves, e.g. one per time step ("the solver is called ... every time step",
+ * P:191-192), with the host <-> device transfers of neighbouring solves overlapped with the solves:
+ *   for k = 0 .. count-1:  [eg_solver_set_operator(s, bands) if bands != NULL];
+ *                          eg_solve(s, b[k], NULL, params, x[k], history + k*(maxit+1), info + k)
+ * b[k], x[k]: fp64 local rows, HOST (pinned memory overlaps; pageable works but is serialised by the
+ * driver) or DEVICE.  bands: DEVICE, as for eg_solver_set_operator, or NULL.  history (HOST,
+ * count*(maxit+1) doubles) and info (HOST, count entries) may be NULL.  While solve k runs, the
+ * upload of b[k+1] and the download of x[k-1] run on the library's own copy streams, staged
+ * through two device buffers for b and two for x in the workspace: requires a workspace of at
+ * least eg_workspace_bytes_ex(..., EG_FEATURE_BATCH, ...) (else EG_ERR_WORKSPACE).  Each solve's
+ * x / history / info are bitwise those of the individual eg_solve call.  Blocks until every x[k] is
+ * written.  Stops at the first failing solve; *done (may be NULL) = the number of solves completed.
+ * Errors: those of eg_solve, EG_ERR_ARG, EG_ERR_WORKSPACE. */
+int eg_solve_batch(eg_solver* s, int count, const double* const* b, double* const* x,
+                   const double* const bands[7], const eg_solve_params* params, double* history,
+                   eg_solve_info* info, int* done);
 
 /* Release the NCCL communicator, events and graphs (not the caller's workspace). NULL is a no-op. */
 void eg_solver_destroy(eg_solver* s);

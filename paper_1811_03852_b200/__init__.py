@@ -20,14 +20,14 @@ _SO = os.environ.get("EGSOLVE_LIB") or os.path.join(_HERE, "libegsolve.so")  # o
 EG_FP64, EG_MIXED, EG_FP32 = 0, 1, 2
 PRECISIONS = {"fp64": EG_FP64, "mixed": EG_MIXED, "fp32": EG_FP32}
 EG_SOLVE_NO_GRAPH, EG_SOLVE_PROFILE = 1, 2
-EG_FEATURE_TRISOR = 1
+EG_FEATURE_TRISOR, EG_FEATURE_BATCH = 1, 2
 STATUS = {0: "EG_OK", 1: "EG_ERR_ARG", 2: "EG_ERR_SINGULAR_DIAG", 3: "EG_ERR_DEGENERATE_RHS",
           4: "EG_ERR_BREAKDOWN", 5: "EG_ERR_NONFINITE", 6: "EG_ERR_CUDA", 7: "EG_ERR_NCCL",
           8: "EG_ERR_WORKSPACE"}
 # symbols declared in include/egsolve.h (tests check the library exports all of them)
 ABI_SYMBOLS = ("eg_workspace_bytes", "eg_workspace_bytes_ex", "eg_solver_create", "eg_solver_set_operator",
                "eg_solver_set_preconditioner", "eg_apply_operator", "eg_precondition",
-               "eg_solve", "eg_solver_destroy", "eg_last_error", "eg_status_str",
+               "eg_solve", "eg_solve_batch", "eg_solver_destroy", "eg_last_error", "eg_status_str",
                "eg_nccl_unique_id", "eg_num_kernels", "eg_kernel_name", "eg_profile_get",
                "eg_profile_reset")
 
@@ -94,6 +94,8 @@ def lib():
         L.eg_apply_operator.argtypes = [vp, vp, vp]
         L.eg_precondition.argtypes = [vp, vp, vp]
         L.eg_solve.argtypes = [vp, vp, vp, ctypes.POINTER(_Params), vp, vp, ctypes.POINTER(_Info)]
+        L.eg_solve_batch.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                     ctypes.POINTER(_Params), vp, ctypes.POINTER(_Info), ctypes.POINTER(i32)]
         L.eg_solver_destroy.argtypes = [vp]
         L.eg_solver_destroy.restype = None
         L.eg_last_error.argtypes = [vp]
@@ -147,9 +149,10 @@ class Solver:
     torch.distributed process group for a latitude-band decomposition (one rank per GPU).
     """
 
-    def __init__(self, grid, bands, precision="mixed", group=None, stream=None, trisor=False):
+    def __init__(self, grid, bands, precision="mixed", group=None, stream=None, trisor=False, batch=False):
         """trisor=True sizes the workspace for the colour-split tri-SOR copies (EG_FEATURE_TRISOR);
-        set_preconditioner("trisor") works either way, faster with them."""
+        set_preconditioner("trisor") works either way, faster with them.  batch=True adds the
+        staging buffers solve_batch needs (EG_FEATURE_BATCH)."""
         import torch
         self.grid = tuple(int(v) for v in grid)
         nx, ny, nz = self.grid
@@ -183,7 +186,8 @@ class Solver:
         self._grid = _Grid(nx, ny, nz)
         nbytes = ctypes.c_size_t()
         rc = lib().eg_workspace_bytes_ex(ctypes.byref(self._grid), dptr, self.mode,
-                                         EG_FEATURE_TRISOR if trisor else 0, ctypes.byref(nbytes))
+                                         (EG_FEATURE_TRISOR if trisor else 0) | (EG_FEATURE_BATCH if batch else 0),
+                                         ctypes.byref(nbytes))
         if rc:
             raise EgError(rc, "eg_workspace_bytes_ex")
         self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
@@ -263,6 +267,29 @@ class Solver:
         if rc and raise_on_error:
             self._check(rc, "eg_solve")
         return out, inf, hist[: inf.iters + 1]
+
+    def solve_batch(self, bs, xs, bands=None, tol=1e-4, maxit=200, restart_every=150, flags=0,
+                    check_every=0, raise_on_error=True):
+        """eg_solve_batch: solve for every b in `bs` into the matching `xs` (fp64; pinned host tensors
+        or numpy arrays, or CUDA tensors), re-scaling `bands` (CUDA, as for set_operator) before each
+        solve if given, with the transfers of neighbouring solves overlapped.  Needs batch=True at
+        construction.  Returns the list of SolveInfo."""
+        n = len(bs)
+        assert len(xs) == n
+        pb = (ctypes.c_void_p * max(n, 1))(*[_ptr(v).value for v in bs])
+        px = (ctypes.c_void_p * max(n, 1))(*[_ptr(v).value for v in xs])
+        pbands = None
+        if bands is not None:
+            pbands = (ctypes.c_void_p * 7)(*[bands[d].data_ptr() for d in range(7)])
+        prm = _Params(float(tol), int(maxit), int(restart_every), int(flags), int(check_every))
+        infos = (_Info * max(n, 1))()
+        done = ctypes.c_int()
+        rc = lib().eg_solve_batch(self._h, n, pb, px, pbands, ctypes.byref(prm), None, infos, ctypes.byref(done))
+        out = [SolveInfo(i.iters, bool(i.converged), i.restarts, i.breakdowns, i.status, i.final_R, i.true_R)
+               for i in list(infos)[: done.value]]
+        if rc and raise_on_error:
+            self._check(rc, "eg_solve_batch")
+        return out
 
     # ---- profiling ----
     def profile(self):

@@ -36,7 +36,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
     size_t off_bands, off_diag, off_bhat, off_x64, off_x32, off_xg, off_vec, off_z, off_pv, off_slots,
-        off_gsum, off_state, base_total, off_split, total;
+        off_gsum, off_state, base_total, off_split, off_batch, total;
     size_t vsz;      // sizeof(V)
     size_t xsz;      // sizeof(X)
     int64_t n, row, nyl;
@@ -73,6 +73,7 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t fe
     L->base_total = o;
     // EG_FEATURE_TRISOR: colour-split (E,W,N,S), (U,D) and f for the red-black tri-SOR sweeps
     L->off_split = o; if (features & EG_FEATURE_TRISOR) o = align_up(o + 7 * n * L->vsz, A);
+    L->off_batch = o; if (features & EG_FEATURE_BATCH) o = align_up(o + 4 * n * 8, A);
     L->total = o;
     return true;
 }
@@ -112,6 +113,9 @@ struct eg_solver {
     int epoch_base = 1;         // first epoch of the next solve (flags are never reset)
     int precond = EG_PRECOND_TRIDIAG;  // NEXT-1: EG_PRECOND_TRISOR selects red-black tri-SOR
     void* split = nullptr;             // colour-split B4 | B2 | f for tri-SOR (NULL: not available)
+    double* batch = nullptr;           // eg_solve_batch staging: b[2] | x[2] (NULL: not available)
+    cudaStream_t cin = nullptr, cout = nullptr;  // eg_solve_batch copy streams (owned)
+    cudaEvent_t ev_in[2]{}, ev_x[2]{}, ev_out[2]{};
     bool split_valid = false;          // the split bands match the current operator
     int sor_sweeps = 3;
     double sor_omega = 1.5;
@@ -119,14 +123,18 @@ struct eg_solver {
     double* gsum = nullptr;  // [G][3] local
     double* gall = nullptr;  // [G][3] all ranks
     DevState* dstate = nullptr;
-    DevState* hstate = nullptr;  // pinned host mirror
+    DevState* hstate = nullptr;  // pinned, mapped host mirror
+    void* hstate_dev = nullptr;  // its device address
     int wth = 128;               // Thomas CTA width (columns)
     int cpt = 1;                 // columns per thread of the Thomas / update kernels (2 if nx even)
     size_t smem_th = 0;
     bool use_tm = false;         // fp32 Thomas with TMEM-resident factors (nz <= 128)
     size_t smem_tm = 0;
-    // graph of one iteration, keyed on the iterate pointer
-    cudaGraphExec_t graph = nullptr;
+    // graphs of one iteration, keyed on the iterate pointer (two: eg_solve_batch alternates buffers)
+    cudaGraphExec_t graphs[2]{};
+    void* graphs_x[2]{};
+    int graph_next = 0;  // entry replaced on the next miss
+    cudaGraphExec_t graph = nullptr;  // the entry for the current solve
     void* graph_x = nullptr;
     // NCCL
     ncclComm_t comm = nullptr;
@@ -584,8 +592,24 @@ int verify(eg_solver* s, void* x_it) {
     return finalize<MODE, W_VERIFY>(s, 0);
 }
 
+// DevState <-> its host mirror by a one-CTA copy kernel through mapped pinned memory, not by
+// cudaMemcpyAsync: a small DMA copy would queue behind the multi-GB transfers eg_solve_batch keeps
+// in flight on the copy engines
+__global__ void k_copy_words(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int n) {
+    for (int w = threadIdx.x; w < n; w += blockDim.x) dst[w] = src[w];
+}
+
+int state_to_host(eg_solver* s, const void* dev, void* host, size_t bytes) {
+    const size_t off = (const unsigned char*)host - (const unsigned char*)s->hstate;
+    k_copy_words<<<1, 256, 0, s->st>>>((const uint32_t*)dev, (uint32_t*)((unsigned char*)s->hstate_dev + off),
+                                       (int)(bytes / 4));
+    CK(cudaGetLastError());
+    return EG_OK;
+}
+
 int read_state(eg_solver* s) {
-    CK(cudaMemcpyAsync(s->hstate, s->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, s->st));
+    int rc = state_to_host(s, s->dstate, s->hstate, sizeof(DevState));
+    if (rc) return rc;
     CK(cudaStreamSynchronize(s->st));
     if (s->profiling) drain_profile(s);
     return EG_OK;
@@ -663,7 +687,8 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     }
     h->epoch = s->epoch_base;
     s->epoch_base += 8 * (prm->maxit + 4);
-    CK(cudaMemcpyAsync(s->dstate, h, sizeof(DevState), cudaMemcpyHostToDevice, s->st));
+    k_copy_words<<<1, 256, 0, s->st>>>((const uint32_t*)s->hstate_dev, (uint32_t*)s->dstate, (int)(sizeof(DevState) / 4));
+    CK(cudaGetLastError());
 
     if ((rc = start<MODE>(s, x_it, bdev, 1, x0 == nullptr))) return rc;
     if ((rc = read_state(s))) return rc;
@@ -674,9 +699,14 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     int bd_at = -1;
     const int chunk_max = prm->check_every > 0 ? std::min(prm->check_every, HIST_CAP) : 8;
 
-    // graph for this iterate pointer
-    if (use_graph && rc == EG_OK && (s->graph == nullptr || s->graph_x != x_it)) {
-        if (s->graph) { cudaGraphExecDestroy(s->graph); s->graph = nullptr; }
+    // graph for this iterate pointer (two cached entries)
+    s->graph = nullptr;
+    for (int gi = 0; gi < 2; ++gi)
+        if (s->graphs[gi] && s->graphs_x[gi] == x_it) s->graph = s->graphs[gi];
+    if (use_graph && rc == EG_OK && s->graph == nullptr) {
+        const int gi = s->graph_next;
+        s->graph_next ^= 1;
+        if (s->graphs[gi]) { cudaGraphExecDestroy(s->graphs[gi]); s->graphs[gi] = nullptr; }
         cudaGraph_t gph;
         if (!s->cap_st) CK(cudaStreamCreateWithFlags(&s->cap_st, cudaStreamNonBlocking));
         cudaStream_t user = s->st;
@@ -689,9 +719,10 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
         s->st = user;
         if (irc) return irc;
         CK(ce);
-        CK(cudaGraphInstantiate(&s->graph, gph, 0));
+        CK(cudaGraphInstantiate(&s->graphs[gi], gph, 0));
         cudaGraphDestroy(gph);
-        s->graph_x = x_it;
+        s->graphs_x[gi] = x_it;
+        s->graph = s->graphs[gi];
     }
 
     while (rc == EG_OK) {
@@ -780,9 +811,10 @@ int create_impl(eg_solver* s, const double* const bands[7]) {
         k_scale<V><<<grid, 256, 0, s->st>>>(s->geo, in, (V*)s->B4, (V*)s->B2, s->diag, err);
         CK(cudaGetLastError());
     }
-    int herr = 0;
-    CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s->st));
+    int rc = state_to_host(s, err, &s->hstate->err, sizeof(int));
+    if (rc) return rc;
     CK(cudaStreamSynchronize(s->st));
+    const int herr = s->hstate->err;
     if (herr & 2) return fail(s, EG_ERR_SINGULAR_DIAG, "a_C is zero or non-finite at some point");
     if (herr & 1)
         return fail(s, EG_ERR_ARG, "non-finite band, or nonzero band at an absent neighbour");
@@ -998,7 +1030,7 @@ int eg_workspace_bytes_ex(const eg_grid* grid, const eg_dist* dist, eg_precision
                           size_t* bytes) {
     int64_t jb, je;
     int rank, nranks;
-    if (!valid_grid(grid) || !bytes || prec < EG_FP64 || prec > EG_FP32 || (features & ~EG_FEATURE_TRISOR))
+    if (!valid_grid(grid) || !bytes || prec < EG_FP64 || prec > EG_FP32 || (features & ~(EG_FEATURE_TRISOR | EG_FEATURE_BATCH)))
         return EG_ERR_ARG;
     if (!valid_dist(grid, dist, &jb, &je, &rank, &nranks)) return EG_ERR_ARG;
     Layout L;
@@ -1024,8 +1056,21 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         delete s;
         return EG_ERR_ARG;
     }
-    make_layout(grid, s->j_end - s->j_begin, prec, &s->L, EG_FEATURE_TRISOR);
-    const bool room_split = workspace_bytes >= s->L.total && grid->nx % 2 == 0;
+    // optional regions, in layout order: the colour-split tri-SOR copies, then the batch staging
+    Layout Lt, Lb, Ltb;
+    make_layout(grid, s->j_end - s->j_begin, prec, &Lt, EG_FEATURE_TRISOR);
+    make_layout(grid, s->j_end - s->j_begin, prec, &Lb, EG_FEATURE_BATCH);
+    make_layout(grid, s->j_end - s->j_begin, prec, &Ltb, EG_FEATURE_TRISOR | EG_FEATURE_BATCH);
+    // the caller sized the workspace with eg_workspace_bytes_ex(features): recover the features
+    uint32_t feat = 0;
+    if (workspace_bytes >= Ltb.total) feat = EG_FEATURE_TRISOR | EG_FEATURE_BATCH;
+    else if (workspace_bytes >= Lt.total && workspace_bytes >= Lb.total)
+        feat = Lt.total >= Lb.total ? EG_FEATURE_TRISOR : EG_FEATURE_BATCH;
+    else if (workspace_bytes >= Lt.total) feat = EG_FEATURE_TRISOR;
+    else if (workspace_bytes >= Lb.total) feat = EG_FEATURE_BATCH;
+    const bool room_split = (feat & EG_FEATURE_TRISOR) && grid->nx % 2 == 0;
+    const bool room_batch = (feat & EG_FEATURE_BATCH) != 0;
+    make_layout(grid, s->j_end - s->j_begin, prec, &s->L, feat);
     if (workspace_bytes < s->L.base_total || ((uintptr_t)workspace & 255)) {
         delete s;
         return EG_ERR_WORKSPACE;
@@ -1044,11 +1089,14 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         s->zext[d] = s->ws + L.off_z + (size_t)d * align_up((L.n + 2 * L.row) * L.vsz, 256);
     s->ready_flags = (int*)(s->ws + L.off_pv);
     s->split = room_split ? (void*)(s->ws + L.off_split) : nullptr;
+    s->batch = room_batch ? (double*)(s->ws + L.off_batch) : nullptr;
     s->slots = (double*)(s->ws + L.off_slots);
     s->gsum = (double*)(s->ws + L.off_gsum);
     s->gall = s->gsum + 8 * 3;
     s->dstate = (DevState*)(s->ws + L.off_state);
-    if (cudaMallocHost(&s->hstate, sizeof(DevState)) != cudaSuccess) {
+    if (cudaHostAlloc(&s->hstate, sizeof(DevState), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&s->hstate_dev, s->hstate, 0) != cudaSuccess) {
+        if (s->hstate) cudaFreeHost(s->hstate);
         delete s;
         return EG_ERR_CUDA;
     }
@@ -1193,11 +1241,13 @@ int eg_solver_set_preconditioner(eg_solver* s, int kind, int sweeps, double omeg
     } else {
         return fail(s, EG_ERR_ARG, "unknown preconditioner %d", kind);
     }
-    if (s->graph) {  // the captured iteration depends on the preconditioner
-        cudaGraphExecDestroy(s->graph);
-        s->graph = nullptr;
-        s->graph_x = nullptr;
-    }
+    for (int gi = 0; gi < 2; ++gi)  // the captured iteration depends on the preconditioner
+        if (s->graphs[gi]) {
+            cudaGraphExecDestroy(s->graphs[gi]);
+            s->graphs[gi] = nullptr;
+            s->graphs_x[gi] = nullptr;
+        }
+    s->graph = nullptr;
     return EG_OK;
 }
 
@@ -1224,10 +1274,67 @@ int eg_solve(eg_solver* s, const double* b, const double* x0, const eg_solve_par
     return rc;
 }
 
+int eg_solve_batch(eg_solver* s, int count, const double* const* b, double* const* x,
+                   const double* const bands[7], const eg_solve_params* params, double* history,
+                   eg_solve_info* info, int* done) {
+    if (done) *done = 0;
+    if (!s || count < 0 || (count > 0 && (!b || !x)) || !params || params->maxit < 0 || !(params->tol >= 0.0))
+        return s ? fail(s, EG_ERR_ARG, "bad batch arguments") : EG_ERR_ARG;
+    for (int k = 0; k < count; ++k)
+        if (!b[k] || !x[k]) return fail(s, EG_ERR_ARG, "NULL b / x in the batch");
+    if (!s->batch) return fail(s, EG_ERR_WORKSPACE, "eg_solve_batch needs an EG_FEATURE_BATCH workspace");
+    if (!s->cin) {
+        CK(cudaStreamCreateWithFlags(&s->cin, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s->cout, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&s->ev_in[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&s->ev_x[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&s->ev_out[i], cudaEventDisableTiming));
+        }
+    }
+    const size_t nb = (size_t)s->L.n * sizeof(double);
+    double* db[2] = {s->batch, s->batch + s->L.n};
+    double* dx[2] = {s->batch + 2 * s->L.n, s->batch + 3 * s->L.n};
+    auto upload = [&](int k) -> int {  // b[k] -> db[k % 2] on the input copy stream
+        CK(cudaMemcpyAsync(db[k & 1], b[k], nb, cudaMemcpyDefault, s->cin));
+        CK(cudaEventRecord(s->ev_in[k & 1], s->cin));
+        return EG_OK;
+    };
+    int rc = count > 0 ? upload(0) : EG_OK;
+    const size_t hs = (size_t)params->maxit + 1;
+    for (int k = 0; k < count && rc == EG_OK; ++k) {
+        const int i = k & 1;
+        // db[(k+1) % 2] was read by solve k-1, which has returned: refill it while solve k runs
+        if (k + 1 < count && (rc = upload(k + 1))) break;
+        CK(cudaStreamWaitEvent(s->st, s->ev_in[i], 0));
+        if (k >= 2) CK(cudaStreamWaitEvent(s->st, s->ev_out[i], 0));  // dx[i]'s download (solve k-2)
+        if (bands && (rc = eg_solver_set_operator(s, bands))) break;
+        rc = eg_solve(s, db[i], nullptr, params, dx[i], history ? history + (size_t)k * hs : nullptr,
+                      info ? info + k : nullptr);
+        if (rc) break;
+        CK(cudaEventRecord(s->ev_x[i], s->st));
+        CK(cudaStreamWaitEvent(s->cout, s->ev_x[i], 0));
+        CK(cudaMemcpyAsync(x[k], dx[i], nb, cudaMemcpyDefault, s->cout));  // overlaps solve k+1
+        CK(cudaEventRecord(s->ev_out[i], s->cout));
+        if (done) *done = k + 1;
+    }
+    CK(cudaStreamSynchronize(s->cout));
+    CK(cudaStreamSynchronize(s->cin));
+    return rc;
+}
+
 void eg_solver_destroy(eg_solver* s) {
     if (!s) return;
-    if (s->graph) cudaGraphExecDestroy(s->graph);
+    for (int gi = 0; gi < 2; ++gi)
+        if (s->graphs[gi]) cudaGraphExecDestroy(s->graphs[gi]);
     if (s->cap_st) cudaStreamDestroy(s->cap_st);
+    if (s->cin) cudaStreamDestroy(s->cin);
+    if (s->cout) cudaStreamDestroy(s->cout);
+    for (int i = 0; i < 2; ++i) {
+        if (s->ev_in[i]) cudaEventDestroy(s->ev_in[i]);
+        if (s->ev_x[i]) cudaEventDestroy(s->ev_x[i]);
+        if (s->ev_out[i]) cudaEventDestroy(s->ev_out[i]);
+    }
     if (s->comm) ncclCommDestroy(s->comm);
     for (auto& p : s->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto e : s->evpool) cudaEventDestroy(e);

@@ -393,3 +393,34 @@ def test_fused_phases_repeatable_table1_sequence():
             for tol in (1e-3, 1e-4):
                 (x0, i0, h0), (x1, i1, h1) = out[(0, tol)], out[(1, tol)]
                 assert i0 == i1 and np.array_equal(h0, h1) and torch.equal(x0, x1), (d, tol)
+
+
+def test_solve_batch_matches_individual_solves():
+    """eg_solve_batch overlaps the transfers of neighbouring solves (copy streams, two staging
+    buffers each for b and x): every solve's x, iteration count and status are those of the
+    individual eg_solve call, for pinned host, pageable (numpy) and device buffers, with and without
+    re-scaling the operator before each solve."""
+    prob = gen.Problem(128, 40, 20, seed=17)
+    bands, b0 = gen.host(prob)
+    g = (prob.nx, prob.ny, prob.nz)
+    bd = torch.from_numpy(bands).cuda()
+    s = egs.Solver(g, bd, "mixed", batch=True)
+    rng = np.random.default_rng(5)
+    bs = [b0 * (1.0 + 0.1 * k) + 0.01 * rng.standard_normal(prob.n) for k in range(5)]
+    ref = [s.solve(torch.from_numpy(v).cuda(), tol=1e-6, maxit=100) for v in bs]
+    # pinned host buffers, operator re-scaled before every solve
+    hb = [torch.from_numpy(v).pin_memory() for v in bs]
+    hx = [torch.empty(prob.n, dtype=torch.float64).pin_memory() for _ in bs]
+    infos = s.solve_batch(hb, hx, bands=bd, tol=1e-6, maxit=100)
+    for (x, i, _), xh, ib in zip(ref, hx, infos):
+        assert ib.iters == i.iters and ib.converged and torch.equal(xh, x.cpu())
+    # pageable numpy and device buffers
+    nx_ = [np.empty(prob.n) for _ in bs]
+    s.solve_batch(bs, nx_, tol=1e-6, maxit=100)
+    dx = [torch.empty(prob.n, dtype=torch.float64, device="cuda") for _ in bs]
+    s.solve_batch([torch.from_numpy(v).cuda() for v in bs], dx, tol=1e-6, maxit=100)
+    for (x, _, _), xn, xd in zip(ref, nx_, dx):
+        assert np.array_equal(xn, x.cpu().numpy()) and torch.equal(xd, x)
+    assert s.solve_batch([], [], tol=1e-6) == []
+    with pytest.raises(egs.EgError):   # no EG_FEATURE_BATCH staging in the workspace
+        egs.Solver(g, bd, "mixed").solve_batch(hb[:1], hx[:1], tol=1e-6)
