@@ -1148,8 +1148,12 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         // two stage rings (elimination / stencil inputs) share what the z ring leaves
         const int na = ring < budget ? (int)((budget - ring) / ma_stage_bytes(1)) : 0;
         const int nb = ring < budget ? (int)((budget - ring) / ma_stage_bytes(2)) : 0;
-        s->use_march = s->use_tm && grid->nx % 4 == 0 && nz8 <= 8 * MA_MAX_CH &&
-                       7 * nz8 <= 512 && s->L.tiles <= nsm && na >= 4 && !(nf && nf[0] == '1');
+        // below ~2^18 local points the launch-latency-bound 5-kernel schedule is faster
+        // (profiles/r01_schedule_compare.txt); EG_FUSE=1 forces the fused one (tests)
+        const char* ff = getenv("EG_FUSE");
+        const bool big = s->L.n >= (int64_t)1 << 18 || (ff && ff[0] == '1');
+        s->use_march = s->use_tm && grid->nx % 4 == 0 && nz8 <= 8 * MA_MAX_CH && 7 * nz8 <= 512 &&
+                       s->L.tiles <= nsm && na >= 4 && big && !(nf && nf[0] == '1');
         if (s->use_march) {
             s->mg.fst_a = std::min(MA_MAX_STAGES, na - na / 2);
             s->mg.sst_a = std::min(MA_MAX_STAGES, na / 2);

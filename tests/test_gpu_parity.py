@@ -236,8 +236,10 @@ def test_multirank_finaliser_path_bitwise_equal(mode, monkeypatch):
     s1 = egs.Solver(g, bd, mode)
     x1, i1, h1 = s1.solve(torch.from_numpy(b).cuda(), tol=1e-6, maxit=100)
     monkeypatch.setenv("EG_FORCE_NCCL", "1")
+    monkeypatch.setenv("EG_FUSE", "1")
     s2 = egs.Solver(g, bd, mode)
     monkeypatch.delenv("EG_FORCE_NCCL")
+    monkeypatch.delenv("EG_FUSE")
     x2, i2, h2 = s2.solve(torch.from_numpy(b).cuda(), tol=1e-6, maxit=100)
     assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
     if mode == "mixed":  # the fused phases run on the multi-rank path too (edge rows + ghost rows)
@@ -260,7 +262,7 @@ MARCH_CASES = [gen.CONFIGS["C1"], RAGGED, FUSED_ODD, FUSED_THIN, gen.CONFIGS["C2
 @pytest.mark.parametrize("strips", [None, 1, 2, 3])
 def test_fused_phases_match_unfused_schedule(prob, mode, strips, monkeypatch):
     """The fused marching phase kernels (march.cuh: Thomas + stencil of a latitude strip per CTA,
-    the default for fp32 vectors on one GPU) compute z, v, s, t with the same operations as the
+    the default for fp32 vectors from 2^18 local points; EG_FUSE=1 forces them here) compute z, v, s, t with the same operations as the
     5-kernel schedule (EG_NO_FUSE=1) and write the same reduction slots, so the solve is bitwise
     identical, whatever the number of strips (EG_MARCH_STRIPS: one-row strips, one strip per tile
     column, odd counts whose strips alternate direction)."""
@@ -270,7 +272,9 @@ def test_fused_phases_match_unfused_schedule(prob, mode, strips, monkeypatch):
     bt = torch.from_numpy(b).cuda()
     if strips is not None:
         monkeypatch.setenv("EG_MARCH_STRIPS", str(strips))
+    monkeypatch.setenv("EG_FUSE", "1")   # small grids default to the 5-kernel schedule
     s1 = egs.Solver(g, bd, mode)
+    monkeypatch.delenv("EG_FUSE")
     monkeypatch.delenv("EG_MARCH_STRIPS", raising=False)
     monkeypatch.setenv("EG_NO_FUSE", "1")
     s2 = egs.Solver(g, bd, mode)
