@@ -129,6 +129,7 @@ struct eg_solver {
     int cpt = 1;                 // columns per thread of the Thomas / update kernels (2 if nx even)
     size_t smem_th = 0;
     bool use_tm = false;         // fp32 Thomas with TMEM-resident factors (nz <= 128)
+    bool use_tm64 = false;       // fp64 Thomas with TMEM-resident factors (nz <= 80)
     size_t smem_tm = 0;
     // graphs of one iteration, keyed on the iterate pointer (two: eg_solve_batch alternates buffers)
     cudaGraphExec_t graphs[2]{};
@@ -506,7 +507,8 @@ int iteration(eg_solver* s, void* x_it) {
             else if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
             else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
         } else {
-            if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+            if (s->use_tm64) k_thomas_tm64<1><<<gtm, 128, TM64_SMEM, s->st>>>(s->geo, v, nullptr, v.z);
+            else if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
             else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
         }
         CK(cudaGetLastError());
@@ -525,7 +527,8 @@ int iteration(eg_solver* s, void* x_it) {
             else if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
             else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
         } else {
-            if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+            if (s->use_tm64) k_thomas_tm64<2><<<gtm, 128, TM64_SMEM, s->st>>>(s->geo, v, nullptr, v.zs);
+            else if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
             else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
         }
         CK(cudaGetLastError());
@@ -859,6 +862,14 @@ int precond_impl(eg_solver* s, const void* r, void* z) {
             return EG_OK;
         }
     }
+    if constexpr (MODE == 0) {
+        if (s->use_tm64) {
+            const dim3 gtm((unsigned)((s->grid.nx + 127) / 128), (unsigned)s->L.nyl);
+            k_thomas_tm64<0><<<gtm, 128, TM64_SMEM, s->st>>>(s->geo, v, (const V*)r, (V*)z);
+            CK(cudaGetLastError());
+            return EG_OK;
+        }
+    }
     if (s->cpt == 2) k_thomas<MODE, 0, 2><<<gt, s->wth / 2, s->smem_th, s->st>>>(s->geo, v, (const V*)r, (V*)z);
     else k_thomas<MODE, 0, 1><<<gt, s->wth, s->smem_th, s->st>>>(s->geo, v, (const V*)r, (V*)z);
     CK(cudaGetLastError());
@@ -1115,6 +1126,7 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     {
         const char* no_tm = getenv("EG_NO_TMEM");
         s->use_tm = prec != EG_FP64 && grid->nz <= 128 && !(no_tm && no_tm[0] == '1');
+        s->use_tm64 = prec == EG_FP64 && grid->nz <= 80 && !(no_tm && no_tm[0] == '1');
         s->smem_tm = std::max<size_t>(TM_SMEM, (size_t)grid->nz * 128 * sizeof(float));
     }
     if (s->smem_th > 227 * 1024) {
@@ -1123,6 +1135,11 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         return rc;
     }
     int rc = prec == EG_FP64 ? set_thomas_smem<0>(s) : prec == EG_MIXED ? set_thomas_smem<1>(s) : set_thomas_smem<2>(s);
+    if (rc == EG_OK && s->use_tm64) {
+        for (const void* f : {(const void*)k_thomas_tm64<0>, (const void*)k_thomas_tm64<1>, (const void*)k_thomas_tm64<2>})
+            if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, TM64_SMEM) != cudaSuccess)
+                rc = fail(s, EG_ERR_CUDA, "k_thomas_tm64 attributes");
+    }
     // EG_FORCE_NCCL=1 runs a single GPU through the multi-rank path (1-rank communicator: local
     // group sums -> ncclAllGather -> logic kernel, all inside the captured graph) so that path is
     // exercised by the single-GPU parity tests.

@@ -69,6 +69,11 @@ __device__ __forceinline__ void pf_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// L2 prefetch distance (levels) of the shared-memory-factor Thomas kernel (the FP64 path), 0 = off
+#ifndef TH_PF
+#define TH_PF 16
+#endif
+
 // FP32 mode keeps its global sums in binary32: emulate exactly by rounding after every add
 template <int MODE> __device__ __forceinline__ double rs(double a) {
     return MODE == 2 ? (double)(float)a : a;
@@ -342,6 +347,16 @@ __global__ void __launch_bounds__(128) k_thomas(Geo g, Vecs<MODE> vv,
                 if (KIND == 2) v[e] = ldv<CPT>(Vv + o);
                 u[e] = ldv<2 * CPT>(UD + 2 * o);
             }
+            if (TH_PF > 0 && k + TH_PF < nz) {  // warp-uniform: L2 prefetch TH_PF levels ahead
+                const int of = (k + TH_PF) * nx;
+                const int l = threadIdx.x & 31;
+                if ((l * CPT * (int)sizeof(V)) % 32 == 0) {  // one per 32-byte sector
+                    pf_l2(A0 + of);
+                    if (KIND == 1) { pf_l2(Pp + of); pf_l2(Vv + of); }
+                    if (KIND == 2) pf_l2(Vv + of);
+                }
+                if ((l * 2 * CPT * (int)sizeof(V)) % 32 == 0) pf_l2(UD + 2 * of);
+            }
         }
     };
     load(0, ca, cp, cv, cu);
@@ -588,6 +603,144 @@ __global__ void __launch_bounds__(128, 4) k_thomas_tm(Geo g, Vecs<MODE> vv, cons
     thomas_tm_tile<MODE, KIND>(g, vv, (int64_t)blockIdx.y * g.row, i, act, base + ((uint32_t)(warp * 32) << 16),
                                reinterpret_cast<float*>(smraw), beta, omega, alpha, fresh, fin, zout);
     tm_free128(base);
+}
+
+// FP64 Thomas with the elimination factors c'_k in TENSOR MEMORY (two 32-bit columns per level;
+// 256 columns per 128-column CTA, so at most two CTAs per SM, which the shared-memory request also
+// enforces) and y_k in shared memory [k][128]: 8 warps per SM instead of the 6 the two
+// shared-memory factor arrays allow, plus an L2 prefetch TM_PF levels ahead.  Same recurrence,
+// operation for operation, as k_thomas<0>.  KIND as in k_thomas.  grid (ceil(nx/128), nyl), 128 thr.
+constexpr int TM64_SMEM = 80 * 1024;  // >= nz * 128 * 8 (nz <= 80); > 228 KB / 3
+template <int KIND>
+__global__ void __launch_bounds__(128, 2) k_thomas_tm64(Geo g, Vecs<0> vv, const double* __restrict__ fin,
+                                                        double* __restrict__ zout) {
+    using V = double;
+    constexpr int KB = 4;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ uint32_t tm_slot;
+    V beta = 0, omega = 0, alpha = 0;
+    bool fresh = false;
+    if (KIND != 0) {
+        const DevState* st = vv.st;
+        if (st->halt != H_RUN) return;  // uniform
+        if (KIND == 1) {
+            fresh = st->fresh != 0;
+            beta = st->beta_v;
+            omega = st->omega_v;
+        } else {
+            alpha = st->alpha_v;
+        }
+    }
+    if ((threadIdx.x >> 5) == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tm_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = tm_slot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+    const int nx = (int)g.nx, nz = (int)g.nz;
+    const int i_raw = blockIdx.x * 128 + tid;
+    const bool act = i_raw < nx;
+    const int i = act ? i_raw : nx - 1;  // inactive lanes read a valid column, never store
+    const int64_t base = (int64_t)blockIdx.y * g.row + i;
+    const V* __restrict__ A0 = (KIND == 0 ? fin : vv.r) + base;
+    const V* __restrict__ Pp = vv.p + base;
+    const V* __restrict__ Vv = vv.v + base;
+    const V* __restrict__ UD = vv.B2 + 2 * base;
+    V* __restrict__ Pw = (KIND == 1 ? vv.p : vv.s) + base;
+    V* __restrict__ Zw = zout + base;
+    V* ys = reinterpret_cast<V*>(smraw);
+    V ca[KB], cp[KB], cv[KB], na[KB], np[KB], nv[KB];
+    VecN<V, 2> cu[KB], nu[KB];
+#pragma unroll
+    for (int e = 0; e < KB; ++e) {
+        ca[e] = cp[e] = cv[e] = na[e] = np[e] = nv[e] = 0.0;
+        cu[e].v[0] = cu[e].v[1] = nu[e].v[0] = nu[e].v[1] = 0.0;
+    }
+    auto load = [&](int k0, V(&a)[KB], V(&p)[KB], V(&v)[KB], VecN<V, 2>(&u)[KB]) {
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const int o = min(k0 + e, nz - 1) * nx;  // tail levels re-read the last one (L1 hit)
+            a[e] = A0[o];
+            if (KIND == 1 && !fresh) { p[e] = Pp[o]; v[e] = Vv[o]; }
+            if (KIND == 2) v[e] = Vv[o];
+            u[e] = ldv<2>(UD + 2 * o);
+            if (TM_PF > 0 && k0 + e + TM_PF < nz) {  // warp-uniform
+                const int of = (k0 + e + TM_PF) * nx;
+                if ((tid & 3) == 0) {  // one prefetch per 32-byte sector of each array
+                    pf_l2(A0 + of);
+                    if (KIND == 1) { pf_l2(Pp + of); pf_l2(Vv + of); }
+                    if (KIND == 2) pf_l2(Vv + of);
+                }
+                if ((tid & 1) == 0) pf_l2(UD + 2 * of);
+            }
+        }
+    };
+    load(0, ca, cp, cv, cu);
+    V cprev = 0, yprev = 0;
+    for (int k0 = 0; k0 < nz; k0 += KB) {
+        if (k0 + KB < nz) load(k0 + KB, na, np, nv, nu);
+        float cw[2 * KB];  // the c'_k as pairs of 32-bit words
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            const int k = k0 + e;
+            V c = 0;
+            if (k < nz) {
+                V f;
+                if (KIND == 0) f = ca[e];
+                else if (KIND == 1) f = fresh ? ca[e] : fma(beta, fma(-omega, cv[e], cp[e]), ca[e]);
+                else f = fma(-alpha, cv[e], ca[e]);
+                if (KIND != 0 && act) Pw[k * nx] = f;
+                const V u = cu[e].v[0], d = cu[e].v[1];
+                V y;
+                if (k == 0) {
+                    c = u;
+                    y = f;
+                } else {
+                    const V inv = rcp_fast<V>(fma(-d, cprev, (V)1));
+                    c = u * inv;
+                    y = fma(-d, yprev, f) * inv;
+                }
+                ys[k * 128 + tid] = y;
+                cprev = c;
+                yprev = y;
+            }
+            const unsigned long long cb = __double_as_longlong(c);
+            cw[2 * e] = __uint_as_float((uint32_t)cb);
+            cw[2 * e + 1] = __uint_as_float((uint32_t)(cb >> 32));
+        }
+        tm_st8(tl + (uint32_t)(2 * k0), cw);
+#pragma unroll
+        for (int e = 0; e < KB; ++e) { ca[e] = na[e]; cp[e] = np[e]; cv[e] = nv[e]; cu[e] = nu[e]; }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    V zn = yprev;
+    if (act) Zw[(nz - 1) * nx] = zn;
+    for (int k0 = ((nz - 1) / KB) * KB; k0 >= 0; k0 -= KB) {
+        float cw[2 * KB];
+        tm_ld8(tl + (uint32_t)(2 * k0), cw);
+#pragma unroll
+        for (int e = KB - 1; e >= 0; --e) {
+            const int k = k0 + e;
+            if (k <= nz - 2) {
+                const V c = __longlong_as_double((long long)(((unsigned long long)__float_as_uint(cw[2 * e + 1]) << 32) |
+                                                             __float_as_uint(cw[2 * e])));
+                zn = fma(-c, zn, ys[k * 128 + tid]);
+                if (act) Zw[k * nx] = zn;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tbase) : "memory");
+    }
 }
 
 // Multi-GPU fused schedule: z of the band's first and last local rows (those with a neighbouring
