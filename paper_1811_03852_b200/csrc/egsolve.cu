@@ -431,8 +431,10 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
         for (int colour = 0; colour < 2; ++colour) {
             {
                 ProfScope ps(s, KID_SOR, sor_alg_bytes(s, KIND, sw, colour));
+                bool tma = false;
                 if constexpr (MODE != 0) {
-                    if (s->sor_tma && s->split) {
+                    tma = s->sor_tma && s->split;
+                    if (tma) {  // fp32 with colour-split copies: the first-sweep red kernel + TMA sweeps
                         const int so_smem = SO_STAGES * SO_STAGE_FLOATS * 4 + 128;
                         if (sw == 0 && colour == 0)  // red half + f of both colours
                             k_sor_first_red<MODE, KIND><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, (const float*)fin,
@@ -443,17 +445,17 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
                         else
                             k_sor_tma<MODE, false><<<2 * s->nsm, SO_THREADS, so_smem, s->st>>>(
                                 s->geo, v, (float*)z, colour, s->sor_omega, KIND != 0, s->sor_maps[zi]);
-                        CK(cudaGetLastError());
-                        goto launched;
                     }
                 }
-                if (sw == 0)
-                    k_sor_half<MODE, KIND, true><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, colour, s->sor_omega, 0, sp);
-                else
-                    k_sor_half<MODE, 0, false><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fsrc, z, colour, s->sor_omega,
-                                                                                   KIND != 0, sp);
+                if (!tma) {
+                    if (sw == 0)
+                        k_sor_half<MODE, KIND, true><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, colour,
+                                                                                         s->sor_omega, 0, sp);
+                    else
+                        k_sor_half<MODE, 0, false><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fsrc, z, colour,
+                                                                                       s->sor_omega, KIND != 0, sp);
+                }
                 CK(cudaGetLastError());
-            launched:;
             }
             if ((rc = halo_ghosted(s, z))) return rc;
         }
