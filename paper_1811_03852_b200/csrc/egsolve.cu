@@ -1329,9 +1329,9 @@ int eg_solve_batch(eg_solver* s, int count, const double* const* b, double* cons
         const int i = k & 1;
         // db[(k+1) % 2] was read by solve k-1, which has returned: refill it while solve k runs
         if (k + 1 < count && (rc = upload(k + 1))) break;
+        if (bands && (rc = eg_solver_set_operator(s, bands))) break;  // overlaps the upload of b[k]
         CK(cudaStreamWaitEvent(s->st, s->ev_in[i], 0));
         if (k >= 2) CK(cudaStreamWaitEvent(s->st, s->ev_out[i], 0));  // dx[i]'s download (solve k-2)
-        if (bands && (rc = eg_solver_set_operator(s, bands))) break;
         rc = eg_solve(s, db[i], nullptr, params, dx[i], history ? history + (size_t)k * hs : nullptr,
                       info ? info + k : nullptr);
         if (rc) break;
