@@ -775,7 +775,7 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
         if (h->halt == H_START_MAXIT) break;
     }
 
-    if (rc == EG_OK || rc == EG_ERR_BREAKDOWN || rc == EG_ERR_NONFINITE) {
+    if (rc != EG_ERR_CUDA && rc != EG_ERR_NCCL) {  // x = 0 if no update has stored it
         const int rc0 = materialise_x0<MODE>(s, x_it);
         if (rc0) return rc0;
     }

@@ -199,6 +199,10 @@ def test_error_paths():
     with pytest.raises(egs.EgError) as e:
         s.solve(torch.zeros(prob.n, dtype=torch.float64, device="cuda"))
     assert e.value.status == 3
+    # the degenerate right-hand side leaves x = 0 (the entry does not store it; the exit does)
+    out = torch.full((prob.n,), float("nan"), dtype=torch.float64, device="cuda")
+    _, info, _ = s.solve(torch.zeros(prob.n, dtype=torch.float64, device="cuda"), out=out, raise_on_error=False)
+    assert info.status == 3 and bool(torch.all(out == 0.0))
     bb = b.copy(); bb[5] = np.nan
     _, info, _ = s.solve(torch.from_numpy(bb).cuda(), raise_on_error=False)
     assert info.status == 5
