@@ -70,7 +70,8 @@ typedef enum { EG_FP64 = 0, EG_MIXED = 1, EG_FP32 = 2 } eg_precision;
  * order and aligned to the 8 fixed reduction row-groups (group g = rows [g*ny/G, (g+1)*ny/G),
  * G = min(8, ny)), i.e. nranks must divide G; that fixed grouping makes every global sum — and
  * so x and the history — bitwise identical for any nranks.  nccl_unique_id points to the 128-byte
- * ncclUniqueId from eg_nccl_unique_id() on rank 0, broadcast by the caller (NULL if nranks == 1). */
+ * ncclUniqueId from eg_nccl_unique_id() on rank 0, broadcast by the caller (NULL if nranks == 1),
+ * or to an id from eg_loopback_id() (the in-process test transport, below). */
 typedef struct {
     int64_t j_begin, j_end;
     int32_t rank, nranks;
@@ -197,6 +198,19 @@ const char* eg_status_str(int status);
 
 /* Fill out[128] with a fresh ncclUniqueId (call on rank 0, broadcast to the others). */
 int eg_nccl_unique_id(char out[128]);
+
+/* In-process loopback transport, for testing the latitude-band decomposition (DESIGN.md
+ * §Multi-GPU) on ONE GPU.  Fills out[128] with an id naming a new group of nranks ranks; pass it
+ * as eg_dist.nccl_unique_id to exactly nranks eg_solver_create calls in this process (one per
+ * rank), all on the same device and the SAME stream (EG_ERR_ARG otherwise).  Every call that
+ * exchanges data (eg_apply_operator, tri-SOR eg_precondition, eg_solve, eg_solve_batch) must then
+ * be made on all ranks concurrently, one host thread per rank: each halo exchange and group-sum
+ * all-gather is a host barrier plus device-to-device copies on the shared stream, so the ranks'
+ * kernels run one after another in enqueue order and never wait on each other.  Solves are
+ * launched kernel by kernel (no CUDA graph).  A rank that fails or stops calling makes the others'
+ * exchange fail with EG_ERR_NCCL after 120 s.  The group is freed with its last member; an id must
+ * not be reused after that.  Errors: EG_ERR_ARG (out NULL, nranks < 1). */
+int eg_loopback_id(int nranks, char out[128]);
 
 /* ---- kernel-level profiling (EG_SOLVE_PROFILE): CUDA events on the solver's stream ---- */
 int eg_num_kernels(void);

@@ -28,7 +28,7 @@ STATUS = {0: "EG_OK", 1: "EG_ERR_ARG", 2: "EG_ERR_SINGULAR_DIAG", 3: "EG_ERR_DEG
 ABI_SYMBOLS = ("eg_workspace_bytes", "eg_workspace_bytes_ex", "eg_solver_create", "eg_solver_set_operator",
                "eg_solver_set_preconditioner", "eg_apply_operator", "eg_precondition",
                "eg_solve", "eg_solve_batch", "eg_solver_destroy", "eg_last_error", "eg_status_str",
-               "eg_nccl_unique_id", "eg_num_kernels", "eg_kernel_name", "eg_profile_get",
+               "eg_nccl_unique_id", "eg_loopback_id", "eg_num_kernels", "eg_kernel_name", "eg_profile_get",
                "eg_profile_reset")
 
 
@@ -103,6 +103,7 @@ def lib():
         L.eg_status_str.argtypes = [i32]
         L.eg_status_str.restype = ctypes.c_char_p
         L.eg_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.eg_loopback_id.argtypes = [i32, ctypes.c_char_p]
         L.eg_num_kernels.restype = i32
         L.eg_kernel_name.argtypes = [i32]
         L.eg_kernel_name.restype = ctypes.c_char_p
@@ -131,6 +132,16 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def loopback_id(nranks: int) -> bytes:
+    """Id of a new in-process loopback group (eg_loopback_id): pass it as
+    Solver(..., dist=(rank, nranks, id)) for each rank, all on one stream, one thread per rank."""
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().eg_loopback_id(nranks, buf)
+    if rc:
+        raise EgError(rc, "eg_loopback_id")
+    return buf.raw
+
+
 def _ptr(t) -> ctypes.c_void_p:
     if t is None:
         return ctypes.c_void_p(0)
@@ -149,10 +160,13 @@ class Solver:
     torch.distributed process group for a latitude-band decomposition (one rank per GPU).
     """
 
-    def __init__(self, grid, bands, precision="mixed", group=None, stream=None, trisor=False, batch=False):
+    def __init__(self, grid, bands, precision="mixed", group=None, stream=None, trisor=False, batch=False,
+                 dist=None):
         """trisor=True sizes the workspace for the colour-split tri-SOR copies (EG_FEATURE_TRISOR);
         set_preconditioner("trisor") works either way, faster with them.  batch=True adds the
-        staging buffers solve_batch needs (EG_FEATURE_BATCH)."""
+        staging buffers solve_batch needs (EG_FEATURE_BATCH).  dist=(rank, nranks, id) gives the
+        decomposition explicitly instead of a process group (id: 128 bytes from nccl_unique_id()
+        or loopback_id())."""
         import torch
         self.grid = tuple(int(v) for v in grid)
         nx, ny, nz = self.grid
@@ -162,19 +176,24 @@ class Solver:
         self.device = bands.device
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self._uid = None
-        if group is not None:
-            import torch.distributed as dist
-            rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        uid = None
+        if dist is not None:
+            rank, nranks, uid = int(dist[0]), int(dist[1]), dist[2]
+        elif group is not None:
+            import torch.distributed as tdist
+            rank, nranks = tdist.get_rank(group), tdist.get_world_size(group)
         else:
             rank, nranks = 0, 1
         self.rank, self.nranks = rank, nranks
         self.j_begin, self.j_end = band_rows(ny, rank, nranks) if nranks > 1 else (0, ny)
         self.n_local = (self.j_end - self.j_begin) * nx * nz
         if nranks > 1:
-            import torch.distributed as dist
-            obj = [nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0), group=group)
-            self._uid = ctypes.create_string_buffer(obj[0], 128)
+            if uid is None:
+                import torch.distributed as tdist
+                obj = [nccl_unique_id() if rank == 0 else None]
+                tdist.broadcast_object_list(obj, src=tdist.get_global_rank(group, 0), group=group)
+                uid = obj[0]
+            self._uid = ctypes.create_string_buffer(uid, 128)
             self._dist = _Dist(self.j_begin, self.j_end, rank, nranks,
                                ctypes.cast(self._uid, ctypes.c_void_p))
             dptr = ctypes.byref(self._dist)

@@ -2,16 +2,20 @@
 //
 // Host responsibilities only: validation, workspace carving, launch geometry, the restart /
 // verification state machine of DESIGN.md §Algorithm (mirrors), CUDA-graph
-// replay of the iteration, NCCL halo exchange and group-sum all-gather for latitude bands, and
+// replay of the iteration, NCCL halo exchange and group-sum all-gather for latitude bands (or the
+// in-process loopback transport that runs the same decomposition on one GPU for tests), and
 // per-kernel CUDA-event profiling.  All arithmetic of the method runs in the kernels.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -82,6 +86,48 @@ struct PendingEv { int kid; cudaEvent_t a, b; double bytes; };
 
 }  // namespace
 
+// In-process loopback transport (eg_loopback_id): the ranks of a latitude-band decomposition are
+// handles in ONE process on ONE GPU, each driven by its own host thread, all created on the same
+// stream.  An exchange posts this rank's buffers, meets the other ranks at a host barrier, enqueues
+// device-to-device copies from the neighbours' buffers on the shared stream and meets them again
+// (so no rank moves on and overwrites a posted buffer before everyone has enqueued its reads).
+// Every kernel of every rank runs in enqueue order on that one stream: no kernel ever waits for
+// another rank's kernel (B200_PROFILING.md: ranks must not spin on each other on one GPU).
+struct LoopGroup {
+    int n = 0;
+    int refs = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    bool broken = false;
+    bool have_st = false;
+    cudaStream_t st = nullptr;
+    std::vector<const unsigned char*> first, last;  // posted edge rows
+    std::vector<const double*> gsum;                // posted group sums
+};
+constexpr char kLoopMagic[8] = {'E', 'G', 'L', 'O', 'O', 'P', 'B', 'K'};
+
+// all n ranks arrive or the wait times out (a rank that failed never comes): false = broken group
+bool lb_barrier(LoopGroup* G) {
+    std::unique_lock<std::mutex> lk(G->m);
+    if (G->broken) return false;
+    const uint64_t my = G->gen;
+    if (++G->arrived == G->n) {
+        G->arrived = 0;
+        ++G->gen;
+        G->cv.notify_all();
+        return true;
+    }
+    const bool ok = G->cv.wait_for(lk, std::chrono::seconds(120), [&] { return G->gen != my || G->broken; });
+    if (!ok || G->broken) {
+        G->broken = true;
+        G->cv.notify_all();
+        return false;
+    }
+    return true;
+}
+
 struct eg_solver {
     eg_grid grid{};
     int64_t j_begin = 0, j_end = 0;
@@ -137,8 +183,9 @@ struct eg_solver {
     int graph_next = 0;  // entry replaced on the next miss
     cudaGraphExec_t graph = nullptr;  // the entry for the current solve
     void* graph_x = nullptr;
-    // NCCL
+    // NCCL, or the loopback group (tests)
     ncclComm_t comm = nullptr;
+    LoopGroup* lb = nullptr;
     // profiling
     bool profiling = false;
     std::vector<cudaEvent_t> evpool;
@@ -253,12 +300,29 @@ Vecs<MODE> vecs(eg_solver* s, void* x_it) {
 
 // -------- multi-GPU plumbing (latitude bands) --------
 // exchange the boundary rows of a ghosted array with the j-neighbours
+bool multi(const eg_solver* s) { return s->comm != nullptr || s->lb != nullptr; }
+
+int lb_fail(eg_solver* s) {
+    return fail(s, EG_ERR_NCCL, "loopback group: a rank failed or did not arrive within 120 s");
+}
+
 int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz) {
     if (s->nranks == 1) return EG_OK;
     const size_t rowb = (size_t)s->L.row * esz;
     ncclDataType_t ty = esz == 8 ? ncclDouble : ncclFloat;
     unsigned char* first = (unsigned char*)row0;
     unsigned char* last = first + (size_t)(s->L.nyl - 1) * rowb;
+    if (s->lb) {
+        LoopGroup* G = s->lb;
+        G->first[s->rank] = first;
+        G->last[s->rank] = last;
+        if (!lb_barrier(G)) return lb_fail(s);
+        if (s->rank > 0) CK(cudaMemcpyAsync(ghost_lo, G->last[s->rank - 1], rowb, cudaMemcpyDeviceToDevice, s->st));
+        if (s->rank < s->nranks - 1)
+            CK(cudaMemcpyAsync(ghost_hi, G->first[s->rank + 1], rowb, cudaMemcpyDeviceToDevice, s->st));
+        if (!lb_barrier(G)) return lb_fail(s);
+        return EG_OK;
+    }
     NK(ncclGroupStart());
     if (s->rank > 0) {
         NK(ncclSend(first, s->L.row, ty, s->rank - 1, s->comm, s->st));
@@ -283,7 +347,7 @@ int finalize(eg_solver* s, int first, int tiles = 0) {
     ProfScope ps(s, KID_FIN);
     Geo geo = s->geo;
     if (tiles > 0) geo.tiles = tiles;  // slots per row of the producing kernel
-    if (s->comm == nullptr) {  // one GPU: group sums and logic in one CTA
+    if (!multi(s)) {  // one GPU: group sums and logic in one CTA
         k_fin<MODE, WHICH><<<1, 1024, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum, first);
         CK(cudaGetLastError());
         return EG_OK;
@@ -292,7 +356,17 @@ int finalize(eg_solver* s, int first, int tiles = 0) {
     k_fin_groups<MODE, WHICH><<<1, 1024, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum);
     CK(cudaGetLastError());
     const int gl = s->geo.g_hi - s->geo.g_lo;
-    NK(ncclAllGather(s->gsum, s->gall, (size_t)gl * NQ, ncclDouble, s->comm, s->st));
+    if (s->lb) {  // all-gather: rank r's block lands at gall + r * gl * NQ, as ncclAllGather places it
+        LoopGroup* G = s->lb;
+        G->gsum[s->rank] = s->gsum;
+        if (!lb_barrier(G)) return lb_fail(s);
+        for (int r = 0; r < s->nranks; ++r)
+            CK(cudaMemcpyAsync(s->gall + (size_t)r * gl * NQ, G->gsum[r], (size_t)gl * NQ * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s->st));
+        if (!lb_barrier(G)) return lb_fail(s);
+    } else {
+        NK(ncclAllGather(s->gsum, s->gall, (size_t)gl * NQ, ncclDouble, s->comm, s->st));
+    }
     k_fin_logic<MODE, WHICH><<<1, 32, 0, s->st>>>(geo, s->gall, s->dstate, first);
     CK(cudaGetLastError());
     return EG_OK;
@@ -333,7 +407,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
     if constexpr (MODE != 0) {
         const unsigned grid = (unsigned)(s->mg.strips * s->L.tiles);
         const dim3 gedge((unsigned)s->L.tiles, 2u);
-        if (s->comm) {  // latitude bands: z of the band's edge rows -> the neighbours' ghost rows
+        if (multi(s)) {  // latitude bands: z of the band's edge rows -> the neighbours' ghost rows
             k_edge_rows<MODE, 1><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.z);
             CK(cudaGetLastError());
             if ((rc = halo_ghosted(s, v.z))) return rc;
@@ -368,7 +442,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
 #endif
         if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
-        if (s->comm) {
+        if (multi(s)) {
             k_edge_rows<MODE, 2><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.zs);
             CK(cudaGetLastError());
             if ((rc = halo_ghosted(s, v.zs))) return rc;
@@ -647,7 +721,8 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     const int64_t n = s->L.n;
     int rc = EG_OK;
     s->profiling = (prm->flags & EG_SOLVE_PROFILE) != 0;
-    const bool use_graph = !(prm->flags & (EG_SOLVE_NO_GRAPH | EG_SOLVE_PROFILE));
+    // (loopback ranks meet at host barriers inside every exchange: launched directly, never replayed)
+    const bool use_graph = !(prm->flags & (EG_SOLVE_NO_GRAPH | EG_SOLVE_PROFILE)) && s->lb == nullptr;
     eg_solve_info inf{};
 
     // ---- inputs: b (host -> staged into bhat, scaled in place), x iterate ----
@@ -1147,7 +1222,26 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     // exercised by the single-GPU parity tests.
     const char* force = getenv("EG_FORCE_NCCL");
     const bool force_nccl = s->nranks == 1 && force && force[0] == '1';
-    if (rc == EG_OK && (s->nranks > 1 || force_nccl)) {
+    const bool loop = rc == EG_OK && s->nranks > 1 && dist->nccl_unique_id &&
+                      memcmp(dist->nccl_unique_id, kLoopMagic, sizeof kLoopMagic) == 0;
+    if (loop) {  // in-process loopback group (eg_loopback_id)
+        LoopGroup* G = nullptr;
+        int32_t gn = 0;
+        memcpy(&G, (const char*)dist->nccl_unique_id + 8, sizeof G);
+        memcpy(&gn, (const char*)dist->nccl_unique_id + 16, sizeof gn);
+        if (!G || gn != s->nranks) {
+            rc = fail(s, EG_ERR_ARG, "loopback id is for %d ranks, dist says %d", gn, s->nranks);
+        } else {
+            std::lock_guard<std::mutex> lk(G->m);
+            if (G->have_st && G->st != s->st) {
+                rc = fail(s, EG_ERR_ARG, "the ranks of a loopback group must share one stream");
+            } else {
+                G->have_st = true;
+                G->st = s->st;
+                s->lb = G;
+            }
+        }
+    } else if (rc == EG_OK && (s->nranks > 1 || force_nccl)) {
         ncclUniqueId id;
         ncclResult_t r = ncclSuccess;
         if (force_nccl) r = ncclGetUniqueId(&id);
@@ -1359,6 +1453,15 @@ void eg_solver_destroy(eg_solver* s) {
         if (s->ev_out[i]) cudaEventDestroy(s->ev_out[i]);
     }
     if (s->comm) ncclCommDestroy(s->comm);
+    if (s->lb) {  // the last member frees the group
+        LoopGroup* G = s->lb;
+        bool last;
+        {
+            std::lock_guard<std::mutex> lk(G->m);
+            last = --G->refs == 0;
+        }
+        if (last) delete G;
+    }
     for (auto& p : s->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto e : s->evpool) cudaEventDestroy(e);
     if (s->hstate) cudaFreeHost(s->hstate);
@@ -1388,6 +1491,21 @@ int eg_nccl_unique_id(char out[128]) {
     if (ncclGetUniqueId(&id) != ncclSuccess) return EG_ERR_NCCL;
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
     memcpy(out, &id, 128);
+    return EG_OK;
+}
+
+int eg_loopback_id(int nranks, char out[128]) {
+    if (!out || nranks < 1) return EG_ERR_ARG;
+    LoopGroup* G = new LoopGroup();
+    G->n = G->refs = nranks;
+    G->first.assign(nranks, nullptr);
+    G->last.assign(nranks, nullptr);
+    G->gsum.assign(nranks, nullptr);
+    memset(out, 0, 128);
+    memcpy(out, kLoopMagic, sizeof kLoopMagic);
+    memcpy(out + 8, &G, sizeof G);
+    const int32_t n32 = nranks;
+    memcpy(out + 16, &n32, sizeof n32);
     return EG_OK;
 }
 
