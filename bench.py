@@ -162,7 +162,8 @@ def oracle_sample(prob, precision, target_s=12.0):
 def run_reference(args, prob, ws, rank):
     if rank != 0:
         return
-    import oracle  # noqa: F401  (the reference arm is the CPU oracle)
+    import oracle  # the reference arm is the CPU oracle
+    oracle.set_threads(os.cpu_count() or 1)  # all host cores, also under torchrun (OMP_NUM_THREADS=1)
     for _ in range(args.warmup):
         oracle_sample(prob, args.precision, target_s=1.0)
     vals, secs = [], 0.0
@@ -402,10 +403,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-trisor", action="store_true", help="skip the tri-SOR preconditioner block")
     args = ap.parse_args()
-    subprocess.check_call(["make", "-s", "all"], cwd=ROOT, stdout=subprocess.DEVNULL)
+    ws, rank, local = dist_init(args)
+    if rank == 0:  # one build, not one per rank racing on the same files
+        subprocess.check_call(["make", "-s", "all"], cwd=ROOT, stdout=subprocess.DEVNULL)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
     import gen
     prob = gen.CONFIGS[args.config]
-    ws, rank, local = dist_init(args)
     if args.impl == "reference":
         run_reference(args, prob, ws, rank)
     else:

@@ -93,6 +93,12 @@ def threads() -> int:
     return int(lib().oracle_threads())
 
 
+def set_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's row loops (results do not depend on it: per-row partial
+    sums are added in row order).  For launchers that export OMP_NUM_THREADS=1 (torchrun)."""
+    lib().omp_set_num_threads(ctypes.c_int(int(n)))
+
+
 class OracleError(RuntimeError):
     def __init__(self, status):
         super().__init__(STATUS.get(status, str(status)))
