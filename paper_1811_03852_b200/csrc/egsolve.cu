@@ -1257,7 +1257,7 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         const int64_t nz8 = (grid->nz + MA_KB - 1) / MA_KB * MA_KB;
         const size_t ring = 3 * (size_t)nz8 * MA_RING_W * sizeof(float);
-        const size_t budget = 227 * 1024 - 2048 - 128;  // dynamic + static shared memory per CTA
+        const size_t budget = 227 * 1024 - 3072 - 128;  // dynamic + static shared memory per CTA
         // two stage rings (elimination / stencil inputs) share what the z ring leaves
         const int na = ring < budget ? (int)((budget - ring) / ma_stage_bytes(1)) : 0;
         const int nb = ring < budget ? (int)((budget - ring) / ma_stage_bytes(2)) : 0;
@@ -1272,6 +1272,16 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
             s->mg.sst_a = std::min(MA_MAX_STAGES, na / 2);
             s->mg.fst_b = std::min(MA_MAX_STAGES, nb - nb / 2);
             s->mg.sst_b = std::min(MA_MAX_STAGES, nb / 2);
+            const char* fa = getenv("EG_MARCH_FST_A");  // tuning: elimination-ring stages (rest: stencil)
+            const char* fb = getenv("EG_MARCH_FST_B");
+            if (fa && atoi(fa) >= 2 && na - atoi(fa) >= 2) {
+                s->mg.fst_a = std::min(MA_MAX_STAGES, atoi(fa));
+                s->mg.sst_a = std::min(MA_MAX_STAGES, na - atoi(fa));
+            }
+            if (fb && atoi(fb) >= 2 && nb - atoi(fb) >= 2) {
+                s->mg.fst_b = std::min(MA_MAX_STAGES, atoi(fb));
+                s->mg.sst_b = std::min(MA_MAX_STAGES, nb - atoi(fb));
+            }
             s->mg.strips = (int)std::min<int64_t>(s->L.nyl, nsm / s->L.tiles);
             const char* fs = getenv("EG_MARCH_STRIPS");  // tests: fewer, longer strips
             if (fs && atoi(fs) >= 1) s->mg.strips = std::min(s->mg.strips, atoi(fs));

@@ -17,8 +17,8 @@
 // three global sums.
 //
 // The inputs a CTA streams (r, p, v, (U,D) for the elimination; (E,W,N,S), rhat0 for the stencil)
-// do not depend on its arithmetic, so a producer warp streams them with TMA tensor copies into a
-// ring of MA_KB-level stages (mbarrier full / empty pairs) far ahead of the four consumer warps.  The
+// do not depend on its arithmetic, so two producer warps stream them with TMA tensor copies into
+// rings of MA_KS-level stages (mbarrier full / empty pairs) far ahead of the consumer warps.  The
 // arithmetic, its order and the reduction slots are those of k_thomas_tm + k_stencil, so the fused
 // schedule is bitwise identical to the 5-kernel one (tests/test_gpu_parity.py).
 //
@@ -39,7 +39,7 @@ namespace eg {
 
 constexpr int MA_KB = 8;                               // levels per stage
 constexpr int MA_CONS = 128;                           // consumer threads: one column each
-constexpr int MA_THREADS = 2 * MA_CONS + 64;           // stencil + Thomas warps, producer, publisher
+constexpr int MA_THREADS = 2 * MA_CONS + 128;          // stencil + Thomas warps, 2 producers, publisher, halo
 // stage = one MA_KB-level chunk of one row.  Elimination ring: r, (p,) v, (U, D); stencil ring:
 // (E, W, N, S) (, rhat0): 640 floats / level in phase A, 512 in phase B, for both rings
 constexpr int MA_KS = 4;  // levels per stage: a chunk of MA_KB levels is two stages (finer refill)
@@ -217,7 +217,7 @@ struct MarchGeo {
 constexpr int MA_MAX_CH = 9;     // chunks per column (nz <= 72)
 
 // KIND 1: phase A, KIND 2: phase B.  grid strips*tiles, block MA_THREADS: warps 0-3 stencil (S),
-// warps 4-7 Thomas (F; warp 4+w shares TMEM lanes, i.e. columns, with S warp w), warp 8 TMA producer,
+// warps 4-7 Thomas (F; warp 4+w shares TMEM lanes, i.e. columns, with S warp w), warps 8 / 10 TMA producers,
 // warp 9 publisher.  Dynamic shared memory: the two stage rings + 3*ceil8(nz)*130*4 B z ring + 128 B
 // of alignment slack (padded so that only one CTA fits an SM).
 //
@@ -252,6 +252,8 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     __shared__ __align__(8) uint64_t fullF[MA_MAX_STAGES], emptyF[MA_MAX_STAGES];
     __shared__ __align__(8) uint64_t fullS[MA_MAX_STAGES], emptyS[MA_MAX_STAGES];
     __shared__ __align__(8) uint64_t sread[MA_MAX_CH], zready[2], zdone[2];
+    __shared__ __align__(8) uint64_t hready[2], hfree[2], pubd[2];
+    __shared__ float hbuf[2][2][8 * MA_MAX_CH];  // E / W halo columns of rows r_x, slot x & 1
     __shared__ uint32_t tm_slot;
     __shared__ double red[32 * 3];
     DevState* st = vv.st;
@@ -291,6 +293,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
         for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], MA_CONS); }
         for (int c = 0; c < MA_MAX_CH; ++c) mbar_init(&sread[c], MA_CONS);
         for (int b = 0; b < 2; ++b) { mbar_init(&zready[b], MA_CONS); mbar_init(&zdone[b], MA_CONS); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&hready[b], 32); mbar_init(&hfree[b], MA_CONS); mbar_init(&pubd[b], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const uint32_t tbase = tm_alloc512(&tm_slot);  // contains __syncthreads()
@@ -300,8 +303,10 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
 #endif
     MA_CLK(t_all);
 
-    // ------------------------------------------------------------------ producer warp
-    if (warp == 8) {
+    // ------------------------------------------------------------------ producer warps
+    // warp 8 fills the elimination ring, warp 10 the stencil ring: one ring never waits for room in
+    // the other (a single producer in a fixed interleave starves one role whenever the other lags)
+    if (warp == 8 || warp == 10) {
         if (lane == 0 && L > 0) {
             int fslot = 0, fround = 0, sslot = 0, sround = 0;
             // elimination inputs of row jr, levels k0..k0+7: r, (p, v) or v, (U, D)
@@ -332,17 +337,14 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 if (KIND == 1) tma3(sb + OFF_RH, &maps.rh, i0, k0, jr, fb);
                 if (++sslot == NSS) { sslot = 0; ++sround; }
             };
-            for (int k0 = 0; k0 < NZ8; k0 += KS) fwd_stage(row_of(0), k0);
-            if (L >= 2)
-                for (int k0 = 0; k0 < NZ8; k0 += KS) fwd_stage(row_of(1), k0);
             for (int m = 0; m < L; ++m)
                 for (int k0 = 0; k0 < NZ8; k0 += KS) {
-                    sten_stage(row_of(m), k0);
-                    if (m + 2 < L) fwd_stage(row_of(m + 2), k0);
+                    if (warp == 8) fwd_stage(row_of(m), k0);
+                    else sten_stage(row_of(m), k0);
                 }
         }
 #ifdef MA_TRACE
-        if (lane == 0) {
+        if (lane == 0 && warp == 8) {
             MA_ADD(10, t_all);
             for (int q = 9; q < 11; ++q) g_ma_trace[(KIND - 1) * 512 * 16 + blockIdx.x * 16 + q] = tr[q];
         }
@@ -356,7 +358,33 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                 mbar_wait_sleep(&zdone[x & 1], (uint32_t)((x >> 1) & 1), 256);
                 MA_J(3);
                 st_release(flags + (int64_t)row_of(x) * T + t, epoch);  // gpu-scope release: z(r_x)
+                mbar_arrive(&pubd[x & 1]);
             }
+        return;
+    }
+    // ------------------------------------------------------------------ halo warp
+    // E / W halo columns of r_x (the neighbouring tiles' z, after their ready flags) into hbuf[x & 1],
+    // well ahead of the stencil of r_x: the stencil warps never wait on another CTA mid-step
+    const int tW = (t == 0) ? T - 1 : t - 1, tE = (t + 1 == T) ? 0 : t + 1;
+    const int iWg = (i0 == 0) ? nx - 1 : i0 - 1;         // W halo column (tile t-1, periodic)
+    const int iEg = (i0 + min(128, nx - i0) == nx) ? 0 : i0 + min(128, nx - i0);  // E halo column
+    if (warp == 11) {
+        V* __restrict__ Zh = KIND == 1 ? vv.z : vv.zs;
+        for (int x = 0; x < L; ++x) {
+            if (x >= 2) mbar_wait_sleep(&hfree[x & 1], (uint32_t)(((x - 2) >> 1) & 1), 64);  // copied out
+            const int jr = row_of(x);
+            if (lane < 2) {
+                const int* f = flags + (int64_t)jr * T + (lane == 0 ? tW : tE);
+                while (ld_acquire(f) != epoch) __nanosleep(64);
+            }
+            __syncwarp();
+            for (int k = lane; k < nz; k += 32) {
+                const V* zg = Zh + (int64_t)jr * g.row + (int64_t)k * nx;
+                hbuf[x & 1][0][k] = __ldcg(zg + iWg);
+                hbuf[x & 1][1][k] = __ldcg(zg + iEg);
+            }
+            mbar_arrive(&hready[x & 1]);  // every lane releases its own stores
+        }
         return;
     }
 
@@ -474,7 +502,9 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             MA_TFENCE_BEFORE();
             mbar_arrive(&zready[x & 1]);  // the S warps may read z(r_x) from the ring
             // the publisher may release the ready flag: these arrivals (release, CTA scope) and its
-            // wait (acquire) order every thread's z stores before its gpu-scope release of the flag
+            // wait (acquire) order every thread's z stores before its gpu-scope release of the flag.
+            // zdone[x & 1] must not run two phases ahead of the publisher: r_{x-2} published first.
+            if (x >= 2) mbar_wait(&pubd[x & 1], (uint32_t)(((x - 2) >> 1) & 1));
             mbar_arrive(&zdone[x & 1]);
             MA_ADD(14, t0);
         };
@@ -495,9 +525,6 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
         // ============================ stencil warps ============================
         V* __restrict__ Yw = KIND == 1 ? vv.v : vv.t;
         const int64_t per_q = (int64_t)nyl * T;
-        const int iWg = (i0 == 0) ? nx - 1 : i0 - 1;       // W halo column (tile t-1, periodic)
-        const int iEg = (i0 + w == nx) ? 0 : i0 + w;        // E halo column (tile t+1, periodic)
-        const int tW = (t == 0) ? T - 1 : t - 1, tE = (t + 1 == T) ? 0 : t + 1;
         int cslot = 0;
         uint32_t cphase = 0;
         auto wait_flag = [&](int row, int tile) {
@@ -509,7 +536,16 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             const V* src = Zw + (int64_t)row * g.row + i;
             for (int k = 0; k < nz; ++k) dst[k * MA_RING_W] = __ldcg(src + (int64_t)k * nx);
         };
-        float hw = 0.f, he = 0.f;  // prefetched halo values of r_{m+1} (thread k = tid < nz)
+        // E / W halo of r_x from hbuf into its ring slot (threads k = tid < nz), then free hbuf[x & 1]
+        auto copy_halo = [&](int x) {
+            if (tid < nz) {
+                mbar_wait(&hready[x & 1], (uint32_t)((x >> 1) & 1));
+                float* zr = slot_ptr(x);
+                zr[tid * MA_RING_W] = hbuf[x & 1][0][tid];
+                zr[tid * MA_RING_W + w + 1] = hbuf[x & 1][1][tid];
+            }
+            mbar_arrive(&hfree[x & 1]);
+        };
         for (int m = 0; m < L; ++m) {
             const int j = row_of(m);
             const int64_t jg = g.j0 + j;
@@ -530,18 +566,13 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             const bool ld_next = m == L - 1 && (dir > 0 ? hasN : hasS);   // r_L exists
             if (m == 0 || ld_next) {
                 if (tid == 0) {
-                    if (m == 0) { wait_flag(j, tW); wait_flag(j, tE); }
                     // rows of a neighbouring rank sit in the ghost rows -1 / nyl, exchanged before
                     // the launch: no flag
                     if (ld_prev && j - dir >= 0 && j - dir < nyl) wait_flag(j - dir, t);
                     if (ld_next && j + dir >= 0 && j + dir < nyl) wait_flag(j + dir, t);
                 }
                 cons_bar();
-                if (m == 0 && tid < nz) {
-                    const V* zg = Zw + (int64_t)j * g.row + (int64_t)tid * nx;
-                    zC0[tid * MA_RING_W] = __ldcg(zg + iWg);
-                    zC0[tid * MA_RING_W + w + 1] = __ldcg(zg + iEg);
-                }
+                if (m == 0) copy_halo(0);
                 if (ld_prev) load_row(slot_ptr(m - 1) + 1 + col, j - dir);
                 if (ld_next) load_row(slot_ptr(m + 1) + 1 + col, j + dir);
                 cons_bar();
@@ -559,24 +590,6 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             V zprev = 0.f;
             for (int c = 0; c < nch; ++c) {
                 const int k0 = c * KB;
-                if (c == (3 * nch) / 4 && m + 1 < L) {  // halo of r_{m+1} (published at the end of step m-1)
-                    MA_CLK(t_h);
-                    if (tid == 0) {
-                        const int jn = row_of(m + 1);
-                        wait_flag(jn, tW);
-                        wait_flag(jn, tE);
-                        // zdone[x & 1] may run at most one phase ahead of the publisher: it must have
-                        // published r_m before the F warps arrive for r_{m+2} (after sread of this step)
-                        if (m + 2 < L) wait_flag(j, t);
-                    }
-                    cons_bar();
-                    if (tid < nz) {
-                        const V* zg = Zw + (int64_t)row_of(m + 1) * g.row + (int64_t)tid * nx;
-                        hw = __ldcg(zg + iWg);
-                        he = __ldcg(zg + iEg);
-                    }
-                    MA_ADD(4, t_h);
-                }
                 // U, D (, s) of r_m from TMEM, bands / rhat0 from the stage, z from the ring
                 float ub[KB], db[KB], sv[KB];
                 tm_ld8_nw(tU(us) + (uint32_t)k0, ub);
@@ -661,10 +674,10 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) vv.slots[q * per_q + (int64_t)j * T + t] = acc[q];
             }
-            if (m + 1 < L && tid < nz) {
-                float* zn1 = slot_ptr(m + 1);
-                zn1[tid * MA_RING_W] = hw;
-                zn1[tid * MA_RING_W + w + 1] = he;
+            if (m + 1 < L) {
+                MA_CLK(t_h);
+                copy_halo(m + 1);
+                MA_ADD(1, t_h);
             }
             cons_bar();  // ring halo and `red` are rewritten by the next step
             MA_ADD(8, t_red);

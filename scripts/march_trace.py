@@ -34,7 +34,7 @@ assert egs.lib().eg_debug_march_trace(buf, 1024 * 16) == 0
 t = np.frombuffer(buf, dtype=np.uint64).reshape(2, 512, 16).astype(np.float64)[0 if a.which == "A" else 1]
 ncta = int((t[:, 0] > 0).sum())
 t = t[:ncta]
-names = ["S total", "-", " S stage waits", "-", " S flag/halo/boundary sync", " S wait z(r_m+1) from F",
+names = ["S total", " S halo copy (wait hready)", " S stage waits", "-", " S boundary-row sync", " S wait z(r_m+1) from F",
          " S stencil pass", "-", " S reduce", "PRODUCER empty-wait", "PRODUCER total", "F total",
          " F stage waits", " F wait sread (S behind)", " F back subst", " F elimination"]
 print(f"CTAs {ncta}; cycles per CTA (mean / min / max) of the last phase {a.which} launch")
