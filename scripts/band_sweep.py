@@ -1,0 +1,51 @@
+"""Per-rank work of the latitude-band decomposition, measured on one GPU: a C5 band of ny/P rows
+(2560 x 1920/P x 70) timed as a whole problem (fixed 8 iterations, CUDA events), for the fused
+schedule with each strip count and for the 5-kernel schedule.  The halo exchange and the
+all-gather are not included (they need P GPUs)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+import paper_1811_03852_b200 as egs  # noqa: E402
+
+base = gen.CONFIGS["C5"]
+for P in [int(a) for a in (sys.argv[1:] or ["1", "2", "4", "8"])]:
+    prob = base.with_(ny=base.ny // P)
+    bands = torch.empty((7, prob.n), dtype=torch.float64, device="cuda")
+    b = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    x = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    gen.device(prob, bands, b)
+    variants = [("5-kernel", {"EG_NO_FUSE": "1"}), ("fused default", {})] + \
+        [(f"fused strips={k}", {"EG_MARCH_STRIPS": str(k)}) for k in (1, 2, 3, 4, 5, 6)]
+    for name, env in variants:
+        for k in ("EG_NO_FUSE", "EG_MARCH_STRIPS"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, "mixed")
+        for k in env:
+            os.environ.pop(k, None)
+        s.solve(b, tol=0.0, maxit=8, out=x)
+        best = 1e30
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            s.solve(b, tol=0.0, maxit=8, out=x)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        s.profile_reset()
+        s.solve(b, tol=0.0, maxit=8, out=x, flags=egs.EG_SOLVE_PROFILE)
+        p = s.profile()
+        ks = ("phase_A", "phase_B") if p["phase_A"][1] else ("thomas_p", "stencil_dot_A")
+        kt = " ".join(f"{k} {p[k][0] / max(p[k][1], 1):.3f}" for k in ks)
+        print(f"P={P} ({prob.nx}x{prob.ny}x{prob.nz}) {name:18s}: solve(8) {best:.3f} ms, "
+              f"{best / 8 * P:.3f} ms x P per iteration; {kt}", flush=True)
+        s.close()
+        del s
+    del bands, b, x
+    torch.cuda.empty_cache()
