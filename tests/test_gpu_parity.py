@@ -18,7 +18,10 @@ egs = pytest.importorskip("paper_1811_03852_b200")
 
 RAGGED = gen.Problem(200, 37, 13, seed=8)     # nx not a multiple of the 128-column tile, odd rows
 SMALLEST = gen.Problem(3, 1, 1, seed=9)       # degenerate: one latitude row, one level
-CASES = [gen.CONFIGS["C1"], RAGGED, gen.Problem(130, 9, 70, seed=10), SMALLEST]
+# columns at and past the kernels' limits: nz = 81 (> 80, the FP64 TMEM Thomas), 129 (> 128, the
+# fp32 TMEM Thomas), 200 (the shared-memory Thomas with 32-column CTAs)
+DEEP = [gen.Problem(64, 5, 81, seed=18), gen.Problem(64, 5, 129, seed=19), gen.Problem(40, 6, 200, seed=20)]
+CASES = [gen.CONFIGS["C1"], RAGGED, gen.Problem(130, 9, 70, seed=10), SMALLEST] + DEEP
 MODES = ["fp64", "mixed", "fp32"]
 
 
@@ -70,7 +73,7 @@ FUSED_THIN = gen.Problem(192, 3, 70, seed=12)   # fewer rows than the per-CTA ro
 
 
 @pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED, gen.Problem(130, 9, 70, seed=10), FUSED_ODD,
-                                  FUSED_THIN], ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+                                  FUSED_THIN] + DEEP, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("tol", [1e-3, 1e-4])
 def test_solve_parity(prob, mode, tol):
