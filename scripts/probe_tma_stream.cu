@@ -8,8 +8,8 @@
 // the access pattern and ring depth are the limit.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_1811_03852_b200/csrc \
-//        -I../include probe_tma_stream.cu -o /tmp/probe -lcuda
-//   /tmp/probe [strips=7] [stagesF=6] [stagesS=5] [ring_kb=112]
+//        -I../include probe_tma_stream.cu -o probe_tma_stream -lcuda   (binary git-ignored)
+//   ./probe_tma_stream [strips=7] [stagesF=6] [stagesS=5] [ring_kb=112]
 #include <cuda.h>
 #include <cuda_runtime.h>
 
