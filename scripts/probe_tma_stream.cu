@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_probe(int nx, int nz, int nyl
         }
         return;
     }
-    if (warp == 9) return;
+    if (warp >= 9) return;  // (MA_THREADS also counts the phase kernels' publisher and halo warps)
     const bool isF = warp >= 4;
     const int col = tid & 127;
     int slot = 0;
