@@ -266,7 +266,15 @@ __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, con
     V* __restrict__ Fr = sp.f + rb + m;                           // colour 0 (red) half of the row
     V* __restrict__ Fb = sp.f + rb + nx / 2 + m;                  // colour 1 (black)
     const V* __restrict__ b2 = sp.b2 + 2 * (rb + m);              // red colour-split (U, D)
-    V* __restrict__ Xw = x + q0 + red;
+    // x is written as whole (red, black) pairs, the black one 0 (x = 0 before the first sweep; the
+    // black half overwrites it): full 32-byte sectors, no read-for-merge of the partial ones
+    V* __restrict__ Xw = x + q0;
+    auto st_pair = [&](int64_t o, V xr) {
+        VecN<V, 2> pr;
+        pr.v[0] = red ? 0.f : xr;
+        pr.v[1] = red ? xr : 0.f;
+        stv<2>(Xw + o, pr);
+    };
     VecN<V, 2> ca[KB], cp[KB], cv[KB], na[KB], np[KB], nv[KB];
     VecN<V, 2> cu[KB], nu[KB];
 #pragma unroll
@@ -324,10 +332,10 @@ __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, con
         for (int e = 0; e < KB; ++e) { ca[e] = na[e]; cp[e] = np[e]; cv[e] = nv[e]; cu[e] = nu[e]; }
     }
     V zn = yprev;
-    Xw[(nz - 1) * nx] = zn;
+    st_pair((int64_t)(nz - 1) * nx, zn);
     for (int k = nz - 2; k >= 0; --k) {
         zn = fmaf(-cps[k * W + tid], zn, ys[k * W + tid]);
-        Xw[k * nx] = zn;
+        st_pair((int64_t)k * nx, zn);
     }
 }
 
