@@ -154,6 +154,8 @@ struct eg_solver {
     MarchMaps maps{};
     SorMaps sor_maps[2]{};  // TMA maps of the tri-SOR sweeps writing into z / z_s
     bool sor_tma = false;   // later tri-SOR sweeps on k_sor_tma (fp32, colour-split copies)
+    SorMaps64 sor_maps64[2]{};
+    bool sor_tma64 = false; // later tri-SOR sweeps on k_sor_tma64 (FP64, colour-split copies)
     int nsm = 148;
     size_t smem_march = 0;
     int epoch_base = 1;         // first epoch of the next solve (flags are never reset)
@@ -520,6 +522,12 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
                             k_sor_tma<MODE, false><<<2 * s->nsm, SO_THREADS, so_smem, s->st>>>(
                                 s->geo, v, (float*)z, colour, s->sor_omega, KIND != 0, s->sor_maps[zi]);
                     }
+                }
+                if constexpr (MODE == 0) {
+                    tma = s->sor_tma64 && s->split && sw > 0;
+                    if (tma)
+                        k_sor_tma64<<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)z, colour, s->sor_omega,
+                                                                            KIND != 0, s->sor_maps64[zi]);
                 }
                 if (!tma) {
                     if (sw == 0)
@@ -1044,6 +1052,31 @@ bool make_sor_maps(eg_solver* s) {
     return ok;
 }
 
+bool make_sor_maps64(eg_solver* s) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn || !s->split)
+        return false;
+    EncodeTiledFn enc = (EncodeTiledFn)fn;
+    const int64_t nx = s->grid.nx, nz = s->grid.nz, nyl = s->L.nyl;
+    double* b4s = (double*)s->split;
+    double* b2s = b4s + 4 * s->L.n;
+    double* fs = b2s + 2 * s->L.n;
+    bool ok = true;
+    for (int zi = 0; zi < 2; ++zi) {
+        void* zg = s->zext[zi];  // ghosted: local row r is coordinate r + 1
+        SorMaps64& m = s->sor_maps64[zi];
+        ok = ok && encode_map_box(enc, &m.x6, zg, nx, nz, nyl + 2, 8, 256, S6_KS + 2);
+        ok = ok && encode_map_box(enc, &m.xh, zg, nx, nz, nyl + 2, 8, 4, S6_KS + 2);
+        ok = ok && encode_map_box(enc, &m.x4, zg, nx, nz, nyl + 2, 8, 256, S6_KS);
+        ok = ok && encode_map_box(enc, &m.f, fs, nx, nz, nyl, 8, 128, S6_KS);
+        ok = ok && encode_map_box(enc, &m.b4, b4s, 4 * nx, nz, nyl, 8, 256, S6_KS);
+        ok = ok && encode_map_box(enc, &m.b2, b2s, 2 * nx, nz, nyl, 8, 256, S6_KS);
+    }
+    return ok;
+}
+
 bool valid_dist(const eg_grid* g, const eg_dist* d, int64_t* jb, int64_t* je, int* rank, int* nranks) {
     if (!d) { *jb = 0; *je = g->ny; *rank = 0; *nranks = 1; return true; }
     *jb = d->j_begin; *je = d->j_end; *rank = d->rank; *nranks = d->nranks;
@@ -1306,7 +1339,10 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
                 s->use_march = false;
         }
     }
-    if (rc == EG_OK && s->split && prec != EG_FP64 && grid->nx % 4 == 0 && grid->nz <= SO_MAX_NZ8 && s->use_tm) {
+    // The TMA box of the colour-split f starts at column nx/2 for the second colour: a TMA box must
+    // start on a 16-byte boundary of its row (measured: an illegal-instruction fault otherwise), so
+    // the sweeps need nx/2 * sizeof(V) % 16 == 0, i.e. nx % 8 == 0 (fp32) / nx % 4 == 0 (FP64).
+    if (rc == EG_OK && s->split && prec != EG_FP64 && grid->nx % 8 == 0 && grid->nz <= SO_MAX_NZ8 && s->use_tm) {
         // later tri-SOR sweeps on the TMA-fed kernel (EG_NO_SOR_TMA=1 keeps k_sor_half)
         const char* ns = getenv("EG_NO_SOR_TMA");
         int dev = 0;
@@ -1327,6 +1363,15 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
             attr((const void*)k_sor_first_red<2, 2>, (int)s->smem_th);
         }
         s->sor_tma = e1 == cudaSuccess && !(ns && ns[0] == '1') && make_sor_maps(s);
+    }
+    if (rc == EG_OK && s->split && prec == EG_FP64 && grid->nx % 4 == 0 && grid->nz <= SO_MAX_NZ8) {
+        // FP64: later tri-SOR sweeps on k_sor_tma64 (EG_NO_SOR_TMA=1 keeps k_sor_half)
+        const char* ns = getenv("EG_NO_SOR_TMA");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&s->nsm, cudaDevAttrMultiProcessorCount, dev);
+        const cudaError_t e1 = cudaFuncSetAttribute(k_sor_tma64, cudaFuncAttributeMaxDynamicSharedMemorySize, S6_SMEM);
+        s->sor_tma64 = e1 == cudaSuccess && !(ns && ns[0] == '1') && make_sor_maps64(s);
     }
 #ifdef MA_VERIFY
     if (rc == EG_OK && g_vfy.n != s->L.n) {

@@ -310,7 +310,10 @@ def test_fused_phases_fall_back_outside_their_domain(prob):
     assert p["phase_A"][1] == 0 and p["thomas_p"][1] == 2
 
 
-TRISOR_CASES = [gen.Problem(64, 48, 10, seed=0), gen.Problem(130, 9, 70, seed=10), gen.Problem(128, 37, 13, seed=11)]
+# nx = 130 / 132 / 136: the second colour's colour-split rows start at byte 260 / 264 / 272 (fp32),
+# 520 / 528 / 544 (FP64); the TMA sweeps need a 16-byte boundary there and fall back otherwise
+TRISOR_CASES = [gen.Problem(64, 48, 10, seed=0), gen.Problem(130, 9, 70, seed=10), gen.Problem(128, 37, 13, seed=11),
+                gen.Problem(132, 7, 13, seed=21), gen.Problem(136, 7, 70, seed=22)]
 
 
 @pytest.mark.parametrize("prob", TRISOR_CASES, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
