@@ -524,10 +524,17 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
                     }
                 }
                 if constexpr (MODE == 0) {
-                    tma = s->sor_tma64 && s->split && sw > 0;
-                    if (tma)
-                        k_sor_tma64<<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)z, colour, s->sor_omega,
-                                                                            KIND != 0, s->sor_maps64[zi]);
+                    tma = s->sor_tma64 && s->split;
+                    if (tma) {  // FP64: the same first-sweep red kernel, then the TMA sweeps
+                        if (sw == 0 && colour == 0)
+                            k_sor_first_red<MODE, KIND><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, s->sor_omega, sp);
+                        else if (sw == 0)
+                            k_sor_tma64<true><<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)z, colour,
+                                                                                    s->sor_omega, KIND != 0, s->sor_maps64[zi]);
+                        else
+                            k_sor_tma64<false><<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)z, colour,
+                                                                                     s->sor_omega, KIND != 0, s->sor_maps64[zi]);
+                    }
                 }
                 if (!tma) {
                     if (sw == 0)
@@ -1370,7 +1377,13 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&s->nsm, cudaDevAttrMultiProcessorCount, dev);
-        const cudaError_t e1 = cudaFuncSetAttribute(k_sor_tma64, cudaFuncAttributeMaxDynamicSharedMemorySize, S6_SMEM);
+        cudaError_t e1 = cudaSuccess;
+        auto attr = [&](const void* f, int bytes) {
+            if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        };
+        attr((const void*)k_sor_tma64<true>, S6_SMEM); attr((const void*)k_sor_tma64<false>, S6_SMEM);
+        attr((const void*)k_sor_first_red<0, 0>, (int)s->smem_th); attr((const void*)k_sor_first_red<0, 1>, (int)s->smem_th);
+        attr((const void*)k_sor_first_red<0, 2>, (int)s->smem_th);
         s->sor_tma64 = e1 == cudaSuccess && !(ns && ns[0] == '1') && make_sor_maps64(s);
     }
 #ifdef MA_VERIFY

@@ -259,7 +259,9 @@ __device__ __forceinline__ double join_d(float lo, float hi) {
     return __longlong_as_double((long long)(((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo)));
 }
 
-// grid: persistent (one CTA / SM), block S6_THREADS, dynamic smem S6_SMEM.
+// grid: persistent (one CTA / SM), block S6_THREADS, dynamic smem S6_SMEM.  FIRST: the black half of
+// the first sweep after k_sor_first_red<0, KIND> (rhs = omega (f - H x); the own column is not read).
+template <bool FIRST>
 __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, double* __restrict__ x, int colour,
                                                               double omega_d, int check_halt,
                                                               const __grid_constant__ SorMaps64 maps) {
@@ -361,11 +363,16 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
                     hx = fma(e01.y, xW, hx);
                     hx = fma(e23.x, xN, hx);
                     hx = fma(e23.y, xS, hx);
-                    const V xup = k + 1 < nz ? xp : xc;  // U = 0 on the top level
-                    V tx = xc;
-                    tx = fma(ud.x, xup, tx);
-                    tx = fma(ud.y, xm, tx);  // D = 0 (and x(-1) = 0) at k = 0
-                    const V rhs = fma(om1, tx, om * (f - hx));
+                    V rhs;
+                    if (FIRST) {
+                        rhs = om * (f - hx);
+                    } else {
+                        const V xup = k + 1 < nz ? xp : xc;  // U = 0 on the top level
+                        V tx = xc;
+                        tx = fma(ud.x, xup, tx);
+                        tx = fma(ud.y, xm, tx);  // D = 0 (and x(-1) = 0) at k = 0
+                        rhs = fma(om1, tx, om * (f - hx));
+                    }
                     V c, y;
                     if (k == 0) {
                         c = ud.x;
@@ -422,9 +429,10 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
 // read once per application instead of once per colour.  Arithmetic as k_sor_half<KIND, true>.
 // grid (ceil(nx/2 / 128), nyl), block 128, dynamic smem 2 * nz * 128 * 4.
 template <int MODE, int KIND>
-__global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, const float* __restrict__ fin,
-                                                       float* __restrict__ x, double omega_d, Split<float> sp) {
-    using V = float;
+__global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, const typename Prec<MODE>::V* __restrict__ fin,
+                                                       typename Prec<MODE>::V* __restrict__ x, double omega_d,
+                                                       Split<typename Prec<MODE>::V> sp) {
+    using V = typename Prec<MODE>::V;
     constexpr int KB = 4;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int W = blockDim.x, tid = threadIdx.x;
@@ -464,8 +472,8 @@ __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, con
     V* __restrict__ Xw = x + q0;
     auto st_pair = [&](int64_t o, V xr) {
         VecN<V, 2> pr;
-        pr.v[0] = red ? 0.f : xr;
-        pr.v[1] = red ? xr : 0.f;
+        pr.v[0] = red ? (V)0 : xr;
+        pr.v[1] = red ? xr : (V)0;
         stv<2>(Xw + o, pr);
     };
     VecN<V, 2> ca[KB], cp[KB], cv[KB], na[KB], np[KB], nv[KB];
@@ -496,8 +504,8 @@ __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, con
                 VecN<V, 2> f;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    if (KIND == 1) f.v[c] = fmaf(beta, fmaf(-omega_b, cv[e].v[c], cp[e].v[c]), ca[e].v[c]);
-                    else if (KIND == 2) f.v[c] = fmaf(-alpha, cv[e].v[c], ca[e].v[c]);
+                    if (KIND == 1) f.v[c] = fma(beta, fma(-omega_b, cv[e].v[c], cp[e].v[c]), ca[e].v[c]);
+                    else if (KIND == 2) f.v[c] = fma(-alpha, cv[e].v[c], ca[e].v[c]);
                     else f.v[c] = ca[e].v[c];
                 }
                 if (KIND != 0) stv<2>(Fw + k * nx, f);
@@ -511,9 +519,9 @@ __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, con
                     c = u;
                     y = rhs;
                 } else {
-                    const V inv = rcp_fast<V>(fmaf(-d, cprev, 1.f));
+                    const V inv = rcp_fast<V>(fma(-d, cprev, (V)1));
                     c = u * inv;
-                    y = fmaf(-d, yprev, rhs) * inv;
+                    y = fma(-d, yprev, rhs) * inv;
                 }
                 cps[k * W + tid] = c;
                 ys[k * W + tid] = y;
@@ -527,7 +535,7 @@ __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, con
     V zn = yprev;
     st_pair((int64_t)(nz - 1) * nx, zn);
     for (int k = nz - 2; k >= 0; --k) {
-        zn = fmaf(-cps[k * W + tid], zn, ys[k * W + tid]);
+        zn = fma(-cps[k * W + tid], zn, ys[k * W + tid]);
         st_pair((int64_t)k * nx, zn);
     }
 }
