@@ -26,7 +26,7 @@ struct Maps { CUtensorMap r, p, v, rh, b2, b4; };
 __global__ void __launch_bounds__(MA_THREADS, 1) k_probe(int nx, int nz, int nyl, int T, int strips, int NSF,
                                                          int NSS, float* __restrict__ po, float* __restrict__ zo,
                                                          float* __restrict__ vo, const __grid_constant__ Maps maps,
-                                                         float* sink) {
+                                                         float* sink, int split) {
     constexpr int SF = ma_stage_floats(1), KS = MA_KS;
     extern __shared__ __align__(128) unsigned char smraw[];
     __shared__ __align__(8) uint64_t fullF[MA_MAX_STAGES], emptyF[MA_MAX_STAGES];
@@ -45,18 +45,23 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_probe(int nx, int nz, int nyl
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == 8) {
+    if (warp == 8 || warp == 10) {  // warp 8: both rings in a fixed interleave (split = 0), or the F ring only
+        const bool doS = warp == 8 ? !split : true, doF = warp == 8;
+        if (warp == 10 && !split) return;
         if (lane == 0) {
             int fs = 0, fr = 0, ss = 0, sr = 0;
             for (int m = 0; m < L; ++m)
                 for (int k0 = 0; k0 < NZ8; k0 += KS) {
                     const int j = ja + m;
+                    if (doS) {
                     if (sr > 0) mbar_wait_sleep(&emptyS[ss], (uint32_t)((sr - 1) & 1), 32);
                     mbar_expect_tx(&fullS[ss], MA_BOX_B4 + MA_BOX_V);
                     float* sb = stS + (size_t)ss * SF;
                     tma3(sb, &maps.b4, 2 * i0, k0, j, &fullS[ss]);
                     tma3(sb + KS * 512, &maps.rh, i0, k0, j, &fullS[ss]);
                     if (++ss == NSS) { ss = 0; ++sr; }
+                    }
+                    if (!doF) continue;
                     if (fr > 0) mbar_wait_sleep(&emptyF[fs], (uint32_t)((fr - 1) & 1), 32);
                     mbar_expect_tx(&fullF[fs], 3u * MA_BOX_V + MA_BOX_B2);
                     float* fb = stF + (size_t)fs * SF;
@@ -138,6 +143,7 @@ int main(int argc, char** argv) {
     const int NSF = argc > 2 ? atoi(argv[2]) : 6;
     const int NSS = argc > 3 ? atoi(argv[3]) : 5;
     const int ring_kb = argc > 4 ? atoi(argv[4]) : 0;  // extra smem to mimic the z ring
+    const int split = argc > 5 ? atoi(argv[5]) : 0;    // 1: one producer warp per ring
     const int64_t n = (int64_t)nx * ny * nz;
     const int T = nx / 128;
     float *r, *p, *v, *rh, *b2, *b4, *po, *zo, *vo, *sink;
@@ -162,17 +168,17 @@ int main(int argc, char** argv) {
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     for (int it = 0; it < 2; ++it)
-        k_probe<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, sink);
+        k_probe<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, sink, split);
     cudaEventRecord(a);
     const int reps = 10;
     for (int it = 0; it < reps; ++it)
-        k_probe<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, sink);
+        k_probe<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, sink, split);
     cudaEventRecord(b);
     cudaError_t e = cudaEventSynchronize(b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
     ms /= reps;
-    printf("strips=%d grid=%d stagesF=%d stagesS=%d smem=%zu KB: %.3f ms  %.0f GB/s (52 B/pt)  %s\n", strips, grid,
-           NSF, NSS, smem / 1024, ms, 52.0 * n / (ms * 1e-3) / 1e9, cudaGetErrorString(e));
+    printf("split=%d strips=%d grid=%d stagesF=%d stagesS=%d smem=%zu KB: %.3f ms  %.0f GB/s (52 B/pt)  %s\n", split, strips,
+           grid, NSF, NSS, smem / 1024, ms, 52.0 * n / (ms * 1e-3) / 1e9, cudaGetErrorString(e));
     return e == cudaSuccess ? 0 : 1;
 }
