@@ -156,9 +156,11 @@ int eg_solver_set_preconditioner(eg_solver* s, int kind, int sweeps, double omeg
  * (collective).  Stream-ordered; returns without synchronising. */
 int eg_apply_operator(eg_solver* s, const void* x, void* y);
 
-/* z = T^-1 r per column (the applied preconditioner, reading A-3): T = tridiag(D_k, 1, U_k) of the
- * scaled vertical bands, Thomas recurrence without pivoting (A-14), working precision, no
- * communication (no vertical decomposition).  Stream-ordered. */
+/* z = C^-1 r, the applied preconditioner, in the working precision.  EG_PRECOND_TRIDIAG (default):
+ * z = T^-1 r per column (reading A-3), T = tridiag(D_k, 1, U_k) of the scaled vertical bands,
+ * Thomas recurrence without pivoting (A-14), no communication (no vertical decomposition,
+ * P:263-264).  EG_PRECOND_TRISOR: the red-black tri-SOR sweeps from z = 0, which exchange halo rows
+ * after every half-sweep when distributed (collective).  Stream-ordered. */
 int eg_precondition(eg_solver* s, const void* r, void* z);
 
 /* Solve Ahat x = D_g^-1 b by right-preconditioned BiCGStab (algorithm in DESIGN.md).
@@ -189,7 +191,8 @@ int eg_solve_batch(eg_solver* s, int count, const double* const* b, double* cons
                    const double* const bands[7], const eg_solve_params* params, double* history,
                    eg_solve_info* info, int* done);
 
-/* Release the NCCL communicator, events and graphs (not the caller's workspace). NULL is a no-op. */
+/* Release the NCCL communicator (or the loopback-group membership), streams, events and graphs
+ * (not the caller's workspace).  NULL is a no-op. */
 void eg_solver_destroy(eg_solver* s);
 
 /* Human-readable detail of the last error on this handle ("" if none).  Valid until the next call. */
