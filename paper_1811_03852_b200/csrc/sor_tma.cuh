@@ -428,6 +428,9 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
 // the pair's red column.  The black half then reads f colour-split (k_sor_tma<FIRST>), so r, p, v are
 // read once per application instead of once per colour.  Arithmetic as k_sor_half<KIND, true>.
 // grid (ceil(nx/2 / 128), nyl), block 128, dynamic smem 2 * nz * 128 * 4.
+#ifndef FR_PF
+#define FR_PF 16
+#endif
 template <int MODE, int KIND>
 __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, const typename Prec<MODE>::V* __restrict__ fin,
                                                        typename Prec<MODE>::V* __restrict__ x, double omega_d,
@@ -483,10 +486,18 @@ __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, con
 #pragma unroll
         for (int c = 0; c < 2; ++c) ca[e].v[c] = cp[e].v[c] = cv[e].v[c] = na[e].v[c] = np[e].v[c] = nv[e].v[c] =
             cu[e].v[c] = nu[e].v[c] = 0.f;
+    const bool pf_lane = (tid & (32 / (2 * (int)sizeof(V)) - 1)) == 0;  // one L2 prefetch per 32-byte sector
     auto load = [&](int k0, VecN<V, 2>(&a)[KB], VecN<V, 2>(&p)[KB], VecN<V, 2>(&v)[KB], VecN<V, 2>(&u)[KB]) {
 #pragma unroll
         for (int e = 0; e < KB; ++e) {
             const int o = min(k0 + e, nz - 1) * nx;
+            if (FR_PF > 0 && pf_lane && k0 + e + FR_PF < nz) {  // FR_PF levels ahead
+                const int of = (k0 + e + FR_PF) * nx;
+                pf_l2(A0 + of);
+                if (KIND == 1) { pf_l2(Pp + of); pf_l2(Vv + of); }
+                if (KIND == 2) pf_l2(Vv + of);
+                pf_l2(b2 + 2 * of);
+            }
             a[e] = ldv<2>(A0 + o);
             if (KIND == 1) { p[e] = ldv<2>(Pp + o); v[e] = ldv<2>(Vv + o); }
             if (KIND == 2) v[e] = ldv<2>(Vv + o);
