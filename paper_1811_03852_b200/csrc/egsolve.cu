@@ -1009,7 +1009,7 @@ bool encode_map_box(EncodeTiledFn enc, CUtensorMap* m, void* base, int64_t inner
     const cuuint32_t estr[3] = {1u, 1u, 1u};
     return enc(m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides,
                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool encode_map(EncodeTiledFn enc, CUtensorMap* m, void* base, int64_t inner, int64_t nz, int64_t nyl, int esz,
