@@ -438,3 +438,22 @@ def test_solve_batch_matches_individual_solves():
     assert s.solve_batch([], [], tol=1e-6) == []
     with pytest.raises(egs.EgError):   # no EG_FEATURE_BATCH staging in the workspace
         egs.Solver(g, bd, "mixed").solve_batch(hb[:1], hx[:1], tol=1e-6)
+
+
+def test_solve_batch_stops_at_the_first_failing_solve():
+    """A degenerate right-hand side in the middle of a sequence: the earlier solves complete with
+    their usual results, the batch returns that solve's status and reports how many completed."""
+    prob = gen.Problem(64, 16, 10, seed=18)
+    bands, b0 = gen.host(prob)
+    g = (prob.nx, prob.ny, prob.nz)
+    s = egs.Solver(g, torch.from_numpy(bands).cuda(), "mixed", batch=True)
+    bs = [b0, 2.0 * b0, np.zeros(prob.n), b0]
+    xs = [np.full(prob.n, np.nan) for _ in bs]
+    with pytest.raises(egs.EgError) as e:
+        s.solve_batch(bs, xs, tol=1e-6, maxit=50)
+    assert e.value.status == 3
+    infos = s.solve_batch(bs, xs, tol=1e-6, maxit=50, raise_on_error=False)
+    assert len(infos) == 2 and all(i.converged and i.status == 0 for i in infos)
+    x0, _, _ = s.solve(torch.from_numpy(b0).cuda(), tol=1e-6, maxit=50)
+    assert np.array_equal(xs[0], x0.cpu().numpy()) and np.array_equal(xs[1], 2.0 * xs[0])
+    assert np.isnan(xs[3]).all()  # never started
