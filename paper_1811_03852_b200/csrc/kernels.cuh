@@ -170,11 +170,14 @@ __global__ void __launch_bounds__(256) k_scale(Geo g, Bands7 in, V* __restrict__
 // partials: q0 = ||bhat||^2 (ENTRY), q1 = ||res||^2 (fp64, true residual), q2 = r . r (S).
 // XZERO: x = 0 (written at ENTRY), res = bhat, no operator application.  WRITE = false: verification
 // only (true residual norm, r / rhat0 untouched).  grid (tiles, nyl), RW.
+#ifndef ST_KB
+#define ST_KB 2
+#endif
 template <int MODE, bool ENTRY, bool XZERO, bool WRITE = true>
 __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double* __restrict__ b) {
     using V = typename Prec<MODE>::V;
     using X = typename Prec<MODE>::X;
-    constexpr int KB = XZERO ? 8 : 2;
+    constexpr int KB = XZERO ? 8 : ST_KB;
     double acc[3] = {0.0, 0.0, 0.0};
     const int i = blockIdx.x * RW + threadIdx.x;
     const int64_t jl = blockIdx.y, jg = g.j0 + jl;
@@ -196,14 +199,20 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
         X* __restrict__ xo = vv.x + rb + i;
         V* __restrict__ ro = vv.r + rb + i;
         V* __restrict__ rho = vv.rh + rb + i;
-        constexpr int NA = XZERO ? 2 : 13;
-        double cur[KB][NA], nxt[KB][NA];
+        // per level: fp64 values (bhat, diag, x, xE, xW, xN, xS) and the six bands kept in the
+        // working precision (promoted when used): fewer registers per buffered level
+        constexpr int ND = XZERO ? 2 : 7, NB = XZERO ? 1 : 6;
+        double cd[KB][ND], nd[KB][ND];
+        V cbd[KB][NB], nbd[KB][NB];
 #pragma unroll
-        for (int e = 0; e < KB; ++e)
+        for (int e = 0; e < KB; ++e) {
 #pragma unroll
-            for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a] = 0.0;
+            for (int a = 0; a < ND; ++a) cd[e][a] = nd[e][a] = 0.0;
+#pragma unroll
+            for (int a = 0; a < NB; ++a) cbd[e][a] = nbd[e][a] = (V)0;
+        }
         double xup_c = 0, xup_n = 0;
-        auto load = [&](int k0, double(&c)[KB][NA], double& xup) {
+        auto load = [&](int k0, double(&c)[KB][ND], V(&cb)[KB][NB], double& xup) {
 #pragma unroll
             for (int e = 0; e < KB; ++e) {
                 const int k = k0 + e;
@@ -214,28 +223,27 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
                     if (!XZERO) {
                         const VecN<V, 4> h4 = ldv<4>(b4 + 4 * o);
                         const VecN<V, 2> h2 = ldv<2>(b2 + 2 * o);
-                        c[e][2] = (double)h4.v[0]; c[e][3] = (double)h4.v[1];
-                        c[e][4] = (double)h4.v[2]; c[e][5] = (double)h4.v[3];
-                        c[e][6] = (double)h2.v[0]; c[e][7] = (double)h2.v[1];
-                        c[e][8] = (double)xc[o]; c[e][9] = (double)xE[o]; c[e][10] = (double)xW[o];
-                        c[e][11] = (double)xN[o]; c[e][12] = (double)xS[o];
+                        cb[e][0] = h4.v[0]; cb[e][1] = h4.v[1]; cb[e][2] = h4.v[2]; cb[e][3] = h4.v[3];
+                        cb[e][4] = h2.v[0]; cb[e][5] = h2.v[1];
+                        c[e][2] = (double)xc[o]; c[e][3] = (double)xE[o]; c[e][4] = (double)xW[o];
+                        c[e][5] = (double)xN[o]; c[e][6] = (double)xS[o];
                     }
                 }
             }
             if (!XZERO) xup = (k0 + KB < nz) ? (double)xc[(k0 + KB) * nx] : 0.0;
         };
-        load(0, cur, xup_c);
+        load(0, cd, cbd, xup_c);
         double xprev = 0.0;
         for (int k0 = 0; k0 < nz; k0 += KB) {
-            if (k0 + KB < nz) load(k0 + KB, nxt, xup_n);
+            if (k0 + KB < nz) load(k0 + KB, nd, nbd, xup_n);
 #pragma unroll
             for (int e = 0; e < KB; ++e) {
                 const int k = k0 + e;
                 if (k < nz) {
                     const int o = k * nx;
-                    double bh = cur[e][0];
+                    double bh = cd[e][0];
                     if (ENTRY) {
-                        bh = bh / cur[e][1];
+                        bh = bh / cd[e][1];
                         bh_out[o] = bh;
                         if (MODE == 2) {
                             const double b32 = (double)(float)bh;
@@ -248,15 +256,15 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
                     if (XZERO) {
                         res = bh;  // x = 0 is not stored: DevState.xzero (the first update starts from 0)
                     } else {
-                        const double xm = e == 0 ? xprev : cur[e - 1][8];
-                        const double xp = e + 1 < KB ? (k + 1 < nz ? cur[e + 1][8] : 0.0) : xup_c;
-                        double ax = cur[e][8];
-                        ax += cur[e][2] * cur[e][9];
-                        ax += cur[e][3] * cur[e][10];
-                        ax += cur[e][4] * cur[e][11];
-                        ax += cur[e][5] * cur[e][12];
-                        ax += cur[e][6] * xp;
-                        ax += cur[e][7] * xm;
+                        const double xm = e == 0 ? xprev : cd[e - 1][2];
+                        const double xp = e + 1 < KB ? (k + 1 < nz ? cd[e + 1][2] : 0.0) : xup_c;
+                        double ax = cd[e][2];
+                        ax += (double)cbd[e][0] * cd[e][3];
+                        ax += (double)cbd[e][1] * cd[e][4];
+                        ax += (double)cbd[e][2] * cd[e][5];
+                        ax += (double)cbd[e][3] * cd[e][6];
+                        ax += (double)cbd[e][4] * xp;
+                        ax += (double)cbd[e][5] * xm;
                         res = bh - ax;
                     }
                     acc[1] += res * res;
@@ -268,11 +276,14 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
                     }
                 }
             }
-            if (!XZERO) xprev = cur[KB - 1][8];
+            if (!XZERO) xprev = cd[KB - 1][2];
 #pragma unroll
-            for (int e = 0; e < KB; ++e)
+            for (int e = 0; e < KB; ++e) {
 #pragma unroll
-                for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a];
+                for (int a = 0; a < ND; ++a) cd[e][a] = nd[e][a];
+#pragma unroll
+                for (int a = 0; a < NB; ++a) cbd[e][a] = nbd[e][a];
+            }
             xup_c = xup_n;
         }
     }
