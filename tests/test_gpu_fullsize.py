@@ -4,6 +4,10 @@ launch configuration bench.py times (the default solver, CUDA-graph replay, gene
 * apply / precondition: sampled latitude rows (poles, seam rows, interior) against the oracle run
   on a 3-row sub-grid around each sampled row (the sub-grid's artificial edges are decoupled; rows
   outside the sample are never compared).
+* tri-SOR precondition (NEXT-1, 3 sweeps, omega 1.5, on the TMA sweep kernels): sampled rows
+  against the oracle's sweeps on a window of rows around each; information travels one row per
+  half-sweep, so a row at least 7 rows inside the window is exact (the window's decoupled edges
+  cannot reach it in 6 half-sweeps); windows start on an even row (the colouring's parity).
 * solve (MIXED, tol 1e-4): the full CPU oracle solve of the same inputs (about 70 GB of host RAM
   and a minute on the GPU box's cores) — iterations within 2, ||dx||/||x|| <= 10 tol, and the GPU's
   x has oracle-recomputed true residual < tol.
@@ -64,6 +68,34 @@ def test_c5_apply_and_precondition_sampled_rows(c5):
         zo = oracle.thomas((prob.nx, j1 - j0, prob.nz), "fp64", ahat, xs)[(j - j0) * row:(j - j0 + 1) * row]
         zg = z[j * row:(j + 1) * row].double().cpu().numpy()
         assert np.linalg.norm(zg - zo) <= 1e-5 * np.linalg.norm(zo), j
+
+
+def test_c5_trisor_precondition_sampled_rows(c5):
+    prob, bands, b, _ = c5
+    row = prob.nx * prob.nz
+    st = egs.Solver((prob.nx, prob.ny, prob.nz), bands, "mixed", trisor=True)
+    st.set_preconditioner("trisor", sweeps=3, omega=1.5)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(prob.n, generator=g, device="cuda", dtype=torch.float32)
+    z = st.precondition(x)
+    torch.cuda.synchronize()
+    W = 8
+    for j in (0, 3, 960, 1919):
+        j0 = max(0, j - W)
+        j0 -= j0 % 2                      # same colouring parity as the full grid
+        j1 = min(prob.ny, j + W + 1)
+        hb, _ = gen.host(prob, j0, j1)
+        if j0 > 0:
+            hb[4, :row] = 0.0             # decouple the window's artificial edges
+        if j1 < prob.ny:
+            hb[3, -row:] = 0.0
+        gw = (prob.nx, j1 - j0, prob.nz)
+        ahat, _ = oracle.scale(gw, hb, "mixed")
+        xs = x[j0 * row:j1 * row].double().cpu().numpy()
+        zo = oracle.trisor(gw, "fp64", ahat, xs, sweeps=3, omega=1.5)[(j - j0) * row:(j - j0 + 1) * row]
+        zg = z[j * row:(j + 1) * row].double().cpu().numpy()
+        assert np.linalg.norm(zg - zo) <= 1e-5 * np.linalg.norm(zo), j
+    st.close()
 
 
 def test_c5_solve_matches_full_oracle(c5):
