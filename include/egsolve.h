@@ -30,8 +30,10 @@
  * THREADING.  One handle is not thread-safe; separate handles are independent.  All device work
  * is ordered on the stream given to eg_solver_create.  The fused phase kernels keep
  * one CTA per SM and synchronise CTAs through ready flags, which needs every CTA of a launch
- * resident: do not run two handles' solves concurrently on different streams of the same GPU
- * (serialise them, or create the handles with EG_NO_FUSE=1 in the environment).
+ * resident, so concurrent eg_solve / eg_solve_batch calls of handles that use them are serialised
+ * inside this process (a process-wide lock; the calls block until their kernels finish anyway).
+ * Other processes sharing the GPU are time-sliced, not co-resident, unless MPS is used: with MPS,
+ * serialise the solves yourself or create the handles with EG_NO_FUSE=1 in the environment.
  */
 #ifndef EGSOLVE_H
 #define EGSOLVE_H

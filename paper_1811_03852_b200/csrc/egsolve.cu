@@ -108,6 +108,13 @@ struct LoopGroup {
 };
 constexpr char kLoopMagic[8] = {'E', 'G', 'L', 'O', 'O', 'P', 'B', 'K'};
 
+// The fused phase kernels need every CTA of a launch resident (their CTAs wait on each other's
+// ready flags).  Two of them launched concurrently from different streams of this process could
+// each end up partly resident and wait forever, so solves that use them are serialised here
+// (eg_solve is blocking: every kernel of a solve has finished when the lock is released).
+// Loopback ranks share one stream already and meet at host barriers inside a solve: not locked.
+std::recursive_mutex g_fused_solve_mu;
+
 // all n ranks arrive or the wait times out (a rank that failed never comes): false = broken group
 bool lb_barrier(LoopGroup* G) {
     std::unique_lock<std::mutex> lk(G->m);
@@ -1452,6 +1459,8 @@ int eg_solve(eg_solver* s, const double* b, const double* x0, const eg_solve_par
              double* history, eg_solve_info* info) {
     if (!s || !b || !x || !params || params->maxit < 0 || !(params->tol >= 0.0))
         return s ? fail(s, EG_ERR_ARG, "bad solve arguments") : EG_ERR_ARG;
+    std::unique_lock<std::recursive_mutex> lk(g_fused_solve_mu, std::defer_lock);
+    if (s->use_march && !s->lb) lk.lock();
     int rc = s->mode == EG_FP64 ? solve_impl<0>(s, b, x0, params, x, history, info)
            : s->mode == EG_MIXED ? solve_impl<1>(s, b, x0, params, x, history, info)
                                  : solve_impl<2>(s, b, x0, params, x, history, info);
@@ -1468,6 +1477,8 @@ int eg_solve_batch(eg_solver* s, int count, const double* const* b, double* cons
     for (int k = 0; k < count; ++k)
         if (!b[k] || !x[k]) return fail(s, EG_ERR_ARG, "NULL b / x in the batch");
     if (!s->batch) return fail(s, EG_ERR_WORKSPACE, "eg_solve_batch needs an EG_FEATURE_BATCH workspace");
+    std::unique_lock<std::recursive_mutex> lk(g_fused_solve_mu, std::defer_lock);  // see g_fused_solve_mu
+    if (s->use_march && !s->lb) lk.lock();
     if (!s->cin) {
         CK(cudaStreamCreateWithFlags(&s->cin, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&s->cout, cudaStreamNonBlocking));

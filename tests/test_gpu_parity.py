@@ -457,3 +457,38 @@ def test_solve_batch_stops_at_the_first_failing_solve():
     x0, _, _ = s.solve(torch.from_numpy(b0).cuda(), tol=1e-6, maxit=50)
     assert np.array_equal(xs[0], x0.cpu().numpy()) and np.array_equal(xs[1], 2.0 * xs[0])
     assert np.isnan(xs[3]).all()  # never started
+
+
+def test_concurrent_fused_solves_on_two_streams(monkeypatch):
+    """Two handles solving at the same time from two threads, each on its own stream, with the fused
+    phase kernels (which need all their CTAs resident): the library serialises such solves, so both
+    finish and give bitwise the results of the same solves run one after the other."""
+    import threading
+    monkeypatch.setenv("EG_FUSE", "1")
+    probs = [gen.Problem(192, 144, 70, seed=1), gen.Problem(256, 96, 70, seed=2)]
+    sts = [torch.cuda.Stream() for _ in probs]
+    solvers, rhs = [], []
+    for p, st in zip(probs, sts):
+        bands, b = gen.host(p)
+        solvers.append(egs.Solver((p.nx, p.ny, p.nz), torch.from_numpy(bands).cuda(), "mixed", stream=st))
+        rhs.append(torch.from_numpy(b).cuda())
+    torch.cuda.synchronize()
+    seq = [s.solve(b, tol=0.0, maxit=12)[0].clone() for s, b in zip(solvers, rhs)]
+    outs = [torch.empty_like(x) for x in seq]
+    errs = []
+
+    def run(k):
+        try:
+            for _ in range(5):
+                solvers[k].solve(rhs[k], tol=0.0, maxit=12, out=outs[k])
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+    assert not any(t.is_alive() for t in ts) and not errs
+    torch.cuda.synchronize()
+    assert all(torch.equal(o, x) for o, x in zip(outs, seq))
