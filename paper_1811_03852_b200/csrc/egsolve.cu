@@ -744,7 +744,7 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     int rc = EG_OK;
     s->profiling = (prm->flags & EG_SOLVE_PROFILE) != 0;
     // (loopback ranks meet at host barriers inside every exchange: launched directly, never replayed)
-    const bool use_graph = !(prm->flags & (EG_SOLVE_NO_GRAPH | EG_SOLVE_PROFILE)) && s->lb == nullptr;
+    bool use_graph = !(prm->flags & (EG_SOLVE_NO_GRAPH | EG_SOLVE_PROFILE)) && s->lb == nullptr;
     eg_solve_info inf{};
 
     // ---- inputs: b (host -> staged into bhat, scaled in place), x iterate ----
@@ -819,12 +819,17 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
         cudaError_t ce = cb == cudaSuccess ? cudaStreamEndCapture(s->st, &tmp) : cb;
         gph = tmp;
         s->st = user;
-        if (irc) return irc;
-        CK(ce);
-        CK(cudaGraphInstantiate(&s->graphs[gi], gph, 0));
-        cudaGraphDestroy(gph);
-        s->graphs_x[gi] = x_it;
-        s->graph = s->graphs[gi];
+        cudaError_t ie = cudaErrorUnknown;
+        if (cb == cudaSuccess && irc == EG_OK && ce == cudaSuccess && gph) ie = cudaGraphInstantiate(&s->graphs[gi], gph, 0);
+        if (gph) cudaGraphDestroy(gph);
+        if (ie == cudaSuccess) {
+            s->graphs_x[gi] = x_it;
+            s->graph = s->graphs[gi];
+        } else {  // the graph is an optimisation only: launch the iteration's kernels directly
+            cudaGetLastError();
+            s->graphs[gi] = nullptr;
+            use_graph = false;
+        }
     }
 
     while (rc == EG_OK) {
