@@ -76,7 +76,8 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t fe
     L->off_state = o; o = align_up(o + sizeof(DevState), A);
     L->base_total = o;
     // EG_FEATURE_TRISOR: colour-split (E,W,N,S), (U,D) and f for the red-black tri-SOR sweeps
-    L->off_split = o; if (features & EG_FEATURE_TRISOR) o = align_up(o + 7 * n * L->vsz, A);
+    // and the colour-split x of the fp32 TMA sweeps (ghosted rows: n + 2 rows)
+    L->off_split = o; if (features & EG_FEATURE_TRISOR) o = align_up(o + (8 * n + 2 * row) * L->vsz, A);
     L->off_batch = o; if (features & EG_FEATURE_BATCH) o = align_up(o + 4 * n * 8, A);
     L->total = o;
     return true;
@@ -159,7 +160,7 @@ struct eg_solver {
     bool use_march = false;     // fused phases (fp32 working precision; march.cuh)
     MarchGeo mg{};
     MarchMaps maps{};
-    SorMaps sor_maps[2]{};  // TMA maps of the tri-SOR sweeps writing into z / z_s
+    SorMaps sor_maps{};     // TMA maps of the fp32 tri-SOR sweeps (colour-split arrays)
     bool sor_tma = false;   // later tri-SOR sweeps on k_sor_tma (fp32, colour-split copies)
     SorMaps64 sor_maps64[2]{};
     bool sor_tma64 = false; // later tri-SOR sweeps on k_sor_tma64 (FP64, colour-split copies)
@@ -510,31 +511,38 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
         sp = Split<V>{b4s, b2s, b2s + 2 * s->L.n};
     }
     const int zi = (void*)z == (void*)v.zs ? 1 : 0;
+    // the colour-split x of the fp32 TMA sweeps: ghosted, after f in the split region; row 0 pointer
+    float* xsr = s->split ? (float*)((V*)s->split + 7 * s->L.n) + s->L.row : nullptr;
+    (void)xsr;
     for (int sw = 0; sw < s->sor_sweeps; ++sw)
         for (int colour = 0; colour < 2; ++colour) {
+            bool xs_half = false;  // this half-sweep wrote the colour-split x (else the natural z)
             {
                 ProfScope ps(s, KID_SOR, sor_alg_bytes(s, KIND, sw, colour));
                 bool tma = false;
                 if constexpr (MODE != 0) {
                     tma = s->sor_tma && s->split;
-                    if (tma) {  // fp32 with colour-split copies: the first-sweep red kernel + TMA sweeps
+                    if (tma) {  // fp32 with colour-split copies: x colour-split until the last half-sweep
                         const int so_smem = SO_STAGES * SO_STAGE_FLOATS * 4 + 128;
+                        const int fin_ = sw == s->sor_sweeps - 1 && colour == 1;
                         if (sw == 0 && colour == 0)  // red half + f of both colours
                             k_sor_first_red<MODE, KIND><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, (const float*)fin,
-                                                                                         (float*)z, s->sor_omega, sp);
+                                                                                         (float*)z, s->sor_omega, sp, xsr);
                         else if (sw == 0)
                             k_sor_tma<MODE, true><<<2 * s->nsm, SO_THREADS, so_smem, s->st>>>(
-                                s->geo, v, (float*)z, colour, s->sor_omega, KIND != 0, s->sor_maps[zi]);
+                                s->geo, v, xsr, (float*)z, colour, fin_, s->sor_omega, KIND != 0, s->sor_maps);
                         else
                             k_sor_tma<MODE, false><<<2 * s->nsm, SO_THREADS, so_smem, s->st>>>(
-                                s->geo, v, (float*)z, colour, s->sor_omega, KIND != 0, s->sor_maps[zi]);
+                                s->geo, v, xsr, (float*)z, colour, fin_, s->sor_omega, KIND != 0, s->sor_maps);
+                        xs_half = !fin_;
                     }
                 }
                 if constexpr (MODE == 0) {
                     tma = s->sor_tma64 && s->split;
                     if (tma) {  // FP64: the same first-sweep red kernel, then the TMA sweeps
                         if (sw == 0 && colour == 0)
-                            k_sor_first_red<MODE, KIND><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, s->sor_omega, sp);
+                            k_sor_first_red<MODE, KIND><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, s->sor_omega, sp,
+                                                                                         nullptr);
                         else if (sw == 0)
                             k_sor_tma64<true><<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)z, colour,
                                                                                     s->sor_omega, KIND != 0, s->sor_maps64[zi]);
@@ -553,7 +561,7 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
                 }
                 CK(cudaGetLastError());
             }
-            if ((rc = halo_ghosted(s, z))) return rc;
+            if ((rc = halo_ghosted(s, xs_half ? (void*)xsr : (void*)z))) return rc;
         }
     return EG_OK;
 }
@@ -1057,17 +1065,14 @@ bool make_sor_maps(eg_solver* s) {
     float* b4s = (float*)s->split;
     float* b2s = b4s + 4 * s->L.n;
     float* fs = b2s + 2 * s->L.n;
-    bool ok = true;
-    for (int zi = 0; zi < 2; ++zi) {
-        void* zg = s->zext[zi];  // the ghosted array from its row -1: x rows are addressed as jl + 1
-        SorMaps& m = s->sor_maps[zi];
-        ok = ok && encode_map_box(enc, &m.x6, zg, nx, nz, nyl + 2, 4, 256, SO_KS + 2);
-        ok = ok && encode_map_box(enc, &m.xh, zg, nx, nz, nyl + 2, 4, 4, SO_KS + 2);
-        ok = ok && encode_map_box(enc, &m.x4, zg, nx, nz, nyl + 2, 4, 256, SO_KS);
-        ok = ok && encode_map_box(enc, &m.f, fs, nx, nz, nyl, 4, 128, SO_KS);
-        ok = ok && encode_map_box(enc, &m.b4, b4s, 2 * nx, nz, nyl, 8, 256, SO_KS);
-        ok = ok && encode_map_box(enc, &m.b2, b2s, nx, nz, nyl, 8, 128, SO_KS);
-    }
+    float* xs = fs + s->L.n;  // the colour-split x from its row -1: rows are addressed as jl + 1
+    SorMaps& m = s->sor_maps;
+    bool ok = encode_map_box(enc, &m.xo6, xs, nx, nz, nyl + 2, 4, 128, SO_KS + 2);
+    ok = ok && encode_map_box(enc, &m.x4, xs, nx, nz, nyl + 2, 4, 128, SO_KS);
+    ok = ok && encode_map_box(enc, &m.xh, xs, nx, nz, nyl + 2, 4, 4, SO_KS);
+    ok = ok && encode_map_box(enc, &m.f, fs, nx, nz, nyl, 4, 128, SO_KS);
+    ok = ok && encode_map_box(enc, &m.b4, b4s, 2 * nx, nz, nyl, 8, 256, SO_KS);
+    ok = ok && encode_map_box(enc, &m.b2, b2s, nx, nz, nyl, 8, 128, SO_KS);
     return ok;
 }
 
@@ -1120,10 +1125,12 @@ bool valid_grid(const eg_grid* g) {
 // copies change how much of each loaded sector is used, not what the sweep needs.
 double sor_alg_bytes(const eg_solver* s, int kind, int sweep, int colour) {
     const double V = (double)s->L.vsz, n = (double)s->L.n;
-    if (sweep > 0) return 5 * V * n;                                   // f, 6 bands / 2; x; x / 2
+    // the fp32 TMA sweeps' last half writes z in natural order, both colours (+ V / 2)
+    const double fin_z = (s->sor_tma && s->split && sweep == s->sor_sweeps - 1 && colour == 1) ? 0.5 * V * n : 0.0;
+    if (sweep > 0) return 5 * V * n + fin_z;                           // f, 6 bands / 2; x; x / 2
     const double fin = kind == 0 ? 0.5 : (kind == 1 ? 1.5 : 1.0);     // fin | r, p, v | r, v (one colour)
     const double out = 0.5 + (kind != 0 ? 0.5 : 0.0) + (s->split ? 0.5 : 0.0);  // x, p / s, f split
-    return (fin + (colour == 0 ? 1.0 : 3.0 + 0.5) + out) * V * n;      // red: (U,D) only; black: + (E,W,N,S), red x
+    return (fin + (colour == 0 ? 1.0 : 3.0 + 0.5) + out) * V * n + fin_z;  // red: (U,D) only; black: + (E,W,N,S), red x
 }
 
 // algorithmic HBM bytes of one launch, V = vector / band bytes, X = x bytes

@@ -6,15 +6,18 @@
 // the same x).  Every value a half-sweep reads from x has the other colour or is the updated
 // column's own old value, so CTAs never depend on one another.
 //
-// This kernel serves the sweeps after the first (f = the colour-split right-hand side written by the
-// first sweep).  Work item = (latitude row, 256-column tile): the 128 columns of the sweep's colour,
-// one per consumer thread.  A producer warp streams, per 4-level stage, with 3-D TMA boxes:
-//   x of the row (levels k0-1 .. k0+4, the 256 columns and one 4-wide halo box on each side),
-//   x of the rows j-1 and j+1 (levels k0 .. k0+3), and the colour-split f, (E,W,N,S), (U,D),
-// so every loaded sector is used (the natural-order rows hold the updated column's old value and its
-// E / W neighbours; the N / S rows are shared with the neighbouring rows' items through L2).
-// The Thomas factors c' and y live in TMEM (thread = lane); x_new is written in natural order.
-// Persistent grid (2 CTAs / SM); stage release is ordered before the TMA refill by
+// This kernel serves every half-sweep after the first sweep's red half.  x lives COLOUR-SPLIT
+// during the sweeps (xs: per row and level, the nx/2 columns of colour 0 then those of colour 1;
+// ghosted rows -1 / nyl), like f and the bands, so every array an item touches is contiguous for
+// its 128 columns: the own colour's old x (levels k0-1 .. k0+4), the other colour's x in the row
+// (E / W neighbours, with a 4-wide box on each side for the tile's edge columns and the periodic
+// wrap) and in the rows j-1 / j+1 (N / S), f, (E,W,N,S), (U,D).  An item writes only its own
+// colour's 128 values per level (no half-written natural sectors).  The last half-sweep of an
+// application (FINAL) writes z in natural order instead: both colours as (red, black) pairs, the
+// other colour's values kept in TMEM from the forward pass.
+// Work item = (latitude row, 128 columns of one colour), one column per consumer thread; a producer
+// warp streams 4-level stages with 3-D TMA boxes.  c', y (and for FINAL the other colour) live in
+// TMEM.  Persistent grid (2 CTAs / SM); stage release is ordered before the TMA refill by
 // fence.proxy.async (see march.cuh).
 #pragma once
 #include "march.cuh"
@@ -26,32 +29,34 @@ constexpr int SO_CONS = 128;              // consumer threads (columns of one co
 constexpr int SO_THREADS = SO_CONS + 32;  // + the producer warp
 constexpr int SO_TILE = 256;              // natural columns per item
 // stage layout (floats; every TMA destination 128-byte aligned)
-constexpr int SO_XJ = 0;                              // [KS+2][256]
-constexpr int SO_XHW = SO_XJ + (SO_KS + 2) * 256;      // [KS+2][4]
-constexpr int SO_XHE = SO_XHW + 32;                    // [KS+2][4]
-constexpr int SO_XN = SO_XHE + 32;                     // [KS][256]
-constexpr int SO_XS = SO_XN + SO_KS * 256;             // [KS][256]
-constexpr int SO_F = SO_XS + SO_KS * 256;              // [KS][128]
+constexpr int SO_XO = 0;                               // own colour [KS+2][128], levels k0-1 ..
+constexpr int SO_XT = SO_XO + (SO_KS + 2) * 128;       // other colour, row j [KS][128]
+constexpr int SO_XHW = SO_XT + SO_KS * 128;            // other colour, 4 columns W of the tile [KS][4]
+constexpr int SO_XHE = SO_XHW + 32;                    // other colour, 4 columns E of the tile [KS][4]
+constexpr int SO_XN = SO_XHE + 32;                     // other colour, row j+1 [KS][128]
+constexpr int SO_XS = SO_XN + SO_KS * 128;             // other colour, row j-1 [KS][128]
+constexpr int SO_F = SO_XS + SO_KS * 128;              // [KS][128]
 constexpr int SO_B4 = SO_F + SO_KS * 128;              // [KS][512]
 constexpr int SO_B2 = SO_B4 + SO_KS * 512;             // [KS][256]
 constexpr int SO_STAGE_FLOATS = SO_B2 + SO_KS * 256;
-constexpr int SO_STAGES = 3;
+constexpr int SO_STAGES = 4;
 constexpr int SO_MAX_NZ8 = 72;
-constexpr uint32_t SO_BOX_XJ = (SO_KS + 2) * 256 * 4, SO_BOX_XH = (SO_KS + 2) * 4 * 4, SO_BOX_XR = SO_KS * 256 * 4;
+constexpr uint32_t SO_BOX_XO = (SO_KS + 2) * 128 * 4, SO_BOX_XR = SO_KS * 128 * 4, SO_BOX_XH = SO_KS * 4 * 4;
 constexpr uint32_t SO_BOX_F = SO_KS * 128 * 4, SO_BOX_B4 = SO_KS * 512 * 4, SO_BOX_B2 = SO_KS * 256 * 4;
 
-// tensor maps: x natural with (256, KS+2), (4, KS+2) and (256, KS) boxes; f split (128, KS);
-// (E,W,N,S) split as u64 (256, KS); (U,D) split as u64 (128, KS)
+// tensor maps: xs (ghosted, colour-split) with (128, KS+2), (128, KS) and (4, KS) boxes; f split
+// (128, KS); (E,W,N,S) split as u64 (256, KS); (U,D) split as u64 (128, KS)
 struct SorMaps {
-    CUtensorMap x6, xh, x4, f, b4, b2;
+    CUtensorMap xo6, x4, xh, f, b4, b2;
 };
 
 // grid: persistent (2 CTAs / SM), block SO_THREADS, dynamic smem SO_STAGES * SO_STAGE_FLOATS * 4 + 128.
-// x: the ghosted array's row 0 (updated in place, own colour only).
-// FIRST: the black half of the first sweep (x_old = 0: rhs = omega (f - H x), the red neighbours
-// just written by k_sor_first_red, which also wrote the black columns' f colour-split).
+// xs: the colour-split ghosted x's row 0 (own colour updated in place unless FINAL); z: the natural
+// output's row 0 (written when FINAL).  FIRST: the black half of the first sweep (x_old = 0:
+// rhs = omega (f - H x); the red neighbours and f were written by k_sor_first_red).
 template <int MODE, bool FIRST>
-__global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv, float* __restrict__ x, int colour,
+__global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv, float* __restrict__ xs,
+                                                            float* __restrict__ z, int colour, int final_,
                                                             double omega_d, int check_halt,
                                                             const __grid_constant__ SorMaps maps) {
     static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
@@ -63,15 +68,17 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
     const V om = (V)omega_d, om1 = (V)(1.0 - omega_d);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nx = (int)g.nx, nz = (int)g.nz, nyl = (int)g.nyl;
-    const int tiles = (nx + SO_TILE - 1) / SO_TILE;
+    const int nh = nx / 2;                          // columns per colour
+    const int tiles = (nh + SO_CONS - 1) / SO_CONS;
     const int64_t items = (int64_t)tiles * nyl;
     const int NZ8 = (nz + 7) / 8 * 8;  // levels padded to whole 8-level TMEM chunks
+    const int oc = colour ^ 1;          // the other colour
     float* stages = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
     if (tid == 0) {
-        for (int s = 0; s < SO_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], SO_CONS); }
+        for (int q = 0; q < SO_STAGES; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], SO_CONS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // 256 TMEM columns: c' [0, 72), y [72, 144)
+    // 256 TMEM columns: c' [0, 72), y [72, 144), the other colour (FINAL) [144, 216)
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&tm_slot))
                      : "memory");
@@ -89,26 +96,28 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
             for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
                 const int jl = (int)(it / tiles), t = (int)(it % tiles);
                 const int64_t jg = g.j0 + jl;
-                const int i0 = t * SO_TILE;
-                const int w = min(SO_TILE, nx - i0);
-                const int iWb = (i0 == 0 ? nx - 1 : i0 - 1) - 3;  // W halo box: its last element
-                const int iEb = (i0 + w == nx) ? 0 : i0 + w;      // E halo box: its first element
-                const int cs = colour * (nx / 2) + t * (SO_TILE / 2);  // colour-split column of the tile
+                const int m0 = t * SO_CONS;
+                const int w = min(SO_CONS, nh - m0);
+                const int cs = colour * nh + m0, co = oc * nh + m0;  // split columns of the tile
+                const int hW = oc * nh + (m0 == 0 ? nh : m0) - 4;      // box ending at the W neighbour
+                const int hE = oc * nh + (m0 + w == nh ? 0 : m0 + w);  // box starting at the E neighbour
                 const bool hasN = jg < g.ny - 1, hasS = jg > 0;
-                for (int st = 0; st < nstage; ++st) {
-                    const int k0 = st * SO_KS;
+                for (int q = 0; q < nstage; ++q) {
+                    const int k0 = q * SO_KS;
                     if (round > 0) mbar_wait_sleep(&empty[slot], (uint32_t)((round - 1) & 1), 32);
                     uint64_t* fb = &full[slot];
-                    const uint32_t bytes = SO_BOX_XJ + 2 * SO_BOX_XH + (hasN ? SO_BOX_XR : 0u) +
-                                           (hasS ? SO_BOX_XR : 0u) + SO_BOX_F + SO_BOX_B4 + SO_BOX_B2;
+                    const uint32_t bytes = (FIRST ? 0u : SO_BOX_XO) + SO_BOX_XR + 2 * SO_BOX_XH +
+                                           (hasN ? SO_BOX_XR : 0u) + (hasS ? SO_BOX_XR : 0u) + SO_BOX_F +
+                                           SO_BOX_B4 + SO_BOX_B2;
                     mbar_expect_tx(fb, bytes);
                     float* sb = stages + (size_t)slot * SO_STAGE_FLOATS;
-                    // x maps span the ghosted rows -1 .. nyl: local row r is coordinate r + 1
-                    tma3(sb + SO_XJ, &maps.x6, i0, k0 - 1, jl + 1, fb);
-                    tma3(sb + SO_XHW, &maps.xh, iWb, k0 - 1, jl + 1, fb);
-                    tma3(sb + SO_XHE, &maps.xh, iEb, k0 - 1, jl + 1, fb);
-                    if (hasN) tma3(sb + SO_XN, &maps.x4, i0, k0, jl + 2, fb);
-                    if (hasS) tma3(sb + SO_XS, &maps.x4, i0, k0, jl, fb);
+                    // xs maps span the ghosted rows -1 .. nyl: local row r is coordinate r + 1
+                    if (!FIRST) tma3(sb + SO_XO, &maps.xo6, cs, k0 - 1, jl + 1, fb);
+                    tma3(sb + SO_XT, &maps.x4, co, k0, jl + 1, fb);
+                    tma3(sb + SO_XHW, &maps.xh, hW, k0, jl + 1, fb);
+                    tma3(sb + SO_XHE, &maps.xh, hE, k0, jl + 1, fb);
+                    if (hasN) tma3(sb + SO_XN, &maps.x4, co, k0, jl + 2, fb);
+                    if (hasS) tma3(sb + SO_XS, &maps.x4, co, k0, jl, fb);
                     tma3(sb + SO_F, &maps.f, cs, k0, jl, fb);
                     tma3(sb + SO_B4, &maps.b4, 2 * cs, k0, jl, fb);
                     tma3(sb + SO_B2, &maps.b2, cs, k0, jl, fb);
@@ -123,34 +132,39 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
             const int jl = (int)(it / tiles), t = (int)(it % tiles);
             const int64_t jg = g.j0 + jl;
-            const int i0 = t * SO_TILE;
-            const int w = min(SO_TILE, nx - i0);
+            const int m0 = t * SO_CONS;
+            const int w = min(SO_CONS, nh - m0);
             const bool hasN = jg < g.ny - 1, hasS = jg > 0;
-            const int par = (int)((jg + colour) & 1);
-            const int li = 2 * tid + par;  // natural column within the tile
-            const bool act = li < w;
-            const bool eh = li + 1 >= w, wh = li == 0;  // E / W neighbour in the halo boxes
+            const int par = (int)((jg + colour) & 1);  // natural column of split m: 2 m + par
+            const bool act = tid < w;
+            // the other colour's E neighbour is its split column m + par, the W one m + par - 1
+            const bool eh = par == 1 && tid + 1 >= w, wh = par == 0 && tid == 0;
             V cprev = 0.f, yprev = 0.f;
             for (int k8 = 0; k8 < NZ8; k8 += 8) {  // two stages = one 8-level TMEM chunk
-                float cb[8], yb[8];
+                float cb[8], yb[8], ob[8];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int k0 = k8 + h * SO_KS;
                     mbar_wait(&full[slot], phase);
                     const float* sb = stages + (size_t)slot * SO_STAGE_FLOATS;
                     float xm[SO_KS], xc[SO_KS], xp[SO_KS], xE[SO_KS], xW[SO_KS], xN[SO_KS], xS[SO_KS], f[SO_KS];
+                    float xo[SO_KS];
                     float4 b4[SO_KS];
                     float2 b2[SO_KS];
 #pragma unroll
                     for (int l = 0; l < SO_KS; ++l) {
-                        const float* xr = sb + SO_XJ + (l + 1) * 256;  // level k0 + l
-                        xm[l] = xr[li - 256];
-                        xc[l] = xr[li];
-                        xp[l] = xr[li + 256];
-                        xE[l] = eh ? sb[SO_XHE + (l + 1) * 4] : xr[li + 1];
-                        xW[l] = wh ? sb[SO_XHW + (l + 1) * 4 + 3] : xr[li - 1];
-                        xN[l] = hasN ? sb[SO_XN + l * 256 + li] : xE[l];  // poles: the zero N / S band reads x_E
-                        xS[l] = hasS ? sb[SO_XS + l * 256 + li] : xE[l];
+                        if (!FIRST) {
+                            const float* xr = sb + SO_XO + (l + 1) * 128;  // own colour, level k0 + l
+                            xm[l] = xr[tid - 128];
+                            xc[l] = xr[tid];
+                            xp[l] = xr[tid + 128];
+                        }
+                        const float* xt = sb + SO_XT + l * 128;
+                        xo[l] = xt[tid];  // the other colour in the same natural pair
+                        xE[l] = eh ? sb[SO_XHE + l * 4] : xt[tid + par];
+                        xW[l] = wh ? sb[SO_XHW + l * 4 + 3] : xt[tid + par - 1];
+                        xN[l] = hasN ? sb[SO_XN + l * 128 + tid] : xE[l];  // poles: the zero N / S band reads x_E
+                        xS[l] = hasS ? sb[SO_XS + l * 128 + tid] : xE[l];
                         f[l] = sb[SO_F + l * 128 + tid];
                         b4[l] = *reinterpret_cast<const float4*>(sb + SO_B4 + l * 512 + 4 * tid);
                         b2[l] = *reinterpret_cast<const float2*>(sb + SO_B2 + l * 256 + 2 * tid);
@@ -187,28 +201,39 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
                         }
                         cb[h * SO_KS + l] = c;
                         yb[h * SO_KS + l] = y;
+                        ob[h * SO_KS + l] = xo[l];
                         cprev = c;
                         yprev = y;
                     }
                 }
                 tm_st8(tl + (uint32_t)k8, cb);
                 tm_st8(tl + (uint32_t)(SO_MAX_NZ8 + k8), yb);
+                if (final_) tm_st8(tl + (uint32_t)(2 * SO_MAX_NZ8 + k8), ob);  // warp-uniform
             }
             asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
             // back substitution from the top (padded levels: c' = y = 0 as in the march kernels)
             V zn = 0.f;
-            V* xo = x + (int64_t)jl * g.row + (i0 + (act ? li : 0));
+            float* xsw = xs + (int64_t)jl * g.row + colour * nh + m0 + (act ? tid : 0);
+            float* zw = z + (int64_t)jl * g.row + 2 * (m0 + (act ? tid : 0));
             for (int k8 = NZ8 - 8; k8 >= 0; k8 -= 8) {
-                float cc[8], yy[8];
+                float cc[8], yy[8], oo[8];
                 tm_ld8_nw(tl + (uint32_t)k8, cc);
                 tm_ld8_nw(tl + (uint32_t)(SO_MAX_NZ8 + k8), yy);
+                if (final_) tm_ld8_nw(tl + (uint32_t)(2 * SO_MAX_NZ8 + k8), oo);
                 tm_wait_ld();
 #pragma unroll
                 for (int e = 7; e >= 0; --e) {
                     const int k = k8 + e;
                     zn = (k == nz - 1) ? yy[e] : fmaf(-cc[e], zn, yy[e]);
                     if (k >= nz) zn = 0.f;
-                    if (act && k < nz) xo[(int64_t)k * nx] = zn;
+                    if (act && k < nz) {
+                        if (final_) {  // natural (2 m, 2 m + 1) = (own, other) or (other, own)
+                            const float2 pr = par ? make_float2(oo[e], zn) : make_float2(zn, oo[e]);
+                            *reinterpret_cast<float2*>(zw + (int64_t)k * nx) = pr;
+                        } else {
+                            xsw[(int64_t)k * nx] = zn;
+                        }
+                    }
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -434,7 +459,8 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
 template <int MODE, int KIND>
 __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, const typename Prec<MODE>::V* __restrict__ fin,
                                                        typename Prec<MODE>::V* __restrict__ x, double omega_d,
-                                                       Split<typename Prec<MODE>::V> sp) {
+                                                       Split<typename Prec<MODE>::V> sp,
+                                                       typename Prec<MODE>::V* __restrict__ xsplit) {
     using V = typename Prec<MODE>::V;
     constexpr int KB = 4;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -470,10 +496,16 @@ __global__ void __launch_bounds__(128) k_sor_first_red(Geo g, Vecs<MODE> vv, con
     V* __restrict__ Fr = sp.f + rb + m;                           // colour 0 (red) half of the row
     V* __restrict__ Fb = sp.f + rb + nx / 2 + m;                  // colour 1 (black)
     const V* __restrict__ b2 = sp.b2 + 2 * (rb + m);              // red colour-split (U, D)
-    // x is written as whole (red, black) pairs, the black one 0 (x = 0 before the first sweep; the
-    // black half overwrites it): full 32-byte sectors, no read-for-merge of the partial ones
+    // x of the red column: into the colour-split x (xsplit, the fp32 TMA sweeps), else as whole
+    // (red, black) pairs of the natural x, the black one 0 (x = 0 before the first sweep; the black
+    // half overwrites it): full 32-byte sectors either way, no read-for-merge of partial ones
     V* __restrict__ Xw = x + q0;
+    V* __restrict__ Xs = xsplit ? xsplit + rb + m : nullptr;  // colour 0 (red) half of the row
     auto st_pair = [&](int64_t o, V xr) {
+        if (Xs) {
+            Xs[o] = xr;
+            return;
+        }
         VecN<V, 2> pr;
         pr.v[0] = red ? (V)0 : xr;
         pr.v[1] = red ? xr : (V)0;
