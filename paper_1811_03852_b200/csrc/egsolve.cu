@@ -162,7 +162,7 @@ struct eg_solver {
     MarchMaps maps{};
     SorMaps sor_maps{};     // TMA maps of the fp32 tri-SOR sweeps (colour-split arrays)
     bool sor_tma = false;   // later tri-SOR sweeps on k_sor_tma (fp32, colour-split copies)
-    SorMaps64 sor_maps64[2]{};
+    SorMaps64 sor_maps64{};
     bool sor_tma64 = false; // later tri-SOR sweeps on k_sor_tma64 (FP64, colour-split copies)
     int nsm = 148;
     size_t smem_march = 0;
@@ -512,7 +512,8 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
     }
     const int zi = (void*)z == (void*)v.zs ? 1 : 0;
     // the colour-split x of the fp32 TMA sweeps: ghosted, after f in the split region; row 0 pointer
-    float* xsr = s->split ? (float*)((V*)s->split + 7 * s->L.n) + s->L.row : nullptr;
+    V* xsv = s->split ? (V*)s->split + 7 * s->L.n + s->L.row : nullptr;
+    float* xsr = (float*)xsv;
     (void)xsr;
     for (int sw = 0; sw < s->sor_sweeps; ++sw)
         for (int colour = 0; colour < 2; ++colour) {
@@ -539,16 +540,20 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
                 }
                 if constexpr (MODE == 0) {
                     tma = s->sor_tma64 && s->split;
-                    if (tma) {  // FP64: the same first-sweep red kernel, then the TMA sweeps
+                    if (tma) {  // FP64: the same structure (colour-split x until the last half-sweep)
+                        const int fin_ = sw == s->sor_sweeps - 1 && colour == 1;
                         if (sw == 0 && colour == 0)
                             k_sor_first_red<MODE, KIND><<<gs, s->wth, s->smem_th, s->st>>>(s->geo, v, fin, z, s->sor_omega, sp,
-                                                                                         nullptr);
+                                                                                         xsv);
                         else if (sw == 0)
-                            k_sor_tma64<true><<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)z, colour,
-                                                                                    s->sor_omega, KIND != 0, s->sor_maps64[zi]);
+                            k_sor_tma64<true><<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)xsv, (double*)z,
+                                                                                    colour, fin_, s->sor_omega, KIND != 0,
+                                                                                    s->sor_maps64);
                         else
-                            k_sor_tma64<false><<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)z, colour,
-                                                                                     s->sor_omega, KIND != 0, s->sor_maps64[zi]);
+                            k_sor_tma64<false><<<s->nsm, S6_THREADS, S6_SMEM, s->st>>>(s->geo, v, (double*)xsv, (double*)z,
+                                                                                     colour, fin_, s->sor_omega, KIND != 0,
+                                                                                     s->sor_maps64);
+                        xs_half = !fin_;
                     }
                 }
                 if (!tma) {
@@ -1087,17 +1092,14 @@ bool make_sor_maps64(eg_solver* s) {
     double* b4s = (double*)s->split;
     double* b2s = b4s + 4 * s->L.n;
     double* fs = b2s + 2 * s->L.n;
-    bool ok = true;
-    for (int zi = 0; zi < 2; ++zi) {
-        void* zg = s->zext[zi];  // ghosted: local row r is coordinate r + 1
-        SorMaps64& m = s->sor_maps64[zi];
-        ok = ok && encode_map_box(enc, &m.x6, zg, nx, nz, nyl + 2, 8, 256, S6_KS + 2);
-        ok = ok && encode_map_box(enc, &m.xh, zg, nx, nz, nyl + 2, 8, 4, S6_KS + 2);
-        ok = ok && encode_map_box(enc, &m.x4, zg, nx, nz, nyl + 2, 8, 256, S6_KS);
-        ok = ok && encode_map_box(enc, &m.f, fs, nx, nz, nyl, 8, 128, S6_KS);
-        ok = ok && encode_map_box(enc, &m.b4, b4s, 4 * nx, nz, nyl, 8, 256, S6_KS);
-        ok = ok && encode_map_box(enc, &m.b2, b2s, 2 * nx, nz, nyl, 8, 256, S6_KS);
-    }
+    double* xs = fs + s->L.n;  // the colour-split x from its row -1: rows are addressed as jl + 1
+    SorMaps64& m = s->sor_maps64;
+    bool ok = encode_map_box(enc, &m.xo6, xs, nx, nz, nyl + 2, 8, 128, S6_KS + 2);
+    ok = ok && encode_map_box(enc, &m.x4, xs, nx, nz, nyl + 2, 8, 128, S6_KS);
+    ok = ok && encode_map_box(enc, &m.xh, xs, nx, nz, nyl + 2, 8, 4, S6_KS);
+    ok = ok && encode_map_box(enc, &m.f, fs, nx, nz, nyl, 8, 128, S6_KS);
+    ok = ok && encode_map_box(enc, &m.b4, b4s, 4 * nx, nz, nyl, 8, 256, S6_KS);
+    ok = ok && encode_map_box(enc, &m.b2, b2s, 2 * nx, nz, nyl, 8, 256, S6_KS);
     return ok;
 }
 
@@ -1125,8 +1127,8 @@ bool valid_grid(const eg_grid* g) {
 // copies change how much of each loaded sector is used, not what the sweep needs.
 double sor_alg_bytes(const eg_solver* s, int kind, int sweep, int colour) {
     const double V = (double)s->L.vsz, n = (double)s->L.n;
-    // the fp32 TMA sweeps' last half writes z in natural order, both colours (+ V / 2)
-    const double fin_z = (s->sor_tma && s->split && sweep == s->sor_sweeps - 1 && colour == 1) ? 0.5 * V * n : 0.0;
+    // the TMA sweeps' last half writes z in natural order, both colours (+ V / 2)
+    const double fin_z = ((s->sor_tma || s->sor_tma64) && s->split && sweep == s->sor_sweeps - 1 && colour == 1) ? 0.5 * V * n : 0.0;
     if (sweep > 0) return 5 * V * n + fin_z;                           // f, 6 bands / 2; x; x / 2
     const double fin = kind == 0 ? 0.5 : (kind == 1 ? 1.5 : 1.0);     // fin | r, p, v | r, v (one colour)
     const double out = 0.5 + (kind != 0 ? 0.5 : 0.0) + (s->split ? 0.5 : 0.0);  // x, p / s, f split

@@ -247,32 +247,33 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
     }
 }
 
-// FP64 counterpart of k_sor_tma<MODE, false> (the sweeps after the first), same item geometry and
-// arithmetic as k_sor_half<0, 0, false> operation for operation (so the FP64 tri-SOR result is
-// bitwise unchanged).  Doubles double the stage: 3 stages of 4 levels (57 KB each) fill one CTA per
-// SM; (E,W,N,S) of the 128 colour columns come as two 256-element boxes; c' and y live in TMEM as
-// pairs of 32-bit words (c' [0, 144), y [144, 288) of a 512-column allocation).
+// FP64 counterpart of k_sor_tma (same items, colour-split x, FINAL natural write), arithmetic as
+// k_sor_half<0, ...> operation for operation (so the FP64 tri-SOR result is bitwise unchanged).
+// Doubles double the stage: 4 stages of 4 levels (48 KB each) fill one CTA per SM; (E,W,N,S) of the
+// 128 colour columns come as two 256-element boxes; c', y and (FINAL) the other colour live in TMEM
+// as pairs of 32-bit words (c' [0, 144), y [144, 288), other [288, 432) of a 512-column allocation).
 constexpr int S6_KS = 4;
-constexpr int S6_STAGES = 3;
+constexpr int S6_STAGES = 4;
 constexpr int S6_THREADS = SO_CONS + 32;
-constexpr int S6_XJ = 0;                               // [KS+2][256]
-constexpr int S6_XHW = S6_XJ + (S6_KS + 2) * 256;      // [KS+2][4] (32 reserved: 128-byte aligned)
+constexpr int S6_XO = 0;                               // own colour [KS+2][128]
+constexpr int S6_XT = S6_XO + (S6_KS + 2) * 128;       // other colour, row j [KS][128]
+constexpr int S6_XHW = S6_XT + S6_KS * 128;            // [KS][4] (32 reserved: 128-byte aligned)
 constexpr int S6_XHE = S6_XHW + 32;
-constexpr int S6_XN = S6_XHE + 32;                     // [KS][256]
-constexpr int S6_XS = S6_XN + S6_KS * 256;             // [KS][256]
-constexpr int S6_F = S6_XS + S6_KS * 256;              // [KS][128]
+constexpr int S6_XN = S6_XHE + 32;                     // other colour, row j+1 [KS][128]
+constexpr int S6_XS = S6_XN + S6_KS * 128;             // other colour, row j-1 [KS][128]
+constexpr int S6_F = S6_XS + S6_KS * 128;              // [KS][128]
 constexpr int S6_B4L = S6_F + S6_KS * 128;             // [KS][64 columns x 4]
 constexpr int S6_B4H = S6_B4L + S6_KS * 256;           // [KS][64 columns x 4]
 constexpr int S6_B2 = S6_B4H + S6_KS * 256;            // [KS][128 columns x 2]
 constexpr int S6_STAGE_DOUBLES = S6_B2 + S6_KS * 256;
-constexpr uint32_t S6_BOX_XJ = (S6_KS + 2) * 256 * 8, S6_BOX_XH = (S6_KS + 2) * 4 * 8, S6_BOX_XR = S6_KS * 256 * 8;
+constexpr uint32_t S6_BOX_XO = (S6_KS + 2) * 128 * 8, S6_BOX_XR = S6_KS * 128 * 8, S6_BOX_XH = S6_KS * 4 * 8;
 constexpr uint32_t S6_BOX_F = S6_KS * 128 * 8, S6_BOX_B = S6_KS * 256 * 8;
 constexpr int S6_SMEM = S6_STAGES * S6_STAGE_DOUBLES * 8 + 128;
 
-// maps: x natural with (256, KS+2), (4, KS+2), (256, KS) boxes; f split (128, KS); (E,W,N,S) split
-// [nyl][nz][4 nx] with (256, KS) boxes; (U, D) split [nyl][nz][2 nx] with (256, KS) boxes
+// maps: xs (ghosted, colour-split) with (128, KS+2), (128, KS), (4, KS) boxes; f split (128, KS);
+// (E,W,N,S) split [nyl][nz][4 nx] with (256, KS) boxes; (U, D) split [nyl][nz][2 nx] with (256, KS)
 struct SorMaps64 {
-    CUtensorMap x6, xh, x4, f, b4, b2;
+    CUtensorMap xo6, x4, xh, f, b4, b2;
 };
 
 __device__ __forceinline__ void split_d(double v, float& lo, float& hi) {
@@ -287,7 +288,8 @@ __device__ __forceinline__ double join_d(float lo, float hi) {
 // grid: persistent (one CTA / SM), block S6_THREADS, dynamic smem S6_SMEM.  FIRST: the black half of
 // the first sweep after k_sor_first_red<0, KIND> (rhs = omega (f - H x); the own column is not read).
 template <bool FIRST>
-__global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, double* __restrict__ x, int colour,
+__global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, double* __restrict__ xs,
+                                                              double* __restrict__ z, int colour, int final_,
                                                               double omega_d, int check_halt,
                                                               const __grid_constant__ SorMaps64 maps) {
     using V = double;
@@ -298,9 +300,11 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
     const V om = (V)omega_d, om1 = (V)(1.0 - omega_d);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nx = (int)g.nx, nz = (int)g.nz, nyl = (int)g.nyl;
-    const int tiles = (nx + SO_TILE - 1) / SO_TILE;
+    const int nh = nx / 2;
+    const int tiles = (nh + SO_CONS - 1) / SO_CONS;
     const int64_t items = (int64_t)tiles * nyl;
     const int NZ4 = (nz + S6_KS - 1) / S6_KS * S6_KS;
+    const int oc = colour ^ 1;
     V* stages = reinterpret_cast<V*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
     if (tid == 0) {
         for (int q = 0; q < S6_STAGES; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], SO_CONS); }
@@ -323,25 +327,26 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
             for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
                 const int jl = (int)(it / tiles), t = (int)(it % tiles);
                 const int64_t jg = g.j0 + jl;
-                const int i0 = t * SO_TILE;
-                const int w = min(SO_TILE, nx - i0);
-                const int iWb = (i0 == 0 ? nx - 1 : i0 - 1) - 3;
-                const int iEb = (i0 + w == nx) ? 0 : i0 + w;
-                const int cs = colour * (nx / 2) + t * (SO_TILE / 2);
+                const int m0 = t * SO_CONS;
+                const int w = min(SO_CONS, nh - m0);
+                const int cs = colour * nh + m0, co = oc * nh + m0;
+                const int hW = oc * nh + (m0 == 0 ? nh : m0) - 4;
+                const int hE = oc * nh + (m0 + w == nh ? 0 : m0 + w);
                 const bool hasN = jg < g.ny - 1, hasS = jg > 0;
                 for (int q = 0; q < nstage; ++q) {
                     const int k0 = q * S6_KS;
                     if (round > 0) mbar_wait_sleep(&empty[slot], (uint32_t)((round - 1) & 1), 32);
                     uint64_t* fb = &full[slot];
-                    const uint32_t bytes = S6_BOX_XJ + 2 * S6_BOX_XH + (hasN ? S6_BOX_XR : 0u) + (hasS ? S6_BOX_XR : 0u) +
-                                           S6_BOX_F + 3 * S6_BOX_B;
+                    const uint32_t bytes = (FIRST ? 0u : S6_BOX_XO) + S6_BOX_XR + 2 * S6_BOX_XH +
+                                           (hasN ? S6_BOX_XR : 0u) + (hasS ? S6_BOX_XR : 0u) + S6_BOX_F + 3 * S6_BOX_B;
                     mbar_expect_tx(fb, bytes);
                     V* sb = stages + (size_t)slot * S6_STAGE_DOUBLES;
-                    tma3(sb + S6_XJ, &maps.x6, i0, k0 - 1, jl + 1, fb);
-                    tma3(sb + S6_XHW, &maps.xh, iWb, k0 - 1, jl + 1, fb);
-                    tma3(sb + S6_XHE, &maps.xh, iEb, k0 - 1, jl + 1, fb);
-                    if (hasN) tma3(sb + S6_XN, &maps.x4, i0, k0, jl + 2, fb);
-                    if (hasS) tma3(sb + S6_XS, &maps.x4, i0, k0, jl, fb);
+                    if (!FIRST) tma3(sb + S6_XO, &maps.xo6, cs, k0 - 1, jl + 1, fb);
+                    tma3(sb + S6_XT, &maps.x4, co, k0, jl + 1, fb);
+                    tma3(sb + S6_XHW, &maps.xh, hW, k0, jl + 1, fb);
+                    tma3(sb + S6_XHE, &maps.xh, hE, k0, jl + 1, fb);
+                    if (hasN) tma3(sb + S6_XN, &maps.x4, co, k0, jl + 2, fb);
+                    if (hasS) tma3(sb + S6_XS, &maps.x4, co, k0, jl, fb);
                     tma3(sb + S6_F, &maps.f, cs, k0, jl, fb);
                     tma3(sb + S6_B4L, &maps.b4, 4 * cs, k0, jl, fb);
                     tma3(sb + S6_B4H, &maps.b4, 4 * cs + 256, k0, jl, fb);
@@ -358,28 +363,26 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
             const int jl = (int)(it / tiles), t = (int)(it % tiles);
             const int64_t jg = g.j0 + jl;
-            const int i0 = t * SO_TILE;
-            const int w = min(SO_TILE, nx - i0);
+            const int m0 = t * SO_CONS;
+            const int w = min(SO_CONS, nh - m0);
             const bool hasN = jg < g.ny - 1, hasS = jg > 0;
             const int par = (int)((jg + colour) & 1);
-            const int li = 2 * tid + par;
-            const bool act = li < w;
-            const bool eh = li + 1 >= w, wh = li == 0;
+            const bool act = tid < w;
+            const bool eh = par == 1 && tid + 1 >= w, wh = par == 0 && tid == 0;
             V cprev = 0.0, yprev = 0.0;
             for (int q = 0; q < nstage; ++q) {
                 const int k0 = q * S6_KS;
                 mbar_wait(&full[slot], phase);
                 const V* sb = stages + (size_t)slot * S6_STAGE_DOUBLES;
-                float cw[2 * S6_KS], yw[2 * S6_KS];
+                float cw[2 * S6_KS], yw[2 * S6_KS], ow[2 * S6_KS];
 #pragma unroll
                 for (int l = 0; l < S6_KS; ++l) {
                     const int k = k0 + l;
-                    const V* xr = sb + S6_XJ + (l + 1) * 256;  // level k
-                    const V xm = xr[li - 256], xc = xr[li], xp = xr[li + 256];
-                    const V xE = eh ? sb[S6_XHE + (l + 1) * 4] : xr[li + 1];
-                    const V xW = wh ? sb[S6_XHW + (l + 1) * 4 + 3] : xr[li - 1];
-                    const V xN = hasN ? sb[S6_XN + l * 256 + li] : xE;
-                    const V xS = hasS ? sb[S6_XS + l * 256 + li] : xE;
+                    const V* xt = sb + S6_XT + l * 128;
+                    const V xE = eh ? sb[S6_XHE + l * 4] : xt[tid + par];
+                    const V xW = wh ? sb[S6_XHW + l * 4 + 3] : xt[tid + par - 1];
+                    const V xN = hasN ? sb[S6_XN + l * 128 + tid] : xE;
+                    const V xS = hasS ? sb[S6_XS + l * 128 + tid] : xE;
                     const V f = sb[S6_F + l * 128 + tid];
                     const double2 e01 = *reinterpret_cast<const double2*>(sb + b4off + l * 256);
                     const double2 e23 = *reinterpret_cast<const double2*>(sb + b4off + l * 256 + 2);
@@ -392,6 +395,8 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
                     if (FIRST) {
                         rhs = om * (f - hx);
                     } else {
+                        const V* xr = sb + S6_XO + (l + 1) * 128;  // own colour, level k
+                        const V xm = xr[tid - 128], xc = xr[tid], xp = xr[tid + 128];
                         const V xup = k + 1 < nz ? xp : xc;  // U = 0 on the top level
                         V tx = xc;
                         tx = fma(ud.x, xup, tx);
@@ -410,6 +415,7 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
                     if (k >= nz) c = y = 0.0;  // padded levels: z = 0 above the top
                     split_d(c, cw[2 * l], cw[2 * l + 1]);
                     split_d(y, yw[2 * l], yw[2 * l + 1]);
+                    split_d(xt[tid], ow[2 * l], ow[2 * l + 1]);  // the other colour of the natural pair
                     cprev = c;
                     yprev = y;
                 }
@@ -418,14 +424,17 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
                 if (++slot == S6_STAGES) { slot = 0; phase ^= 1u; }
                 tm_st8(tl + (uint32_t)(2 * k0), cw);
                 tm_st8(tl + (uint32_t)(144 + 2 * k0), yw);
+                if (final_) tm_st8(tl + (uint32_t)(288 + 2 * k0), ow);  // warp-uniform
             }
             asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
             V zn = 0.0;
-            V* xo = x + (int64_t)jl * g.row + (i0 + (act ? li : 0));
+            V* xsw = xs + (int64_t)jl * g.row + colour * nh + m0 + (act ? tid : 0);
+            V* zw = z + (int64_t)jl * g.row + 2 * (m0 + (act ? tid : 0));
             for (int k0 = NZ4 - S6_KS; k0 >= 0; k0 -= S6_KS) {
-                float cc[8], yy[8];
+                float cc[8], yy[8], oo[8];
                 tm_ld8_nw(tl + (uint32_t)(2 * k0), cc);
                 tm_ld8_nw(tl + (uint32_t)(144 + 2 * k0), yy);
+                if (final_) tm_ld8_nw(tl + (uint32_t)(288 + 2 * k0), oo);
                 tm_wait_ld();
 #pragma unroll
                 for (int e = S6_KS - 1; e >= 0; --e) {
@@ -433,7 +442,15 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
                     const V yk = join_d(yy[2 * e], yy[2 * e + 1]);
                     zn = (k == nz - 1) ? yk : fma(-join_d(cc[2 * e], cc[2 * e + 1]), zn, yk);
                     if (k >= nz) zn = 0.0;
-                    if (act && k < nz) xo[(int64_t)k * nx] = zn;
+                    if (act && k < nz) {
+                        if (final_) {
+                            const V ov = join_d(oo[2 * e], oo[2 * e + 1]);
+                            const double2 pr = par ? make_double2(ov, zn) : make_double2(zn, ov);
+                            *reinterpret_cast<double2*>(zw + (int64_t)k * nx) = pr;
+                        } else {
+                            xsw[(int64_t)k * nx] = zn;
+                        }
+                    }
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
