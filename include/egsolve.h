@@ -108,8 +108,9 @@ typedef struct {
 int eg_workspace_bytes(const eg_grid* grid, const eg_dist* dist, eg_precision prec, size_t* bytes);
 
 /* Same, for a solver that will also use optional features.  features: bit mask of
- *   EG_FEATURE_TRISOR: room for colour-split copies of the scaled bands and of the preconditioner's
- *     right-hand side (7 working-precision values per point), which the red-black tri-SOR sweeps
+ *   EG_FEATURE_TRISOR: room for colour-split copies of the scaled bands, of the preconditioner's
+ *     right-hand side and of the sweeps' iterate (8 working-precision values per point plus two
+ *     ghost rows), which the red-black tri-SOR sweeps
  *     (EG_PRECOND_TRISOR) read instead of every other value of the natural-order arrays.  A solver
  *     whose workspace is at least this size uses them; a smaller workspace still runs tri-SOR, on
  *     the natural-order arrays (same results, bitwise).
