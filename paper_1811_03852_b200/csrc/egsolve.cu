@@ -186,6 +186,8 @@ struct eg_solver {
     size_t smem_th = 0;
     bool use_tm = false;         // fp32 Thomas with TMEM-resident factors (nz <= 128)
     bool use_tm64 = false;       // fp64 Thomas with TMEM-resident factors (nz <= 80)
+    bool th_tma64 = false;       // fp64 phase-A Thomas on the TMA-fed kernel (nz <= 72; 6 % faster)
+    ThomasMaps64 thmaps64{};
     size_t smem_tm = 0;
     // graphs of one iteration, keyed on the iterate pointer (two: eg_solve_batch alternates buffers)
     cudaGraphExec_t graphs[2]{};
@@ -618,7 +620,8 @@ int iteration(eg_solver* s, void* x_it) {
             else if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
             else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
         } else {
-            if (s->use_tm64) k_thomas_tm64<1><<<gtm, 128, TM64_SMEM, s->st>>>(s->geo, v, nullptr, v.z);
+            if (s->th_tma64) k_thomas_tma64<1><<<s->nsm, T6_THREADS, T6_SMEM, s->st>>>(s->geo, v, v.z, s->thmaps64);
+            else if (s->use_tm64) k_thomas_tm64<1><<<gtm, 128, TM64_SMEM, s->st>>>(s->geo, v, nullptr, v.z);
             else if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
             else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
         }
@@ -638,6 +641,8 @@ int iteration(eg_solver* s, void* x_it) {
             else if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
             else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
         } else {
+            // (the TMA-fed kernel is slower for this lighter solve, 3.68 vs 3.40 ms at C5: one CTA per SM
+            // cannot hide the FP64 recurrence the 2-CTA TMEM kernel overlaps)
             if (s->use_tm64) k_thomas_tm64<2><<<gtm, 128, TM64_SMEM, s->st>>>(s->geo, v, nullptr, v.zs);
             else if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
             else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
@@ -1103,6 +1108,22 @@ bool make_sor_maps64(eg_solver* s) {
     return ok;
 }
 
+bool make_thomas_maps64(eg_solver* s) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return false;
+    EncodeTiledFn enc = (EncodeTiledFn)fn;
+    const int64_t nx = s->grid.nx, nz = s->grid.nz, nyl = s->L.nyl;
+    ThomasMaps64& m = s->thmaps64;
+    bool ok = encode_map_box(enc, &m.a, s->vec[0], nx, nz, nyl, 8, 128, T6_KS);      // r
+    ok = ok && encode_map_box(enc, &m.p, s->vec[2], nx, nz, nyl, 8, 128, T6_KS);     // p
+    ok = ok && encode_map_box(enc, &m.v, s->vec[3], nx, nz, nyl, 8, 128, T6_KS);     // v
+    ok = ok && encode_map_box(enc, &m.ud, s->B2, 2 * nx, nz, nyl, 8, 256, T6_KS);   // (U, D)
+    return ok;
+}
+
 bool valid_dist(const eg_grid* g, const eg_dist* d, int64_t* jb, int64_t* je, int* rank, int* nranks) {
     if (!d) { *jb = 0; *je = g->ny; *rank = 0; *nranks = 1; return true; }
     *jb = d->j_begin; *je = d->j_end; *rank = d->rank; *nranks = d->nranks;
@@ -1391,6 +1412,15 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
             attr((const void*)k_sor_first_red<2, 2>, (int)s->smem_th);
         }
         s->sor_tma = e1 == cudaSuccess && !(ns && ns[0] == '1') && make_sor_maps(s);
+    }
+    if (rc == EG_OK && prec == EG_FP64 && grid->nx % 2 == 0 && grid->nz <= SO_MAX_NZ8) {
+        // FP64 Thomas of the iteration on the TMA-fed kernel (EG_NO_THOMAS_TMA=1 keeps k_thomas_tm64)
+        const char* nt = getenv("EG_NO_THOMAS_TMA");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&s->nsm, cudaDevAttrMultiProcessorCount, dev);
+        const cudaError_t e1 = cudaFuncSetAttribute(k_thomas_tma64<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, T6_SMEM);
+        s->th_tma64 = e1 == cudaSuccess && !(nt && nt[0] == '1') && make_thomas_maps64(s);
     }
     if (rc == EG_OK && s->split && prec == EG_FP64 && grid->nx % 4 == 0 && grid->nz <= SO_MAX_NZ8) {
         // FP64: later tri-SOR sweeps on k_sor_tma64 (EG_NO_SOR_TMA=1 keeps k_sor_half)

@@ -464,6 +464,173 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
     }
 }
 
+// FP64 Thomas solve of the 5-kernel schedule (a3 / a6 / precondition), TMA-fed: the FP64 analogue of
+// the fp32 path's TMEM Thomas, with the same arithmetic as k_thomas_tm64<KIND> operation for
+// operation (bitwise the same p / s and z).  Item = (latitude row, 128 natural columns), one column
+// per consumer thread; a producer warp streams 4-level stages of r, (p, v) / v / fin and (U, D) with
+// 3-D TMA boxes; c' and y live in TMEM as word pairs (c' [0, 144), y [144, 288)); one CTA per SM.
+// KIND 0: f = fin;  1: p = r + beta (p - omega v), f = p (r only on a fresh iteration);  2: s = r -
+// alpha v, f = s.
+constexpr int T6_KS = 4;
+constexpr int T6_STAGES = 6;
+constexpr int T6_THREADS = SO_CONS + 32;
+constexpr int T6_A = 0;                        // r (or fin) [KS][128]
+constexpr int T6_P = T6_A + T6_KS * 128;       // p [KS][128]
+constexpr int T6_V = T6_P + T6_KS * 128;       // v [KS][128]
+constexpr int T6_UD = T6_V + T6_KS * 128;      // (U, D) [KS][256]
+constexpr int T6_STAGE_DOUBLES = T6_UD + T6_KS * 256;
+constexpr uint32_t T6_BOX_V = T6_KS * 128 * 8, T6_BOX_UD = T6_KS * 256 * 8;
+constexpr int T6_SMEM = T6_STAGES * T6_STAGE_DOUBLES * 8 + 128;
+
+// maps: r, p, v, fin natural (128, KS); (U, D) natural [nyl][nz][2 nx] (256, KS)
+struct ThomasMaps64 {
+    CUtensorMap a, p, v, ud;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(T6_THREADS, 1) k_thomas_tma64(Geo g, Vecs<0> vv, double* __restrict__ zout,
+                                                                 const __grid_constant__ ThomasMaps64 maps) {
+    using V = double;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    __shared__ __align__(8) uint64_t full[T6_STAGES], empty[T6_STAGES];
+    __shared__ uint32_t tm_slot;
+    V beta = 0, omega = 0, alpha = 0;
+    bool fresh = false;
+    if (KIND != 0) {
+        const DevState* st = vv.st;
+        if (st->halt != H_RUN) return;  // uniform
+        if (KIND == 1) {
+            fresh = st->fresh != 0;
+            beta = st->beta_v;
+            omega = st->omega_v;
+        } else {
+            alpha = st->alpha_v;
+        }
+    }
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nx = (int)g.nx, nz = (int)g.nz, nyl = (int)g.nyl;
+    const int tiles = (nx + 127) / 128;
+    const int64_t items = (int64_t)tiles * nyl;
+    const int NZ4 = (nz + T6_KS - 1) / T6_KS * T6_KS;
+    V* stages = reinterpret_cast<V*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    if (tid == 0) {
+        for (int q = 0; q < T6_STAGES; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], SO_CONS); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tm_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = tm_slot;
+    const int nstage = NZ4 / T6_KS;
+    const bool rpv = KIND == 1 && !fresh;  // p and v are read
+
+    if (warp == SO_CONS / 32) {  // ------------------------------------------------ producer
+        if (lane == 0) {
+            int slot = 0, round = 0;
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+                const int jl = (int)(it / tiles), t = (int)(it % tiles);
+                const int i0 = t * 128;
+                for (int q = 0; q < nstage; ++q) {
+                    const int k0 = q * T6_KS;
+                    if (round > 0) mbar_wait_sleep(&empty[slot], (uint32_t)((round - 1) & 1), 32);
+                    uint64_t* fb = &full[slot];
+                    const uint32_t bytes = T6_BOX_V * (1u + (rpv ? 2u : 0u) + (KIND == 2 ? 1u : 0u)) + T6_BOX_UD;
+                    mbar_expect_tx(fb, bytes);
+                    V* sb = stages + (size_t)slot * T6_STAGE_DOUBLES;
+                    tma3(sb + T6_A, &maps.a, i0, k0, jl, fb);
+                    if (rpv) tma3(sb + T6_P, &maps.p, i0, k0, jl, fb);
+                    if (rpv || KIND == 2) tma3(sb + T6_V, &maps.v, i0, k0, jl, fb);
+                    tma3(sb + T6_UD, &maps.ud, 2 * i0, k0, jl, fb);
+                    if (++slot == T6_STAGES) { slot = 0; ++round; }
+                }
+            }
+        }
+    } else {  // ------------------------------------------------------------------ consumers
+        const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+        int slot = 0;
+        uint32_t phase = 0;
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+            const int jl = (int)(it / tiles), t = (int)(it % tiles);
+            const int i = t * 128 + tid;
+            const bool act = i < nx;
+            const int64_t base = (int64_t)jl * g.row + (act ? i : 0);
+            V* __restrict__ Pw = (KIND == 1 ? vv.p : vv.s) + base;
+            V cprev = 0.0, yprev = 0.0;
+            for (int q = 0; q < nstage; ++q) {
+                const int k0 = q * T6_KS;
+                mbar_wait(&full[slot], phase);
+                const V* sb = stages + (size_t)slot * T6_STAGE_DOUBLES;
+                float cw[2 * T6_KS], yw[2 * T6_KS];
+                V fv[T6_KS];
+#pragma unroll
+                for (int l = 0; l < T6_KS; ++l) {
+                    const int k = k0 + l;
+                    const V a = sb[T6_A + l * 128 + tid];
+                    V f;
+                    if (KIND == 0) f = a;
+                    else if (KIND == 1) f = fresh ? a : fma(beta, fma(-omega, sb[T6_V + l * 128 + tid], sb[T6_P + l * 128 + tid]), a);
+                    else f = fma(-alpha, sb[T6_V + l * 128 + tid], a);
+                    const double2 ud = *reinterpret_cast<const double2*>(sb + T6_UD + l * 256 + 2 * tid);
+                    V c, y;
+                    if (k == 0) {
+                        c = ud.x;
+                        y = f;
+                    } else {
+                        const V inv = rcp_fast<V>(fma(-ud.y, cprev, (V)1));
+                        c = ud.x * inv;
+                        y = fma(-ud.y, yprev, f) * inv;
+                    }
+                    if (k >= nz) c = y = 0.0;  // padded levels: z = 0 above the top
+                    fv[l] = f;
+                    split_d(c, cw[2 * l], cw[2 * l + 1]);
+                    split_d(y, yw[2 * l], yw[2 * l + 1]);
+                    cprev = c;
+                    yprev = y;
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&empty[slot]);
+                if (++slot == T6_STAGES) { slot = 0; phase ^= 1u; }
+                if (KIND != 0) {
+#pragma unroll
+                    for (int l = 0; l < T6_KS; ++l)
+                        if (act && k0 + l < nz) Pw[(int64_t)(k0 + l) * nx] = fv[l];
+                }
+                tm_st8(tl + (uint32_t)(2 * k0), cw);
+                tm_st8(tl + (uint32_t)(144 + 2 * k0), yw);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            V zn = 0.0;
+            V* zw = zout + base;
+            for (int k0 = NZ4 - T6_KS; k0 >= 0; k0 -= T6_KS) {
+                float cc[8], yy[8];
+                tm_ld8_nw(tl + (uint32_t)(2 * k0), cc);
+                tm_ld8_nw(tl + (uint32_t)(144 + 2 * k0), yy);
+                tm_wait_ld();
+#pragma unroll
+                for (int e = T6_KS - 1; e >= 0; --e) {
+                    const int k = k0 + e;
+                    const V yk = join_d(yy[2 * e], yy[2 * e + 1]);
+                    zn = (k == nz - 1) ? yk : fma(-join_d(cc[2 * e], cc[2 * e + 1]), zn, yk);
+                    if (k >= nz) zn = 0.0;
+                    if (act && k < nz) zw[(int64_t)k * nx] = zn;
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase) : "memory");
+    }
+}
+
 // The red half of the first sweep (x = 0 before it: rhs = omega f) fused with forming f for BOTH
 // colours: thread m owns the natural column pair (2m, 2m+1) of a row, reads r, p, v (or fin) for
 // both with 8-byte loads, writes p / s (KIND 1 / 2) for both and f colour-split for both, and solves

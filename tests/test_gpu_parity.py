@@ -492,3 +492,25 @@ def test_concurrent_fused_solves_on_two_streams(monkeypatch):
     assert not any(t.is_alive() for t in ts) and not errs
     torch.cuda.synchronize()
     assert all(torch.equal(o, x) for o, x in zip(outs, seq))
+
+
+@pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], gen.Problem(200, 37, 13, seed=8), gen.Problem(388, 23, 70, seed=13)],
+                         ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
+def test_fp64_thomas_tma_matches_tmem_kernel(prob, monkeypatch):
+    """The FP64 iteration's Thomas solves on the TMA-fed kernel (k_thomas_tma64, the default for
+    nz <= 72) give bitwise the results of the TMEM-factor kernel (EG_NO_THOMAS_TMA=1)."""
+    bands, b = gen.host(prob)
+    g = (prob.nx, prob.ny, prob.nz)
+    bd = torch.from_numpy(bands).cuda()
+    bt = torch.from_numpy(b).cuda()
+    s1 = egs.Solver(g, bd, "fp64")
+    monkeypatch.setenv("EG_NO_THOMAS_TMA", "1")
+    s2 = egs.Solver(g, bd, "fp64")
+    monkeypatch.delenv("EG_NO_THOMAS_TMA")
+    for kw in (dict(tol=1e-10, maxit=60, restart_every=5), dict(tol=0.0, maxit=8)):
+        x1, i1, h1 = s1.solve(bt, **kw)
+        x2, i2, h2 = s2.solve(bt, **kw)
+        assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
+    s1.profile_reset()
+    s1.solve(bt, tol=0.0, maxit=2, flags=egs.EG_SOLVE_PROFILE)
+    assert s1.profile()["thomas_p"][1] == 2
