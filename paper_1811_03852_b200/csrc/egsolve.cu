@@ -492,6 +492,21 @@ int iteration_fused(eg_solver* s, void* x_it) {
     return EG_OK;
 }
 
+// the colour-split band copies of the tri-SOR sweeps for the current operator (set_operator writes
+// them itself once tri-SOR is selected; otherwise this pass derives them).  Called before an
+// iteration graph is captured, so that the one-time pass is never part of the replayed graph.
+template <int MODE>
+int ensure_split(eg_solver* s) {
+    using V = typename Prec<MODE>::V;
+    if (!s->split || s->split_valid) return EG_OK;
+    V* b4s = (V*)s->split;
+    const dim3 grid((unsigned)((s->grid.nx + 255) / 256), (unsigned)s->grid.nz, (unsigned)s->L.nyl);
+    k_split_bands<V><<<grid, 256, 0, s->st>>>(s->geo, (const V*)s->B4, (const V*)s->B2, b4s, b4s + 4 * s->L.n);
+    CK(cudaGetLastError());
+    s->split_valid = true;
+    return EG_OK;
+}
+
 // NEXT-1: M^-1 f by `sor_sweeps` red-black tri-SOR sweeps (Eq. 7) into the ghosted array z (row 0
 // pointer).  KIND 1 / 2: the first sweep also forms and stores p (s); later sweeps read it back.
 template <int MODE, int KIND>
@@ -504,12 +519,7 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
     if (s->split) {  // colour-split bands (refreshed after every set_operator) and f
         V* b4s = (V*)s->split;
         V* b2s = b4s + 4 * s->L.n;
-        if (!s->split_valid) {
-            const dim3 grid((unsigned)((s->grid.nx + 255) / 256), (unsigned)s->grid.nz, (unsigned)s->L.nyl);
-            k_split_bands<V><<<grid, 256, 0, s->st>>>(s->geo, v.B4, v.B2, b4s, b2s);
-            CK(cudaGetLastError());
-            s->split_valid = true;
-        }
+        if ((rc = ensure_split<MODE>(s))) return rc;
         sp = Split<V>{b4s, b2s, b2s + 2 * s->L.n};
     }
     const int zi = (void*)z == (void*)v.zs ? 1 : 0;
@@ -819,6 +829,7 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     int bd_at = -1;
     const int chunk_max = prm->check_every > 0 ? std::min(prm->check_every, HIST_CAP) : 8;
 
+    if (s->precond == EG_PRECOND_TRISOR && rc == EG_OK && (rc = ensure_split<MODE>(s))) return rc;
     // graph for this iterate pointer (two cached entries)
     s->graph = nullptr;
     for (int gi = 0; gi < 2; ++gi)
@@ -932,8 +943,13 @@ int create_impl(eg_solver* s, const double* const bands[7]) {
     CK(cudaMemsetAsync(s->dstate, 0, sizeof(DevState), s->st));
     const dim3 grid((unsigned)((s->grid.nx + 255) / 256), (unsigned)s->grid.nz, (unsigned)s->L.nyl);
     {
-        ProfScope ps(s, KID_SCALE);
-        k_scale<V><<<grid, 256, 0, s->st>>>(s->geo, in, (V*)s->B4, (V*)s->B2, s->diag, err);
+        // with the tri-SOR preconditioner selected, the colour-split band copies are written here too
+        // (one pass instead of a later k_split_bands re-reading the packed bands)
+        V* b4s = (s->split && s->precond == EG_PRECOND_TRISOR) ? (V*)s->split : nullptr;
+        V* b2s = b4s ? b4s + 4 * s->L.n : nullptr;
+        ProfScope ps(s, KID_SCALE, alg_bytes(s, KID_SCALE) + (b4s ? 6.0 * s->L.vsz * s->L.n : 0.0));
+        k_scale<V><<<grid, 256, 0, s->st>>>(s->geo, in, (V*)s->B4, (V*)s->B2, s->diag, err, b4s, b2s);
+        s->split_valid = b4s != nullptr;
         CK(cudaGetLastError());
     }
     int rc = state_to_host(s, err, &s->hstate->err, sizeof(int));

@@ -137,7 +137,8 @@ struct Bands7 { const double* b[7]; };
 
 template <class V>
 __global__ void __launch_bounds__(256) k_scale(Geo g, Bands7 in, V* __restrict__ B4, V* __restrict__ B2,
-                                               double* __restrict__ diag, int* __restrict__ err) {
+                                               double* __restrict__ diag, int* __restrict__ err,
+                                               V* __restrict__ B4s, V* __restrict__ B2s) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= g.nx) return;
     const int64_t k = blockIdx.y, jl = blockIdx.z, jg = g.j0 + jl;
@@ -160,6 +161,11 @@ __global__ void __launch_bounds__(256) k_scale(Geo g, Bands7 in, V* __restrict__
     }
     stv<4>(B4 + 4 * q, h4);
     stv<2>(B2 + 2 * q, h2);
+    if (B4s) {  // the colour-split copies of the red-black tri-SOR sweeps (k_split_bands' layout)
+        const int64_t qs = jl * g.row + k * g.nx + ((i + jg) & 1) * (g.nx / 2) + (i >> 1);
+        stv<4>(B4s + 4 * qs, h4);
+        stv<2>(B2s + 2 * qs, h2);
+    }
     diag[q] = c;
     if (e) atomicOr(err, e);
 }

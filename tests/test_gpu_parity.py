@@ -514,3 +514,26 @@ def test_fp64_thomas_tma_matches_tmem_kernel(prob, monkeypatch):
     s1.profile_reset()
     s1.solve(bt, tol=0.0, maxit=2, flags=egs.EG_SOLVE_PROFILE)
     assert s1.profile()["thomas_p"][1] == 2
+
+
+@pytest.mark.parametrize("mode", ["mixed", "fp64"])
+def test_trisor_split_bands_from_set_operator_bitwise(mode):
+    """With tri-SOR selected, set_operator writes the colour-split band copies in the scaling pass;
+    otherwise they are derived before the first solve (never inside the captured iteration graph).
+    Both give bitwise the same solve, graph replay or not."""
+    prob = gen.Problem(136, 20, 13, seed=23)
+    bands, b = gen.host(prob)
+    g = (prob.nx, prob.ny, prob.nz)
+    bd = torch.from_numpy(bands).cuda()
+    bt = torch.from_numpy(b).cuda()
+    s1 = egs.Solver(g, bd, mode, trisor=True)
+    s1.set_preconditioner("trisor", sweeps=3, omega=1.5)      # split copies derived at the solve
+    x1, i1, h1 = s1.solve(bt, tol=1e-8, maxit=40)
+    s2 = egs.Solver(g, 2.0 * bd, mode, trisor=True)            # another operator first
+    s2.set_preconditioner("trisor", sweeps=3, omega=1.5)
+    s2.solve(bt, tol=1e-8, maxit=40)
+    s2.set_operator(bd)                                        # split copies written by the scaling pass
+    x2, i2, h2 = s2.solve(bt, tol=1e-8, maxit=40)
+    x3, i3, h3 = s2.solve(bt, tol=1e-8, maxit=40, flags=egs.EG_SOLVE_NO_GRAPH)
+    assert i1.iters == i2.iters == i3.iters and np.array_equal(h1, h2) and np.array_equal(h1, h3)
+    assert torch.equal(x1, x2) and torch.equal(x1, x3)
