@@ -522,11 +522,9 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
         if ((rc = ensure_split<MODE>(s))) return rc;
         sp = Split<V>{b4s, b2s, b2s + 2 * s->L.n};
     }
-    const int zi = (void*)z == (void*)v.zs ? 1 : 0;
-    // the colour-split x of the fp32 TMA sweeps: ghosted, after f in the split region; row 0 pointer
+    // the colour-split x of the TMA sweeps: ghosted, after f in the split region; row 0 pointer
     V* xsv = s->split ? (V*)s->split + 7 * s->L.n + s->L.row : nullptr;
-    float* xsr = (float*)xsv;
-    (void)xsr;
+    float* xsr = (float*)xsv;  // (the fp32 kernels' view)
     for (int sw = 0; sw < s->sor_sweeps; ++sw)
         for (int colour = 0; colour < 2; ++colour) {
             bool xs_half = false;  // this half-sweep wrote the colour-split x (else the natural z)
