@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     constexpr int OFF_V = (KIND == 1 ? 2 : 1) * KS * 128;   // v after r (, p)
     constexpr int OFF_B2 = (KIND == 1 ? 3 : 2) * KS * 128;  // (U, D) after r, (p,) v
     constexpr int OFF_RH = KS * 512;                         // rhat0 after (E, W, N, S)
-    extern __shared__ __align__(128) unsigned char smraw[];
+    extern __shared__ __align__(128) unsigned char smtma[];
     __shared__ __align__(8) uint64_t fullF[MA_MAX_STAGES], emptyF[MA_MAX_STAGES];
     __shared__ __align__(8) uint64_t fullS[MA_MAX_STAGES], emptyS[MA_MAX_STAGES];
     __shared__ __align__(8) uint64_t sread[MA_MAX_CH], zready[2], zdone[2];
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     const int nch = (nz + KB - 1) / KB;
     const int NZ8 = nch * KB;
     // TMA destinations must be 128-byte aligned; the dynamic region follows the static one
-    float* stF = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    float* stF = reinterpret_cast<float*>(smtma + ((128u - (smem_u32(smtma) & 127u)) & 127u));
     float* stS = stF + (size_t)NSF * SF;
     float* ring = stS + (size_t)NSS * SF;  // [3][NZ8][130]
     const int ring_slot = NZ8 * MA_RING_W;

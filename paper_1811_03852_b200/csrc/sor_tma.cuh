@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
                                                             const __grid_constant__ SorMaps maps) {
     static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
     using V = float;
-    extern __shared__ __align__(128) unsigned char smraw[];
+    extern __shared__ __align__(128) unsigned char smtma[];
     __shared__ __align__(8) uint64_t full[SO_STAGES], empty[SO_STAGES];
     __shared__ uint32_t tm_slot;
     if (check_halt && vv.st->halt != H_RUN) return;  // uniform
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(SO_THREADS, 2) k_sor_tma(Geo g, Vecs<MODE> vv,
     const int64_t items = (int64_t)tiles * nyl;
     const int NZ8 = (nz + 7) / 8 * 8;  // levels padded to whole 8-level TMEM chunks
     const int oc = colour ^ 1;          // the other colour
-    float* stages = reinterpret_cast<float*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    float* stages = reinterpret_cast<float*>(smtma + ((128u - (smem_u32(smtma) & 127u)) & 127u));
     if (tid == 0) {
         for (int q = 0; q < SO_STAGES; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], SO_CONS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
                                                               double omega_d, int check_halt,
                                                               const __grid_constant__ SorMaps64 maps) {
     using V = double;
-    extern __shared__ __align__(128) unsigned char smraw[];
+    extern __shared__ __align__(128) unsigned char smtma[];
     __shared__ __align__(8) uint64_t full[S6_STAGES], empty[S6_STAGES];
     __shared__ uint32_t tm_slot;
     if (check_halt && vv.st->halt != H_RUN) return;  // uniform
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(S6_THREADS, 1) k_sor_tma64(Geo g, Vecs<0> vv, 
     const int64_t items = (int64_t)tiles * nyl;
     const int NZ4 = (nz + S6_KS - 1) / S6_KS * S6_KS;
     const int oc = colour ^ 1;
-    V* stages = reinterpret_cast<V*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    V* stages = reinterpret_cast<V*>(smtma + ((128u - (smem_u32(smtma) & 127u)) & 127u));
     if (tid == 0) {
         for (int q = 0; q < S6_STAGES; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], SO_CONS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -491,7 +491,7 @@ template <int KIND>
 __global__ void __launch_bounds__(T6_THREADS, 1) k_thomas_tma64(Geo g, Vecs<0> vv, double* __restrict__ zout,
                                                                  const __grid_constant__ ThomasMaps64 maps) {
     using V = double;
-    extern __shared__ __align__(128) unsigned char smraw[];
+    extern __shared__ __align__(128) unsigned char smtma[];
     __shared__ __align__(8) uint64_t full[T6_STAGES], empty[T6_STAGES];
     __shared__ uint32_t tm_slot;
     V beta = 0, omega = 0, alpha = 0;
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(T6_THREADS, 1) k_thomas_tma64(Geo g, Vecs<0> v
     const int tiles = (nx + 127) / 128;
     const int64_t items = (int64_t)tiles * nyl;
     const int NZ4 = (nz + T6_KS - 1) / T6_KS * T6_KS;
-    V* stages = reinterpret_cast<V*>(smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u));
+    V* stages = reinterpret_cast<V*>(smtma + ((128u - (smem_u32(smtma) & 127u)) & 127u));
     if (tid == 0) {
         for (int q = 0; q < T6_STAGES; ++q) { mbar_init(&full[q], 1); mbar_init(&empty[q], SO_CONS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
