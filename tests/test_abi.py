@@ -65,13 +65,15 @@ def test_workspace_bytes_and_argument_validation(egs):
     assert L.eg_workspace_bytes(ctypes.byref(g), ctypes.byref(d), egs.EG_MIXED, ctypes.byref(nb)) == 1
     d = egs._Dist(0, 640, 0, 3, None)    # 3 does not divide 8
     assert L.eg_workspace_bytes(ctypes.byref(g), ctypes.byref(d), egs.EG_MIXED, ctypes.byref(nb)) == 1
-    # EG_FEATURE_TRISOR: + colour-split (E,W,N,S), (U,D) and f, 7 working-precision values per point
+    # EG_FEATURE_TRISOR: + colour-split (E,W,N,S), (U,D), f and the sweeps' x (ghosted: + 2 rows),
+    # 8 working-precision values per point
     assert L.eg_workspace_bytes(ctypes.byref(g), None, egs.EG_MIXED, ctypes.byref(nb)) == 0
     nbt, nb0 = ctypes.c_size_t(), ctypes.c_size_t()
     assert L.eg_workspace_bytes_ex(ctypes.byref(g), None, egs.EG_MIXED, 0, ctypes.byref(nb0)) == 0
     assert nb0.value == nb.value
     assert L.eg_workspace_bytes_ex(ctypes.byref(g), None, egs.EG_MIXED, egs.EG_FEATURE_TRISOR, ctypes.byref(nbt)) == 0
-    assert 7 * 4 * n <= nbt.value - nb.value <= 7 * 4 * n + 256
+    row = g.nx * g.nz
+    assert (8 * n + 2 * row) * 4 <= nbt.value - nb.value <= (8 * n + 2 * row) * 4 + 256
     assert L.eg_workspace_bytes_ex(ctypes.byref(g), None, egs.EG_MIXED, 4, ctypes.byref(nbt)) == 1  # unknown bit
     h = ctypes.c_void_p()
     assert L.eg_solver_create(None, None, None, 1, None, 0, None, ctypes.byref(h)) == 1
