@@ -339,9 +339,21 @@ def run_ours(args, prob, ws, rank, local):
         _, tinfo_t, _ = st_.solve(b, tol=1e-4, maxit=200, out=x)
         ev1.record(stream)
         torch.cuda.synchronize(dev)
+        # algorithmic bytes of one step (every launch's, from one profiled step) against the timed rate
+        st_.profile_reset()
+        pinfo = step(egs.EG_SOLVE_PROFILE)
+        ptri = st_.profile()
+        step_bytes = sum(v[1] * v[2] for v in ptri.values())
+        tri_value = sum(i.iters for i in infos_t) / (ms_t / 1000.0)
+        tri_gbps = step_bytes / (ms_t / args.steps / 1000.0) / 1e9
         tri = {"preconditioner": "red-black tri-SOR, 3 sweeps, omega 1.5 (P:243-258)",
-               "value": sum(i.iters for i in infos_t) / (ms_t / 1000.0), "unit": "iter/s",
+               "value": tri_value, "unit": "iter/s",
                "ms_per_step": ms_t / args.steps,
+               "step_roofline": {"alg_bytes_per_step": step_bytes,
+                                 "alg_bytes_per_point_per_iteration": step_bytes / max(pinfo.iters, 1) / prob.n,
+                                 "achieved_GBps": tri_gbps, "frac": tri_gbps / peaks()[0],
+                                 "note": "algorithmic bytes of every launch of one profiled step (set_operator, "
+                                         "entry, 8 iterations, verification) over the timed step time"},
                "restarts_in_timed_region": int(sum(i.restarts for i in infos_t)),
                "note": "fixed 8 iterations per step; with this preconditioner R falls below the fp32 floor "
                        "within the step, so restarts (r recomputed in fp64) are part of the timed work",
