@@ -313,7 +313,8 @@ def test_fused_phases_fall_back_outside_their_domain(prob):
 # nx = 130 / 132 / 136: the second colour's colour-split rows start at byte 260 / 264 / 272 (fp32),
 # 520 / 528 / 544 (FP64); the TMA sweeps need a 16-byte boundary there and fall back otherwise
 TRISOR_CASES = [gen.Problem(64, 48, 10, seed=0), gen.Problem(130, 9, 70, seed=10), gen.Problem(128, 37, 13, seed=11),
-                gen.Problem(132, 7, 13, seed=21), gen.Problem(136, 7, 70, seed=22)]
+                gen.Problem(132, 7, 13, seed=21), gen.Problem(136, 7, 70, seed=22),
+                gen.Problem(64, 6, 100, seed=24)]  # nz > 72: the TMA sweeps' TMEM limit, k_sor_half runs
 
 
 @pytest.mark.parametrize("prob", TRISOR_CASES, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
