@@ -360,12 +360,12 @@ int finalize(eg_solver* s, int first, int tiles = 0) {
     Geo geo = s->geo;
     if (tiles > 0) geo.tiles = tiles;  // slots per row of the producing kernel
     if (!multi(s)) {  // one GPU: group sums and logic in one CTA
-        k_fin<MODE, WHICH><<<1, 1024, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum, first);
+        k_fin<MODE, WHICH><<<(unsigned)(geo.g_hi - geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum, first);
         CK(cudaGetLastError());
         return EG_OK;
     }
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
-    k_fin_groups<MODE, WHICH><<<1, 1024, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum);
+    k_fin_groups<MODE, WHICH><<<(unsigned)(s->geo.g_hi - s->geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum);
     CK(cudaGetLastError());
     const int gl = s->geo.g_hi - s->geo.g_lo;
     if (s->lb) {  // all-gather: rank r's block lands at gall + r * gl * NQ, as ncclAllGather places it

@@ -1227,6 +1227,59 @@ __device__ __forceinline__ void fin_groups(const Geo& g, const double* __restric
     if (lane == 0) gsum[gl * NQ + qq] = s;
 }
 
+// The same sums as fin_groups, with the chains spread over threads: one CTA of FIN_THREADS = 512
+// threads per group, thread (c, l) = (chain, lane) adds the group's slots l + 32 c + 512 m in order
+// of m (exactly lane l's chain c of fin_groups), then warp q combines the chains of quantity q with
+// fin_groups' pairwise tree and shuffle tree: bitwise the same group sums, ~16x the parallelism.
+constexpr int FIN_THREADS = 512;
+template <int NQ>
+__device__ __forceinline__ void fin_group_par(const Geo& g, const double* __restrict__ slots, uint32_t r32, int gl,
+                                              double* __restrict__ gsum) {
+    constexpr int FC = 16;
+    __shared__ double chain[NQ][FC][32];
+    const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+    const int gi = g.g_lo + gl;
+    const int64_t rb = (int64_t)gi * g.ny / g.G - g.j0, re = (int64_t)(gi + 1) * g.ny / g.G - g.j0;
+    const int64_t L = (re - rb) * g.tiles;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const double* src = slots + (int64_t)q * g.nyl * g.tiles + rb * g.tiles;
+        const bool f = (r32 >> q) & 1u;
+        double ac = 0.0;
+        for (int64_t e = lane + 32 * c; e < L; e += 32 * FC) {
+            ac += src[e];
+            if (f) ac = (double)(float)ac;
+        }
+        chain[q][c][lane] = ac;
+    }
+    __syncthreads();
+    if (c < NQ) {
+        const int q = c;
+        const bool f = (r32 >> q) & 1u;
+        double ac[FC];
+#pragma unroll
+        for (int k = 0; k < FC; ++k) ac[k] = chain[q][k][lane];
+#pragma unroll
+        for (int h = FC / 2; h > 0; h >>= 1) {
+#pragma unroll
+            for (int k = 0; k < h; ++k) {
+                ac[k] += ac[k + h];
+                if (f) ac[k] = (double)(float)ac[k];
+            }
+        }
+        double sv = ac[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sv += __shfl_down_sync(0xffffffffu, sv, o);
+            if (f) sv = (double)(float)sv;
+        }
+        if (lane == 0) {
+            gsum[gl * NQ + q] = sv;
+            __threadfence();  // visible device-wide before this CTA's arrival (k_fin's last-CTA logic)
+        }
+    }
+}
+
 template <int MODE, int WHICH>
 __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict__ gall, DevState* st,
                                           int first) {
@@ -1322,30 +1375,41 @@ __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict
 
 // single-GPU finaliser: groups + logic in one CTA (1024 threads)
 template <int MODE, int WHICH>
-__global__ void __launch_bounds__(1024) k_fin(Geo g, const double* __restrict__ slots, DevState* st,
-                                              double* __restrict__ gsum, int first) {
+__global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __restrict__ slots, DevState* st,
+                                                     double* __restrict__ gsum, int first) {
+    // grid: one CTA per reduction group; the last CTA to finish runs the logic
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
     const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
-    if (threadIdx.x == 0) { st->epoch += 1; }  // stamps the next fused phase launch
-    if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st->epoch += 1; }  // stamps the next fused phase launch
+    if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;  // uniform over the grid
     if (WHICH == W_C && st->sexit) {  // s-step exit: no sums needed
-        if (threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gsum, st, first);
+        if (blockIdx.x == 0 && threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gsum, st, first);
         return;
     }
-    fin_groups<NQ>(g, slots, r32, gsum);
+    fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
+    __shared__ int last;
     __syncthreads();
-    if (threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gsum, st, first);
+    if (threadIdx.x == 0) {
+        __threadfence();  // this group's sums before the arrival
+        last = atomicAdd(&st->fin_ctr, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        st->fin_ctr = 0;
+        fin_logic<MODE, WHICH>(g, gsum, st, first);
+    }
 }
 
-// multi-GPU: local groups -> (NCCL all-gather) -> logic
+// multi-GPU: local groups -> (NCCL all-gather) -> logic.  grid: one CTA per local group.
 template <int MODE, int WHICH>
-__global__ void __launch_bounds__(1024) k_fin_groups(Geo g, const double* __restrict__ slots,
-                                                     const DevState* st, double* __restrict__ gsum) {
+__global__ void __launch_bounds__(FIN_THREADS) k_fin_groups(Geo g, const double* __restrict__ slots,
+                                                            const DevState* st, double* __restrict__ gsum) {
     constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
     const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
     if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;
     if (WHICH == W_C && st->sexit) return;
-    fin_groups<NQ>(g, slots, r32, gsum);
+    fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
 }
 
 template <int MODE, int WHICH>
