@@ -1,5 +1,6 @@
-"""FP64 solves of a few problems, printed as hashes of x / history: run under two builds
-(EGSOLVE_LIB) to check that a change is bitwise neutral."""
+"""Solves of a few problems (argument: fp64 | mixed | fp32), printed as hashes of x, the history and
+a preconditioner application: run under two builds (EGSOLVE_LIB) to check that a change is bitwise
+neutral."""
 import hashlib
 import os
 import sys
