@@ -209,6 +209,23 @@ def test_error_paths():
     bb = b.copy(); bb[5] = np.nan
     _, info, _ = s.solve(torch.from_numpy(bb).cuda(), raise_on_error=False)
     assert info.status == 5
+    # argument validation (EG_ERR_ARG before any device work), then the handle still solves
+    bt = torch.from_numpy(b).cuda()
+    for kw in (dict(maxit=-1), dict(tol=float("nan")), dict(tol=-1.0)):
+        with pytest.raises(egs.EgError) as e:
+            s.solve(bt, **kw)
+        assert e.value.status == 1, kw
+    for args in (("trisor", 0, 1.5), ("trisor", 3, 2.0), ("trisor", 3, 0.0), ("nonsense", 3, 1.5)):
+        with pytest.raises((egs.EgError, KeyError)):
+            s.set_preconditioner(*args)
+    podd = gen.Problem(15, 8, 4, seed=4)  # nx odd: no red-black colouring
+    bo, _ = gen.host(podd)
+    so = egs.Solver((podd.nx, podd.ny, podd.nz), torch.from_numpy(bo).cuda(), "mixed")
+    with pytest.raises(egs.EgError) as e:
+        so.set_preconditioner("trisor")
+    assert e.value.status == 1
+    x, info, _ = s.solve(bt, tol=1e-6, maxit=50)
+    assert info.status == 0 and info.converged
 
 
 def test_no_horizontal_coupling_one_iteration():
