@@ -96,3 +96,21 @@ def test_device_generator_bitwise_equals_host(prob):
     gen.device(prob, bands, b)
     hb, hr = gen.host(prob)
     assert np.array_equal(bands.cpu().numpy(), hb) and np.array_equal(b.cpu().numpy(), hr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows", [(0, 5), (5, 11), (11, 17), (8, 9)])
+def test_device_generator_band_equals_host_rows(rows):
+    """A latitude band generated on the device (what each rank of bench.py does) is bitwise the
+    host generator's rows of the global problem."""
+    import torch
+    prob = gen.Problem(33, 17, 5, seed=3)
+    j0, j1 = rows
+    row = prob.nx * prob.nz
+    nloc = (j1 - j0) * row
+    bands = torch.empty((7, nloc), dtype=torch.float64, device="cuda")
+    b = torch.empty(nloc, dtype=torch.float64, device="cuda")
+    gen.device(prob, bands, b, j0, j1)
+    hb, hr = gen.host(prob)
+    assert np.array_equal(bands.cpu().numpy(), hb[:, j0 * row:j1 * row])
+    assert np.array_equal(b.cpu().numpy(), hr[j0 * row:j1 * row])
