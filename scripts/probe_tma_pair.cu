@@ -61,8 +61,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
     float* stS = stF + (size_t)NSF * SF;
     if (tid == 0) {
         // the rank-0 CTA's empty barriers count both CTAs' consumers
-        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], 2 * MA_CONS); }
-        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], 2 * MA_CONS); }
+        // one arrival per consumer warp of both CTAs (after the warp's reads, __syncwarp)
+        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], 2 * MA_CONS / 32); }
+        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], 2 * MA_CONS / 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cluster_sync();
@@ -116,7 +117,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                         b[l] = sb[2 * KS * 128 + l * 128 + col] + ud.y;
                     }
                     fence_proxy_async_smem();
-                    arrive_c(mapa_u32(smem_u32(&emptyF[slot]), 0));
+                    __syncwarp();
+                    if (lane == 0) arrive_c(mapa_u32(smem_u32(&emptyF[slot]), 0));
                     if (++slot == NSF) { slot = 0; ph ^= 1u; }
 #pragma unroll
                     for (int l = 0; l < KS; ++l)
@@ -134,7 +136,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                         a[l] = e.x + e.y + e.z + e.w + sb[KS * 512 + l * 128 + col];
                     }
                     fence_proxy_async_smem();
-                    arrive_c(mapa_u32(smem_u32(&emptyS[slot]), 0));
+                    __syncwarp();
+                    if (lane == 0) arrive_c(mapa_u32(smem_u32(&emptyS[slot]), 0));
                     if (++slot == NSS) { slot = 0; ph ^= 1u; }
 #pragma unroll
                     for (int l = 0; l < KS; ++l)
