@@ -45,7 +45,7 @@ __device__ __forceinline__ uint32_t cta_rank() {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
     k_pair(int nx, int nz, int nyl, int T, int strips, int NSF, int NSS, float* __restrict__ po, float* __restrict__ zo,
-           float* __restrict__ vo, const __grid_constant__ Maps maps) {
+           float* __restrict__ vo, const __grid_constant__ Maps maps, int pair) {
     constexpr int SF = ma_stage_floats(1), KS = MA_KS;
     extern __shared__ __align__(128) unsigned char smp[];
     __shared__ __align__(8) uint64_t fullF[MA_MAX_STAGES], emptyF[MA_MAX_STAGES];
@@ -62,12 +62,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
     if (tid == 0) {
         // the rank-0 CTA's empty barriers count both CTAs' consumers
         // one arrival per consumer warp of both CTAs (after the warp's reads, __syncwarp)
-        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], 2 * MA_CONS / 32); }
-        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], 2 * MA_CONS / 32); }
+        const int ec = (pair ? 2 : 1) * MA_CONS / 32;
+        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], ec); }
+        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], ec); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cluster_sync();
-    if ((warp == 8 || warp == 10) && rk == 0) {
+    if ((warp == 8 || warp == 10) && (rk == 0 || !pair)) {
         if (lane == 0) {
             const bool isF = warp == 8;
             const int NS = isF ? NSF : NSS;
@@ -80,9 +81,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                     const int j = ja + m;
                     if (round > 0) mbar_wait_sleep(&empty[slot], (uint32_t)((round - 1) & 1), 32);
                     const uint32_t bytes = isF ? 3u * MA_BOX_V + MA_BOX_B2 : MA_BOX_B4 + MA_BOX_V;
-                    for (uint32_t c = 0; c < 2; ++c) {  // this CTA's tile, then the peer's (adjacent columns)
-                        const uint32_t bar = mapa_u32(smem_u32(&full[slot]), c);
-                        const uint32_t dst = mapa_u32(smem_u32(st + (size_t)slot * SF), c);
+                    for (uint32_t c = 0; c < (pair ? 2u : 1u); ++c) {  // this CTA's tile (, then the peer's)
+                        const uint32_t tgt = pair ? c : rk;
+                        const uint32_t bar = mapa_u32(smem_u32(&full[slot]), tgt);
+                        const uint32_t dst = mapa_u32(smem_u32(st + (size_t)slot * SF), tgt);
                         const int ic = i0 + 128 * (int)c;
                         expect_tx_c(bar, bytes);
                         if (isF) {
@@ -118,7 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) arrive_c(mapa_u32(smem_u32(&emptyF[slot]), 0));
+                    if (lane == 0) arrive_c(mapa_u32(smem_u32(&emptyF[slot]), pair ? 0u : rk));
                     if (++slot == NSF) { slot = 0; ph ^= 1u; }
 #pragma unroll
                     for (int l = 0; l < KS; ++l)
@@ -137,7 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) arrive_c(mapa_u32(smem_u32(&emptyS[slot]), 0));
+                    if (lane == 0) arrive_c(mapa_u32(smem_u32(&emptyS[slot]), pair ? 0u : rk));
                     if (++slot == NSS) { slot = 0; ph ^= 1u; }
 #pragma unroll
                     for (int l = 0; l < KS; ++l)
@@ -167,6 +169,7 @@ int main(int argc, char** argv) {
     const int nx = 2560, ny = 1920, nz = 70, strips = 7;
     const int NSF = argc > 1 ? atoi(argv[1]) : 6;
     const int NSS = argc > 2 ? atoi(argv[2]) : 5;
+    const int pair = argc > 3 ? atoi(argv[3]) : 1;
     const int64_t n = (int64_t)nx * ny * nz;
     const int T = nx / 128;
     float *r, *p, *v, *rh, *b2, *b4, *po, *zo, *vo;
@@ -187,18 +190,18 @@ int main(int argc, char** argv) {
     const int grid = strips * T;
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
-    for (int it = 0; it < 2; ++it) k_pair<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps);
+    for (int it = 0; it < 2; ++it) k_pair<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, pair);
     cudaError_t e0 = cudaDeviceSynchronize();
     if (e0 != cudaSuccess) { printf("launch failed: %s\n", cudaGetErrorString(e0)); return 1; }
     cudaEventRecord(a);
     const int reps = 10;
-    for (int it = 0; it < reps; ++it) k_pair<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps);
+    for (int it = 0; it < reps; ++it) k_pair<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, pair);
     cudaEventRecord(b);
     cudaError_t e = cudaEventSynchronize(b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
     ms /= reps;
-    printf("pair: strips=%d grid=%d stages=%d+%d smem=%zu KB: %.3f ms  %.0f GB/s (52 B/pt)  %s\n", strips, grid, NSF, NSS,
+    printf("pair=%d: strips=%d grid=%d stages=%d+%d smem=%zu KB: %.3f ms  %.0f GB/s (52 B/pt)  %s\n", pair, strips, grid, NSF, NSS,
            smem / 1024, ms, 52.0 * n / (ms * 1e-3) / 1e9, cudaGetErrorString(e));
     return e == cudaSuccess ? 0 : 1;
 }
