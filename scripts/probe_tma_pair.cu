@@ -50,6 +50,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
     extern __shared__ __align__(128) unsigned char smp[];
     __shared__ __align__(8) uint64_t fullF[MA_MAX_STAGES], emptyF[MA_MAX_STAGES];
     __shared__ __align__(8) uint64_t fullS[MA_MAX_STAGES], emptyS[MA_MAX_STAGES];
+    __shared__ __align__(8) uint64_t pemptyF[MA_MAX_STAGES], pemptyS[MA_MAX_STAGES];  // pair = 2: the peer's relay
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rk = cta_rank();
     const int t = blockIdx.x % T, strip = blockIdx.x / T;
@@ -62,24 +63,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
     if (tid == 0) {
         // the rank-0 CTA's empty barriers count both CTAs' consumers
         // one arrival per consumer warp of both CTAs (after the warp's reads, __syncwarp)
-        const int ec = (pair ? 2 : 1) * MA_CONS / 32;
-        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], ec); }
-        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], ec); }
+        const int ec = (pair == 1 ? 2 : 1) * MA_CONS / 32;
+        for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], ec); mbar_init(&pemptyF[s], 1); }
+        for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], ec); mbar_init(&pemptyS[s], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cluster_sync();
-    if ((warp == 8 || warp == 10) && (rk == 0 || !pair)) {
+    if ((warp == 8 || warp == 10) && pair == 2 && rk == 1) {  // relay: local empty -> the producer CTA
+        if (lane == 0) {
+            const bool isF = warp == 8;
+            const int NS = isF ? NSF : NSS;
+            uint64_t* empty = isF ? emptyF : emptyS;
+            uint64_t* pempty = isF ? pemptyF : pemptyS;
+            int slot = 0, round = 0;
+            for (int m = 0; m < L; ++m)
+                for (int k0 = 0; k0 < NZ8; k0 += KS) {
+                    mbar_wait_sleep(&empty[slot], (uint32_t)(round & 1), 32);
+                    arrive_c(mapa_u32(smem_u32(&pempty[slot]), 0));
+                    if (++slot == NS) { slot = 0; ++round; }
+                }
+        }
+    } else if ((warp == 8 || warp == 10) && (rk == 0 || !pair)) {
         if (lane == 0) {
             const bool isF = warp == 8;
             const int NS = isF ? NSF : NSS;
             uint64_t* full = isF ? fullF : fullS;
             uint64_t* empty = isF ? emptyF : emptyS;
+            uint64_t* pempty = isF ? pemptyF : pemptyS;
             float* st = isF ? stF : stS;
             int slot = 0, round = 0;
             for (int m = 0; m < L; ++m)
                 for (int k0 = 0; k0 < NZ8; k0 += KS) {
                     const int j = ja + m;
                     if (round > 0) mbar_wait_sleep(&empty[slot], (uint32_t)((round - 1) & 1), 32);
+                    if (round > 0 && pair == 2) mbar_wait_sleep(&pempty[slot], (uint32_t)((round - 1) & 1), 32);
                     const uint32_t bytes = isF ? 3u * MA_BOX_V + MA_BOX_B2 : MA_BOX_B4 + MA_BOX_V;
                     for (uint32_t c = 0; c < (pair ? 2u : 1u); ++c) {  // this CTA's tile (, then the peer's)
                         const uint32_t tgt = pair ? c : rk;
@@ -120,7 +137,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) arrive_c(mapa_u32(smem_u32(&emptyF[slot]), pair ? 0u : rk));
+                    if (lane == 0) {
+                        if (pair == 2) mbar_arrive(&emptyF[slot]);  // CTA-local; the relay forwards it
+                        else arrive_c(mapa_u32(smem_u32(&emptyF[slot]), pair ? 0u : rk));
+                    }
                     if (++slot == NSF) { slot = 0; ph ^= 1u; }
 #pragma unroll
                     for (int l = 0; l < KS; ++l)
@@ -139,7 +159,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) arrive_c(mapa_u32(smem_u32(&emptyS[slot]), pair ? 0u : rk));
+                    if (lane == 0) {
+                        if (pair == 2) mbar_arrive(&emptyS[slot]);
+                        else arrive_c(mapa_u32(smem_u32(&emptyS[slot]), pair ? 0u : rk));
+                    }
                     if (++slot == NSS) { slot = 0; ph ^= 1u; }
 #pragma unroll
                     for (int l = 0; l < KS; ++l)
