@@ -29,10 +29,13 @@ __device__ __forceinline__ void tma3_c(uint32_t dst, const CUtensorMap* map, int
         : "memory");
 }
 __device__ __forceinline__ void expect_tx_c(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void arrive_c(uint32_t bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void arrive_c_relaxed(uint32_t bar) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -69,7 +72,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cluster_sync();
-    if ((warp == 8 || warp == 10) && pair == 2 && rk == 1) {  // relay: local empty -> the producer CTA
+    if ((warp == 8 || warp == 10) && pair >= 2 && rk == 1) {  // relay: local empty -> the producer CTA
         if (lane == 0) {
             const bool isF = warp == 8;
             const int NS = isF ? NSF : NSS;
@@ -79,7 +82,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
             for (int m = 0; m < L; ++m)
                 for (int k0 = 0; k0 < NZ8; k0 += KS) {
                     mbar_wait_sleep(&empty[slot], (uint32_t)(round & 1), 32);
-                    arrive_c(mapa_u32(smem_u32(&pempty[slot]), 0));
+                    if (pair == 3) arrive_c_relaxed(mapa_u32(smem_u32(&pempty[slot]), 0));
+                    else arrive_c(mapa_u32(smem_u32(&pempty[slot]), 0));
                     if (++slot == NS) { slot = 0; ++round; }
                 }
         }
@@ -96,7 +100,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                 for (int k0 = 0; k0 < NZ8; k0 += KS) {
                     const int j = ja + m;
                     if (round > 0) mbar_wait_sleep(&empty[slot], (uint32_t)((round - 1) & 1), 32);
-                    if (round > 0 && pair == 2) mbar_wait_sleep(&pempty[slot], (uint32_t)((round - 1) & 1), 32);
+                    if (round > 0 && pair >= 2) mbar_wait_sleep(&pempty[slot], (uint32_t)((round - 1) & 1), 32);
                     const uint32_t bytes = isF ? 3u * MA_BOX_V + MA_BOX_B2 : MA_BOX_B4 + MA_BOX_V;
                     for (uint32_t c = 0; c < (pair ? 2u : 1u); ++c) {  // this CTA's tile (, then the peer's)
                         const uint32_t tgt = pair ? c : rk;
@@ -138,7 +142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        if (pair == 2) mbar_arrive(&emptyF[slot]);  // CTA-local; the relay forwards it
+                        if (pair >= 2) mbar_arrive(&emptyF[slot]);  // CTA-local; the relay forwards it
                         else arrive_c(mapa_u32(smem_u32(&emptyF[slot]), pair ? 0u : rk));
                     }
                     if (++slot == NSF) { slot = 0; ph ^= 1u; }
@@ -160,7 +164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MA_THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        if (pair == 2) mbar_arrive(&emptyS[slot]);
+                        if (pair >= 2) mbar_arrive(&emptyS[slot]);
                         else arrive_c(mapa_u32(smem_u32(&emptyS[slot]), pair ? 0u : rk));
                     }
                     if (++slot == NSS) { slot = 0; ph ^= 1u; }
@@ -211,6 +215,20 @@ int main(int argc, char** argv) {
     const size_t smem = (size_t)(NSF + NSS) * ma_stage_bytes(1) + 112 * 1024 + 128;  // + the phase kernels' z ring
     cudaFuncSetAttribute(k_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = strips * T;
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(MA_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at;
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = 2; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        int nclu = 0;
+        cudaError_t eo = cudaOccupancyMaxActiveClusters(&nclu, (void*)k_pair, &cfg);
+        printf("max active 2-CTA clusters: %d (%s); grid needs %d\n", nclu, cudaGetErrorString(eo), grid / 2);
+    }
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     for (int it = 0; it < 2; ++it) k_pair<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, pair);
