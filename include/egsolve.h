@@ -91,6 +91,13 @@ typedef struct {
     int32_t restart_every;  /* mandatory restart period (P:553-557, 150 in the UM); <= 0 off */
     uint32_t flags;         /* EG_SOLVE_*                                                    */
     int32_t check_every;    /* iterations between host polls of the device flags; 0 = auto   */
+    const double* rhat0;    /* NULL (default): the shadow residual of BiCGStab is rhat0 = r0    */
+                            /* (reading A-1).  Else a DEVICE fp64 array of the local rows, used */
+                            /* (rounded to the working precision) as rhat0 at the FIRST start   */
+                            /* only; restarts set rhat0 = r (A-11).  If rho = rhat0 . r0 fails  */
+                            /* the breakdown test (A-12: 0, non-finite, or |rho| < eps_V        */
+                            /* ||rhat0|| ||r0||) the solve restarts at once with rhat0 = r0.    */
+                            /* (BiCGStab leaves rhat0 free; used to inject breakdowns in tests.) */
 } eg_solve_params;
 
 typedef struct {

@@ -23,12 +23,14 @@ FP64, MIXED, FP32 = 0, 1, 2
 MODES = {"fp64": FP64, "mixed": MIXED, "fp32": FP32}
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SINGULAR_DIAG", 3: "ERR_DEGENERATE_RHS",
           4: "ERR_BREAKDOWN", 5: "ERR_NONFINITE", 6: "ERR_NOMEM"}
+STATUS_CODES = {v: k for k, v in STATUS.items()}
 
 
 class _Params(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int32),
                 ("restart_every", ctypes.c_int32), ("precond_scale", ctypes.c_double),
-                ("sor_sweeps", ctypes.c_int32), ("sor_omega", ctypes.c_double)]
+                ("sor_sweeps", ctypes.c_int32), ("sor_omega", ctypes.c_double),
+                ("shadow", ctypes.POINTER(ctypes.c_double))]
 
 
 class _Info(ctypes.Structure):
@@ -168,13 +170,15 @@ def dot(grid, mode, a, b) -> float:
 
 
 def solve(grid, mode, ahat6, diag, b, x0=None, tol=1e-4, maxit=200, restart_every=150,
-          precond_scale=1.0, raise_on_error=False, sor_sweeps=0, sor_omega=1.5):
-    """BiCGStab (see oracle.h).  Returns (x, hist[: iters+1], Info)."""
+          precond_scale=1.0, raise_on_error=False, sor_sweeps=0, sor_omega=1.5, rhat0=None):
+    """BiCGStab (see oracle.h).  rhat0: optional shadow residual of the first start (default r0).
+    Returns (x, hist[: iters+1], Info)."""
     nx, ny, nz = grid
     n = nx * ny * nz
     x = np.empty(n, np.float64)
     hist = np.full(maxit + 1, np.nan)
-    prm = _Params(tol, maxit, restart_every, precond_scale, sor_sweeps, sor_omega)
+    sh = None if rhat0 is None else np.ascontiguousarray(rhat0, np.float64)
+    prm = _Params(tol, maxit, restart_every, precond_scale, sor_sweeps, sor_omega, _dp(sh))
     info = _Info()
     rc = lib().oracle_solve(nx, ny, nz, _mode(mode), _dp(np.ascontiguousarray(ahat6)), _dp(diag),
                             _dp(np.ascontiguousarray(b, np.float64)),

@@ -266,6 +266,7 @@ int oracle_solve(int64_t nx, int64_t ny, int64_t nz, int mode, const double* aha
     int last_start = 0;     /* i at the last (re)start, for the mandatory restart (A-11) */
     int bd_at = -1;         /* completed-iteration count at the last breakdown (A-12) */
     int first = 1;
+    int use_shadow = prm->shadow != 0;  /* the caller's rhat0 at the first start only */
     double rho = 0, alpha = 0, omega = 1, beta = 0, rh_norm = 0;
     int fresh = 1;
 
@@ -280,13 +281,22 @@ start:
         if (rt < tol) { inf.converged = 1; goto done; }
         if (i >= maxit) goto done;
     }
-    for (int64_t q = 0; q < n; ++q) { r[q] = rv(mode, r64[q]); rh[q] = r[q]; }
+    for (int64_t q = 0; q < n; ++q) {
+        r[q] = rv(mode, r64[q]);
+        rh[q] = use_shadow ? rv(mode, prm->shadow[q]) : r[q];   /* rhat0 = r0 (A-1) unless given */
+    }
+    use_shadow = 0;
     rho = oracle_dot(nx, ny, nz, mode, rh, r);
     rh_norm = sqrt(oracle_dot(nx, ny, nz, mode, rh, rh));
     beta = 0.0;
     omega = 1.0;
     fresh = 1;              /* p = v = 0, so p_1 = r (A-11) */
     last_start = i;
+    {   /* the breakdown test of rho (A-12) applies at a (re)start too: r orthogonal to rhat0 */
+        const double rr0 = oracle_dot(nx, ny, nz, mode, r, r);
+        if (rho == 0.0 || !isfinite(rho) || !isfinite(rh_norm) || fabs(rho) < eps_v * rh_norm * sqrt(rr0))
+            goto breakdown;
+    }
 
     while (i < maxit) {
         const int it = i + 1;

@@ -96,6 +96,8 @@ typedef struct {
     double precond_scale;  /* test hook: M^-1 -> precond_scale * T^-1 (A-3); 1 */
     int32_t sor_sweeps;    /* 0: M^-1 = T^-1 (hot path, A-3); > 0: tri-SOR with this many sweeps */
     double sor_omega;      /* tri-SOR over-relaxation (1.5 in the UM) */
+    const double* shadow;  /* NULL: rhat0 = r0 (reading A-1).  Else rhat0 = round_V(shadow) at the
+                              FIRST start only (BiCGStab leaves rhat0 free; restarts use r, A-11) */
 } oracle_params;
 
 typedef struct {
@@ -105,7 +107,10 @@ typedef struct {
 
 /* Right-("post-")preconditioned BiCGStab on Ahat x = bhat with M^-1 = T^-1, following the
  * step-by-step reading in DESIGN.md §Oracle algorithm, P:230-288, P:337-348,
- * P:537-557.  b, x0 (may be NULL = 0) and x are binary64 arrays of n.  hist has >= maxit+1
+ * P:537-557.  At every (re)start, rho = rhat0 . r is put to the same breakdown test as after an
+ * iteration (A-12: 0, non-finite, or |rho| < eps_V ||rhat0|| ||r||, "scalar weights ... close to or
+ * equal to zero"); a breakdown there restarts (with rhat0 = r) like any other.
+ * b, x0 (may be NULL = 0) and x are binary64 arrays of n.  hist has >= maxit+1
  * entries: hist[0] = true relative residual of x0, hist[i] = R after iteration i.
  * Returns an OR_* status (also in info->status). */
 int oracle_solve(int64_t nx, int64_t ny, int64_t nz, int mode, const double* ahat6,

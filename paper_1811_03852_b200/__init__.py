@@ -50,7 +50,7 @@ class _Dist(ctypes.Structure):
 class _Params(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int32),
                 ("restart_every", ctypes.c_int32), ("flags", ctypes.c_uint32),
-                ("check_every", ctypes.c_int32)]
+                ("check_every", ctypes.c_int32), ("rhat0", ctypes.c_void_p)]
 
 
 class _Info(ctypes.Structure):
@@ -267,25 +267,29 @@ class Solver:
         return z
 
     def solve(self, b, x0=None, tol=1e-4, maxit=200, restart_every=150, flags=0, check_every=0,
-              out=None, raise_on_error=True):
+              out=None, raise_on_error=True, history=True, rhat0=None):
         """Solve; b / x0 / out may be CUDA tensors or (pinned) host tensors / numpy arrays (fp64).
-        Returns (x, SolveInfo, history[: iters+1] numpy)."""
+        history=False skips the residual history (no host array of maxit + 1 doubles; returned as
+        None).  rhat0: optional fp64 CUDA tensor, the shadow residual of the first start
+        (eg_solve_params.rhat0; default r0).  Returns (x, SolveInfo, history[: iters+1] numpy)."""
         import torch
         if out is None:
             if isinstance(b, np.ndarray):
                 out = np.empty(self.n_local, np.float64)
             else:
                 out = torch.empty(self.n_local, dtype=torch.float64, device=b.device)
-        hist = np.full(maxit + 1, np.nan)
-        prm = _Params(float(tol), int(maxit), int(restart_every), int(flags), int(check_every))
+        if rhat0 is not None:
+            assert rhat0.dtype == torch.float64 and rhat0.numel() == self.n_local  # device memory: checked by eg_solve
+        hist = np.full(int(maxit) + 1, np.nan) if history else None
+        prm = _Params(float(tol), int(maxit), int(restart_every), int(flags), int(check_every), _ptr(rhat0))
         info = _Info()
         rc = lib().eg_solve(self._h, _ptr(b), _ptr(x0), ctypes.byref(prm), _ptr(out),
-                            ctypes.c_void_p(hist.ctypes.data), ctypes.byref(info))
+                            _ptr(hist), ctypes.byref(info))
         inf = SolveInfo(info.iters, bool(info.converged), info.restarts, info.breakdowns,
                         info.status, info.final_R, info.true_R)
         if rc and raise_on_error:
             self._check(rc, "eg_solve")
-        return out, inf, hist[: inf.iters + 1]
+        return out, inf, (hist[: inf.iters + 1] if history else None)
 
     def solve_batch(self, bs, xs, bands=None, tol=1e-4, maxit=200, restart_every=150, flags=0,
                     check_every=0, raise_on_error=True):
@@ -300,7 +304,7 @@ class Solver:
         pbands = None
         if bands is not None:
             pbands = (ctypes.c_void_p * 7)(*[bands[d].data_ptr() for d in range(7)])
-        prm = _Params(float(tol), int(maxit), int(restart_every), int(flags), int(check_every))
+        prm = _Params(float(tol), int(maxit), int(restart_every), int(flags), int(check_every), None)
         infos = (_Info * max(n, 1))()
         done = ctypes.c_int()
         rc = lib().eg_solve_batch(self._h, n, pb, px, pbands, ctypes.byref(prm), None, infos, ctypes.byref(done))

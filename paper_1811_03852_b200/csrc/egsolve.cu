@@ -107,6 +107,7 @@ struct LoopGroup {
     std::vector<const unsigned char*> first, last;  // posted edge rows
     std::vector<const double*> gsum;                // posted group sums
 };
+constexpr int kMaxIt = 1 << 26;  // epochs (8 per iteration at most) stay far below 2^31
 constexpr char kLoopMagic[8] = {'E', 'G', 'L', 'O', 'O', 'P', 'B', 'K'};
 
 // The fused phase kernels need every CTA of a launch resident (their CTAs wait on each other's
@@ -114,7 +115,10 @@ constexpr char kLoopMagic[8] = {'E', 'G', 'L', 'O', 'O', 'P', 'B', 'K'};
 // each end up partly resident and wait forever, so solves that use them are serialised here
 // (eg_solve is blocking: every kernel of a solve has finished when the lock is released).
 // Loopback ranks share one stream already and meet at host barriers inside a solve: not locked.
-std::recursive_mutex g_fused_solve_mu;
+// One lock per device: solves on different GPUs never compete for SMs (and NCCL ranks driven as
+// threads of one process must not block each other).
+constexpr int kMaxDevices = 64;
+std::recursive_mutex g_fused_solve_mu[kMaxDevices];
 
 // all n ranks arrive or the wait times out (a rank that failed never comes): false = broken group
 bool lb_barrier(LoopGroup* G) {
@@ -166,7 +170,8 @@ struct eg_solver {
     bool sor_tma64 = false; // later tri-SOR sweeps on k_sor_tma64 (FP64, colour-split copies)
     int nsm = 148;
     size_t smem_march = 0;
-    int epoch_base = 1;         // first epoch of the next solve (flags are never reset)
+    int64_t epoch_base = 1;     // first epoch of the next solve (flags are reset before 2^30)
+    int device = 0;             // the CUDA device the handle was created on
     int precond = EG_PRECOND_TRIDIAG;  // NEXT-1: EG_PRECOND_TRISOR selects red-black tri-SOR
     void* split = nullptr;             // colour-split B4 | B2 | f for tri-SOR (NULL: not available)
     double* batch = nullptr;           // eg_solve_batch staging: b[2] | x[2] (NULL: not available)
@@ -364,7 +369,7 @@ int finalize(eg_solver* s, int first, int tiles = 0) {
         CK(cudaGetLastError());
         return EG_OK;
     }
-    constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
+    constexpr int NQ = fin_nq(WHICH);
     k_fin_groups<MODE, WHICH><<<(unsigned)(s->geo.g_hi - s->geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum);
     CK(cudaGetLastError());
     const int gl = s->geo.g_hi - s->geo.g_lo;
@@ -678,7 +683,7 @@ int iteration(eg_solver* s, void* x_it) {
 
 // start / restart / verification (rows a2, a11)
 template <int MODE>
-int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero) {
+int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero, const double* shadow = nullptr) {
     using X = typename Prec<MODE>::X;
     Vecs<MODE> v = vecs<MODE>(s, x_it);
     int rc;
@@ -697,7 +702,13 @@ int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero) {
         else k_start<MODE, false, false><<<gr, RW, 0, s->st>>>(s->geo, v, b);
         CK(cudaGetLastError());
     }
-    return finalize<MODE, W_START>(s, entry);
+    if ((rc = finalize<MODE, W_START>(s, entry))) return rc;
+    if (shadow) {  // the caller's rhat0 replaces rhat0 = r0 (the first start only; restarts use r, A-11)
+        ProfScope ps(s, KID_START, (8.0 + 2.0 * s->L.vsz) * s->L.n);
+        k_shadow<MODE><<<gr, RW, 0, s->st>>>(s->geo, v, shadow);
+        CK(cudaGetLastError());
+    }
+    return shadow ? finalize<MODE, W_SHADOW>(s, 0) : EG_OK;
 }
 
 // true residual of the current x only, r / rhat0 untouched (A-6 verification, final true_R)
@@ -809,16 +820,18 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     h->xzero = x0 == nullptr ? 1 : 0;  // entry from x = 0 does not store x (the first update starts from 0)
     // ready flags are stamped with epochs that only ever grow: reserve this solve's range
     // (at most ~5 finalisers per iteration) and wrap around with a flag reset well before overflow
-    if (s->epoch_base > (1 << 30)) {
+    // (eg_solve sets epoch_base past the last epoch used; the reservation covers error exits)
+    const int64_t reserve = 8 * ((int64_t)prm->maxit + 4);
+    if (s->epoch_base + reserve > ((int64_t)1 << 30)) {
         CK(cudaMemsetAsync(s->ready_flags, 0, (size_t)s->L.nyl * s->L.tiles * sizeof(int), s->st));
         s->epoch_base = 1;
     }
-    h->epoch = s->epoch_base;
-    s->epoch_base += 8 * (prm->maxit + 4);
+    h->epoch = (int)s->epoch_base;
+    s->epoch_base += reserve;
     k_copy_words<<<1, 256, 0, s->st>>>((const uint32_t*)s->hstate_dev, (uint32_t*)s->dstate, (int)(sizeof(DevState) / 4));
     CK(cudaGetLastError());
 
-    if ((rc = start<MODE>(s, x_it, bdev, 1, x0 == nullptr))) return rc;
+    if ((rc = start<MODE>(s, x_it, bdev, 1, x0 == nullptr, prm->rhat0))) return rc;
     if ((rc = read_state(s))) return rc;
     if (h->halt == H_DEGENERATE) rc = EG_ERR_DEGENERATE_RHS;
     else if (h->halt == H_NONFINITE) rc = EG_ERR_NONFINITE;
@@ -1236,6 +1249,7 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
     s->grid = *grid;
     s->mode = prec;
     s->st = (cudaStream_t)stream;
+    cudaGetDevice(&s->device);
     if (!valid_dist(grid, dist, &s->j_begin, &s->j_end, &s->rank, &s->nranks)) {
         delete s;
         return EG_ERR_ARG;
@@ -1517,11 +1531,16 @@ int eg_solve(eg_solver* s, const double* b, const double* x0, const eg_solve_par
              double* history, eg_solve_info* info) {
     if (!s || !b || !x || !params || params->maxit < 0 || !(params->tol >= 0.0))
         return s ? fail(s, EG_ERR_ARG, "bad solve arguments") : EG_ERR_ARG;
-    std::unique_lock<std::recursive_mutex> lk(g_fused_solve_mu, std::defer_lock);
+    if (params->maxit > kMaxIt) return fail(s, EG_ERR_ARG, "maxit > %d", kMaxIt);
+    if (params->rhat0 && !is_device_ptr(params->rhat0)) return fail(s, EG_ERR_ARG, "rhat0 must be device memory");
+    std::unique_lock<std::recursive_mutex> lk(g_fused_solve_mu[s->device % kMaxDevices], std::defer_lock);
     if (s->use_march && !s->lb) lk.lock();
     int rc = s->mode == EG_FP64 ? solve_impl<0>(s, b, x0, params, x, history, info)
            : s->mode == EG_MIXED ? solve_impl<1>(s, b, x0, params, x, history, info)
                                  : solve_impl<2>(s, b, x0, params, x, history, info);
+    // every finaliser launch bumps the epoch, including launches of a replayed chunk past a halt: the
+    // next solve starts past the last epoch this one used (the host mirror is read after the last one)
+    s->epoch_base = std::max<int64_t>(s->epoch_base, (int64_t)s->hstate->epoch + 1);
     if (rc != EG_OK && info) info->status = rc;
     return rc;
 }
@@ -1535,7 +1554,8 @@ int eg_solve_batch(eg_solver* s, int count, const double* const* b, double* cons
     for (int k = 0; k < count; ++k)
         if (!b[k] || !x[k]) return fail(s, EG_ERR_ARG, "NULL b / x in the batch");
     if (!s->batch) return fail(s, EG_ERR_WORKSPACE, "eg_solve_batch needs an EG_FEATURE_BATCH workspace");
-    std::unique_lock<std::recursive_mutex> lk(g_fused_solve_mu, std::defer_lock);  // see g_fused_solve_mu
+    if (params->maxit > kMaxIt) return fail(s, EG_ERR_ARG, "maxit > %d", kMaxIt);
+    std::unique_lock<std::recursive_mutex> lk(g_fused_solve_mu[s->device % kMaxDevices], std::defer_lock);
     if (s->use_march && !s->lb) lk.lock();
     if (!s->cin) {
         CK(cudaStreamCreateWithFlags(&s->cin, cudaStreamNonBlocking));

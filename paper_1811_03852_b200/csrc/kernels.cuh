@@ -1172,7 +1172,23 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
 // Finalisers.  fin_groups: warp w sums quantity (w % NQ) of local group (w / NQ): lane l sums the
 // group's (row, tile) slots l, l+32, l+64, ... in 16 fixed chains, then a fixed shuffle tree.
 // fin_logic (thread 0): groups in order -> totals -> BiCGStab scalars and control flags.
-enum Which { W_START = 0, W_A = 1, W_B = 2, W_C = 3, W_VERIFY = 4 };
+enum Which { W_START = 0, W_A = 1, W_B = 2, W_C = 3, W_VERIFY = 4, W_SHADOW = 5 };
+// quantities per slot row of each finaliser: A sigma | B t.s, t.t, s.s | C rhat0.r, r.r |
+// START / VERIFY ||bhat||^2, ||res||^2 (fp64), r.r | SHADOW rhat0.r, rhat0.rhat0
+__host__ __device__ constexpr int fin_nq(int which) {
+    return which == W_A ? 1 : (which == W_C || which == W_SHADOW) ? 2 : 3;
+}
+// FP32 mode: which of them are binary32 sums (bit q); the true residual stays fp64
+template <int MODE>
+__host__ __device__ constexpr uint32_t fin_r32(int which) {
+    return MODE != 2 ? 0x0u : (which == W_START || which == W_VERIFY) ? 0x5u : which == W_SHADOW ? 0x3u : 0x7u;
+}
+
+// breakdown test of rho at a (re)start and after an iteration (A-12): exactly 0, non-finite, or
+// |rho| < eps_V ||rhat0|| ||r|| ("scalar weights ... close to or equal to zero")
+__device__ __forceinline__ bool rho_breakdown(double rho, double rh_norm, double rr, double eps) {
+    return rho == 0.0 || !isfinite(rho) || fabs(rho) < eps * rh_norm * sqrt(rr);
+}
 
 template <int NQ>
 __device__ __forceinline__ void fin_groups(const Geo& g, const double* __restrict__ slots, uint32_t r32,
@@ -1283,8 +1299,8 @@ __device__ __forceinline__ void fin_group_par(const Geo& g, const double* __rest
 template <int MODE, int WHICH>
 __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict__ gall, DevState* st,
                                           int first) {
-    constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
-    const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
+    constexpr int NQ = fin_nq(WHICH);
+    const uint32_t r32 = fin_r32<MODE>(WHICH);
     using V = typename Prec<MODE>::V;
     double tot[NQ];
 #pragma unroll
@@ -1314,8 +1330,9 @@ __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict
         if (!isfinite(rt)) { st->halt = H_NONFINITE; return; }
         st->true_R = rt;
         if (first) { st->hist[0] = rt; st->final_R = rt; }
-        st->rho = tot[2];
+        st->rho = tot[2];  // rhat0 = r (A-1, A-11); eg_solve's rhat0 replaces it next (W_SHADOW)
         st->rh_norm = sqrt(tot[2]);
+        st->rr0 = tot[2];
         st->beta = 0.0; st->beta_v = 0.0;
         st->omega = 1.0; st->omega_v = 1.0;
         st->fresh = 1;
@@ -1323,10 +1340,17 @@ __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict
         st->last_start = st->iter;
         if (rt < st->tol) st->halt = H_START_CONVERGED;
         else if (st->iter >= st->maxit) st->halt = H_START_MAXIT;
+        else if (rho_breakdown(st->rho, st->rh_norm, tot[2], st->eps_v)) st->halt = H_BD_ABORT;
         else st->halt = H_RUN;
         return;
     }
     if (st->halt != H_RUN) return;
+    if (WHICH == W_SHADOW) {  // a caller-given rhat0 at the first start: rho = rhat0 . r
+        st->rho = tot[0];
+        st->rh_norm = sqrt(tot[1]);
+        if (rho_breakdown(st->rho, st->rh_norm, st->rr0, st->eps_v) || !isfinite(st->rh_norm)) st->halt = H_BD_ABORT;
+        return;
+    }
     if (WHICH == W_A) {
         const double sigma = tot[0];
         if (sigma == 0.0 || !isfinite(sigma)) { st->halt = H_BD_ABORT; return; }
@@ -1358,8 +1382,7 @@ __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict
         st->final_R = R;
         if (!isfinite(R)) { st->halt = H_NONFINITE; return; }
         if (R < st->tol) { st->halt = H_CONVERGED; return; }
-        if (rho_n == 0.0 || !isfinite(rho_n) || fabs(rho_n) < st->eps_v * st->rh_norm * sqrt(rr) ||
-            st->omega == 0.0) {
+        if (rho_breakdown(rho_n, st->rh_norm, rr, st->eps_v) || st->omega == 0.0) {
             st->halt = H_BD_END;
             return;
         }
@@ -1378,15 +1401,16 @@ template <int MODE, int WHICH>
 __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __restrict__ slots, DevState* st,
                                                      double* __restrict__ gsum, int first) {
     // grid: one CTA per reduction group; the last CTA to finish runs the logic
-    constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
-    const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
+    constexpr int NQ = fin_nq(WHICH);
+    const uint32_t r32 = fin_r32<MODE>(WHICH);
     if (blockIdx.x == 0 && threadIdx.x == 0) { st->epoch += 1; }  // stamps the next fused phase launch
-    if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;  // uniform over the grid
-    if (WHICH == W_C && st->sexit) {  // s-step exit: no sums needed
-        if (blockIdx.x == 0 && threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gsum, st, first);
-        return;
-    }
-    fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
+    // halt / sexit are read once, before this CTA's arrival: only the last CTA to arrive (after every
+    // CTA has read them) writes the state, so every CTA takes the same branch
+    const int halt0 = *(volatile const int*)&st->halt;
+    const int sexit0 = *(volatile const int*)&st->sexit;
+    if (WHICH != W_START && WHICH != W_VERIFY && halt0 != H_RUN) return;  // (then nobody writes)
+    // s-step exit (W_C): no sums needed, but every CTA still arrives so that the counter is reset
+    if (!(WHICH == W_C && sexit0)) fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
     __shared__ int last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1405,8 +1429,8 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __rest
 template <int MODE, int WHICH>
 __global__ void __launch_bounds__(FIN_THREADS) k_fin_groups(Geo g, const double* __restrict__ slots,
                                                             const DevState* st, double* __restrict__ gsum) {
-    constexpr int NQ = WHICH == W_A ? 1 : (WHICH == W_C ? 2 : 3);
-    const uint32_t r32 = MODE == 2 ? (WHICH == W_START || WHICH == W_VERIFY ? 0x5u : 0x7u) : 0x0u;
+    constexpr int NQ = fin_nq(WHICH);
+    const uint32_t r32 = fin_r32<MODE>(WHICH);
     if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;
     if (WHICH == W_C && st->sexit) return;
     fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
@@ -1419,6 +1443,27 @@ __global__ void k_fin_logic(Geo g, const double* __restrict__ gall, DevState* st
 }
 
 // ---------------------------------------------------------------------------------------------
+// A caller-given shadow residual at the first start (eg_solve_params.rhat0; BiCGStab leaves r̂0 free,
+// A-1 takes r̂0 = r0 by default): rhat0 = round_V(sh); partials rhat0 . r (S), rhat0 . rhat0 (S).
+// Rare (a test / fault-injection hook), so a plain column walk.  grid (tiles, nyl), RW.
+template <int MODE>
+__global__ void __launch_bounds__(RW) k_shadow(Geo g, Vecs<MODE> vv, const double* __restrict__ sh) {
+    using V = typename Prec<MODE>::V;
+    double acc[2] = {0.0, 0.0};
+    const int i = blockIdx.x * RW + threadIdx.x;
+    if (i < g.nx) {
+        const int64_t rb = (int64_t)blockIdx.y * g.row + i;
+        for (int k = 0; k < (int)g.nz; ++k) {
+            const int64_t q = rb + (int64_t)k * g.nx;
+            const V h = (V)sh[q];
+            vv.rh[q] = h;
+            acc_dot<MODE>(acc[0], h, vv.r[q]);
+            acc_dot<MODE>(acc[1], h, h);
+        }
+    }
+    write_slots<2>(g, vv.slots, acc, fin_r32<MODE>(W_SHADOW));
+}
+
 template <class A, class B>
 __global__ void k_convert(const A* __restrict__ src, B* __restrict__ dst, int64_t n) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;

@@ -1,5 +1,5 @@
-"""Per-rank work of the latitude-band decomposition, measured on one GPU: a C5 band of ny/P rows
-(2560 x 1920/P x 70) timed as a whole problem (fixed 8 iterations, CUDA events), for the fused
+"""Per-rank work of the latitude-band decomposition, measured on one GPU: a band of ny/P rows of a
+BASELINE config (default C5: 2560 x 1920/P x 70; `--config C4`) timed as a whole problem (fixed 8 iterations, CUDA events), for the fused
 schedule with each strip count and for the 5-kernel schedule.  The halo exchange and the
 all-gather are not included (they need P GPUs)."""
 import os
@@ -12,15 +12,21 @@ import torch  # noqa: E402
 import gen  # noqa: E402
 import paper_1811_03852_b200 as egs  # noqa: E402
 
-base = gen.CONFIGS["C5"]
-for P in [int(a) for a in (sys.argv[1:] or ["1", "2", "4", "8"])]:
+args = sys.argv[1:]
+cfg = "C5"
+if args and args[0] == "--config":
+    cfg, args = args[1], args[2:]
+quick = "--quick" in args          # default schedules only (no strip sweep)
+args = [a for a in args if a != "--quick"]
+base = gen.CONFIGS[cfg]
+for P in [int(a) for a in (args or ["1", "2", "4", "8"])]:
     prob = base.with_(ny=base.ny // P)
     bands = torch.empty((7, prob.n), dtype=torch.float64, device="cuda")
     b = torch.empty(prob.n, dtype=torch.float64, device="cuda")
     x = torch.empty(prob.n, dtype=torch.float64, device="cuda")
     gen.device(prob, bands, b)
     variants = [("5-kernel", {"EG_NO_FUSE": "1"}), ("fused default", {})] + \
-        [(f"fused strips={k}", {"EG_MARCH_STRIPS": str(k)}) for k in (1, 2, 3, 4, 5, 6)]
+        ([] if quick else [(f"fused strips={k}", {"EG_MARCH_STRIPS": str(k)}) for k in (1, 2, 3, 4, 5, 6)])
     for name, env in variants:
         for k in ("EG_NO_FUSE", "EG_MARCH_STRIPS"):
             os.environ.pop(k, None)

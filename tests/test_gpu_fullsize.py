@@ -10,7 +10,9 @@ launch configuration bench.py times (the default solver, CUDA-graph replay, gene
   cannot reach it in 6 half-sweeps); windows start on an even row (the colouring's parity).
 * solve (MIXED, tol 1e-4): the full CPU oracle solve of the same inputs (about 70 GB of host RAM
   and a minute on the GPU box's cores) — iterations within 2, ||dx||/||x|| <= 10 tol, and the GPU's
-  x has oracle-recomputed true residual < tol.
+  x has oracle-recomputed true residual < tol.  The same at C3 and C4 (MIXED, the default solver:
+  fused phase kernels) and at C5 in the FP64 variant (BASELINE.json config 5's "fp64 variant"; the
+  Table 1 DP column), where the fixed-iteration histories must agree to 1e-10.
 """
 import numpy as np
 import pytest
@@ -118,3 +120,50 @@ def test_c5_solve_matches_full_oracle(c5):
     assert np.linalg.norm(r) / np.linalg.norm(bhat) < 1e-4
     n = min(len(hist), len(ho))
     assert np.allclose(hist[:n], ho[:n], rtol=1e-3)
+
+
+def _full_oracle_parity(prob, mode, tol=1e-4, hist_rtol=None):
+    g = (prob.nx, prob.ny, prob.nz)
+    bands = torch.empty((7, prob.n), dtype=torch.float64, device="cuda")
+    b = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    gen.device(prob, bands, b)
+    s = egs.Solver(g, bands, mode)
+    if mode != "fp64":   # the production path at these sizes: the fused phase kernels
+        s.profile_reset()
+        s.solve(b, tol=0.0, maxit=1, flags=egs.EG_SOLVE_PROFILE)
+        assert s.profile()["phase_A"][1] == 1
+    x, info, hist = s.solve(b, tol=tol, maxit=200)
+    hf = None
+    if hist_rtol is not None:
+        _, _, hf = s.solve(b, tol=0.0, maxit=6)
+    xg = x.cpu().numpy()
+    s.close()
+    del x, s, bands, b
+    torch.cuda.empty_cache()
+    hb, hrhs = gen.host(prob)
+    ahat, diag = oracle.scale(g, hb, mode)
+    del hb
+    xo, ho, io = oracle.solve(g, mode, ahat, diag, hrhs, tol=tol, maxit=200)
+    assert info.converged and info.true_R < tol and io.converged
+    assert abs(info.iters - io.iters) <= 2
+    assert np.linalg.norm(xg - xo) <= 10 * tol * np.linalg.norm(xo)
+    bhat = hrhs / diag
+    r = oracle.residual64(g, ahat, bhat, xg)
+    assert np.linalg.norm(r) / np.linalg.norm(bhat) < tol
+    del xo
+    if hist_rtol is not None:
+        _, hfo, _ = oracle.solve(g, mode, ahat, diag, hrhs, tol=0.0, maxit=6)
+        keep = hfo >= 1e-5
+        assert np.all(np.abs(hf[keep] - hfo[keep]) <= hist_rtol * hfo[keep])
+    return info, io
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_solve_matches_full_oracle_default_path(cfg):
+    """BASELINE.json configs 3 and 4 (MIXED, tol 1e-4) on the default (fused) path."""
+    _full_oracle_parity(gen.CONFIGS[cfg], "mixed", hist_rtol=1e-3)
+
+
+def test_c5_fp64_solve_matches_full_oracle():
+    """BASELINE.json config 5's fp64 variant: the all-fp64 solve against the fp64 oracle."""
+    _full_oracle_parity(C5, "fp64", hist_rtol=1e-10)

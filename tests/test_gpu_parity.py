@@ -29,14 +29,25 @@ def _vnp(mode):
     return np.float64 if mode == "fp64" else np.float32
 
 
-def _make(prob, mode):
+def _make(prob, mode, env=None, monkeypatch=None):
     bands, b = gen.host(prob)
     bd = torch.from_numpy(bands).cuda()
     # poison the caching allocator with NaN so that a read of an unwritten workspace element shows up
     junk = torch.full((4 * 7 * prob.n + (1 << 20),), float("nan"), dtype=torch.float64, device="cuda")
     del junk
+    for k, v in (env or {}).items():
+        monkeypatch.setenv(k, v)
     s = egs.Solver((prob.nx, prob.ny, prob.nz), bd, mode)
+    for k in (env or {}):
+        monkeypatch.delenv(k)
     return s, bands, b
+
+
+def _uses_fused(s, b):
+    """True iff the solver's iteration runs the fused phase kernels (one profiled iteration)."""
+    s.profile_reset()
+    s.solve(b, tol=0.0, maxit=1, flags=egs.EG_SOLVE_PROFILE)
+    return s.profile()["phase_A"][1] == 1
 
 
 def _rel(a, b):
@@ -70,14 +81,20 @@ def test_precondition_parity(prob, mode):
 
 FUSED_ODD = gen.Problem(128, 37, 13, seed=11)   # one 128-column tile, odd ny / nz
 FUSED_THIN = gen.Problem(192, 3, 70, seed=12)   # fewer rows than the per-CTA row ranges
+# below 2^18 points the default is the 5-kernel schedule: these cases force the fused phase kernels
+# (fp32 vectors; FP64 has no fused schedule and runs the 5-kernel one regardless)
+FORCE_FUSED = (FUSED_ODD, FUSED_THIN)
 
 
 @pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED, gen.Problem(130, 9, 70, seed=10), FUSED_ODD,
                                   FUSED_THIN] + DEEP, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("tol", [1e-3, 1e-4])
-def test_solve_parity(prob, mode, tol):
-    s, bands, b = _make(prob, mode)
+def test_solve_parity(prob, mode, tol, monkeypatch):
+    fused = prob in FORCE_FUSED
+    s, bands, b = _make(prob, mode, {"EG_FUSE": "1"} if fused else None, monkeypatch)
+    if fused:
+        assert _uses_fused(s, torch.from_numpy(b).cuda()) == (mode != "fp64")
     g = (prob.nx, prob.ny, prob.nz)
     ahat, diag = oracle.scale(g, bands, mode)
     xo, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=tol, maxit=200)
@@ -95,8 +112,8 @@ def test_solve_parity(prob, mode, tol):
 
 @pytest.mark.parametrize("prob", [gen.CONFIGS["C1"], RAGGED, FUSED_ODD], ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
 @pytest.mark.parametrize("mode", MODES)
-def test_fixed_iteration_history_parity(prob, mode):
-    s, bands, b = _make(prob, mode)
+def test_fixed_iteration_history_parity(prob, mode, monkeypatch):
+    s, bands, b = _make(prob, mode, {"EG_FUSE": "1"} if prob in FORCE_FUSED else None, monkeypatch)
     g = (prob.nx, prob.ny, prob.nz)
     ahat, diag = oracle.scale(g, bands, mode)
     _, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=0.0, maxit=8)
@@ -137,6 +154,35 @@ def test_determinism_and_host_buffers():
     assert isinstance(x3, np.ndarray) and np.array_equal(x3, x1.cpu().numpy()) and np.array_equal(h3, h1)
     xg, ig, hg = s.solve(torch.from_numpy(b).cuda(), tol=1e-5, maxit=100, flags=egs.EG_SOLVE_NO_GRAPH)
     assert torch.equal(xg, x1) and np.array_equal(hg, h1)            # graph replay == direct launch
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["5-kernel", "fused"])
+@pytest.mark.parametrize("mode", MODES)
+def test_warm_start_parity(mode, fused, monkeypatch):
+    """Warm start (x0 != 0, the NEXT-4 workflow): the entry computes r0 = round(bhat - Ahat x0) with
+    fp64 accumulation (k_start<ENTRY, !XZERO>) and the solve continues from x0.  Against the oracle's
+    solve from the same x0: counts within +-2, x within 10 tol, and the fixed-iteration history."""
+    prob = gen.Problem(128, 40, 20, seed=41)
+    s, bands, b = _make(prob, mode, {"EG_FUSE": "1"} if fused else {"EG_NO_FUSE": "1"}, monkeypatch)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, diag = oracle.scale(g, bands, mode)
+    # x0: the oracle's 2-iteration iterate of a perturbed right-hand side (nonzero everywhere, smooth)
+    x0, _, _ = oracle.solve(g, mode, ahat, diag, 1.1 * b + 0.01, tol=0.0, maxit=2)
+    bt, x0t = torch.from_numpy(b).cuda(), torch.from_numpy(x0).cuda()
+    if fused:
+        assert _uses_fused(s, bt) == (mode != "fp64")
+    tol = 1e-5 if mode != "fp32" else 1e-4
+    xo, ho, io = oracle.solve(g, mode, ahat, diag, b, x0=x0, tol=tol, maxit=200)
+    x, info, h = s.solve(bt, x0=x0t, tol=tol, maxit=200)
+    assert io.converged and info.converged and abs(info.iters - io.iters) <= 2 and info.true_R < tol
+    # true R of x0: fp64 sums, except FP32 mode's ||bhat|| (a binary32 sum, order-dependent rounding)
+    assert h[0] == pytest.approx(ho[0], rel=1e-5 if mode == "fp32" else 1e-12)
+    assert _rel(x.cpu().numpy(), xo) <= 10 * tol
+    _, hf, _ = oracle.solve(g, mode, ahat, diag, b, x0=x0, tol=0.0, maxit=6)
+    _, infof, hg = s.solve(bt, x0=x0t, tol=0.0, maxit=6)
+    keep = hf >= 1e-5
+    rt = 1e-10 if mode == "fp64" else 1e-3
+    assert np.all(np.abs(hg[keep] - hf[keep]) <= rt * hf[keep])
 
 
 def test_warm_start_and_zero_iterations():
