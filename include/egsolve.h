@@ -30,10 +30,10 @@
  * THREADING.  One handle is not thread-safe; separate handles are independent.  All device work
  * is ordered on the stream given to eg_solver_create.  The fused phase kernels keep
  * one CTA per SM and synchronise CTAs through ready flags, which needs every CTA of a launch
- * resident, so concurrent eg_solve / eg_solve_batch calls of handles that use them are serialised
- * inside this process (a process-wide lock; the calls block until their kernels finish anyway).
- * Other processes sharing the GPU are time-sliced, not co-resident, unless MPS is used: with MPS,
- * serialise the solves yourself or create the handles with EG_NO_FUSE=1 in the environment.
+ * resident: they are launched COOPERATIVELY, so the runtime either makes the whole grid resident or
+ * fails the launch (EG_ERR_CUDA), never a partly resident grid that waits forever — also with MPS
+ * or other work on the GPU.  Concurrent eg_solve / eg_solve_batch calls of handles that use them
+ * are additionally serialised per device inside this process (they block until done anyway).
  */
 #ifndef EGSOLVE_H
 #define EGSOLVE_H
@@ -119,7 +119,7 @@ int eg_workspace_bytes(const eg_grid* grid, const eg_dist* dist, eg_precision pr
  *     right-hand side and of the sweeps' iterate (8 working-precision values per point plus two
  *     ghost rows), which the red-black tri-SOR sweeps
  *     (EG_PRECOND_TRISOR) read instead of every other value of the natural-order arrays.  A solver
- *     whose workspace is at least this size uses them; a smaller workspace still runs tri-SOR, on
+ *     created with this feature (eg_solver_create_ex) uses them; without it tri-SOR still runs, on
  *     the natural-order arrays (same results, bitwise).
  * features = 0 gives eg_workspace_bytes.  Returns EG_OK or EG_ERR_ARG. */
 #define EG_FEATURE_TRISOR 1u
@@ -142,6 +142,15 @@ int eg_workspace_bytes_ex(const eg_grid* grid, const eg_dist* dist, eg_precision
 int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* const bands[7],
                      eg_precision prec, void* workspace, size_t workspace_bytes, void* stream,
                      eg_solver** out);
+
+/* The same with optional features (EG_FEATURE_* bit mask, as passed to eg_workspace_bytes_ex): the
+ * workspace must be at least eg_workspace_bytes_ex(grid, dist, prec, features) bytes (else
+ * EG_ERR_WORKSPACE), and exactly the requested optional regions are carved from it — a larger
+ * workspace never turns a feature on.  eg_solver_create(...) == eg_solver_create_ex(..., 0, ...).
+ * Errors: those of eg_solver_create; EG_ERR_ARG for an unknown feature bit. */
+int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* const bands[7],
+                        eg_precision prec, uint32_t features, void* workspace, size_t workspace_bytes,
+                        void* stream, eg_solver** out);
 
 /* a1 again on an existing solver: re-scale a NEW operator of the same grid / band / precision into
  * the workspace ("the matrix is time varying and so needs to be recomputed at every time step",
@@ -192,8 +201,8 @@ int eg_solve(eg_solver* s, const double* b, const double* x0, const eg_solve_par
  * driver) or DEVICE.  bands: DEVICE, as for eg_solver_set_operator, or NULL.  history (HOST,
  * count*(maxit+1) doubles) and info (HOST, count entries) may be NULL.  While solve k runs, the
  * upload of b[k+1] and the download of x[k-1] run on the library's own copy streams, staged
- * through two device buffers for b and two for x in the workspace: requires a workspace of at
- * least eg_workspace_bytes_ex(..., EG_FEATURE_BATCH, ...) (else EG_ERR_WORKSPACE).  Each solve's
+ * through two device buffers for b and two for x in the workspace: requires a solver created with
+ * EG_FEATURE_BATCH (eg_solver_create_ex; else EG_ERR_WORKSPACE).  Each solve's
  * x / history / info are bitwise those of the individual eg_solve call.  Blocks until every x[k] is
  * written.  Stops at the first failing solve; *done (may be NULL) = the number of solves completed.
  * Errors: those of eg_solve, EG_ERR_ARG, EG_ERR_WORKSPACE. */

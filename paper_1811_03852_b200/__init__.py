@@ -25,7 +25,8 @@ STATUS = {0: "EG_OK", 1: "EG_ERR_ARG", 2: "EG_ERR_SINGULAR_DIAG", 3: "EG_ERR_DEG
           4: "EG_ERR_BREAKDOWN", 5: "EG_ERR_NONFINITE", 6: "EG_ERR_CUDA", 7: "EG_ERR_NCCL",
           8: "EG_ERR_WORKSPACE"}
 # symbols declared in include/egsolve.h (tests check the library exports all of them)
-ABI_SYMBOLS = ("eg_workspace_bytes", "eg_workspace_bytes_ex", "eg_solver_create", "eg_solver_set_operator",
+ABI_SYMBOLS = ("eg_workspace_bytes", "eg_workspace_bytes_ex", "eg_solver_create", "eg_solver_create_ex",
+               "eg_solver_set_operator",
                "eg_solver_set_preconditioner", "eg_apply_operator", "eg_precondition",
                "eg_solve", "eg_solve_batch", "eg_solver_destroy", "eg_last_error", "eg_status_str",
                "eg_nccl_unique_id", "eg_loopback_id", "eg_num_kernels", "eg_kernel_name", "eg_profile_get",
@@ -89,6 +90,9 @@ def lib():
         L.eg_solver_create.argtypes = [ctypes.POINTER(_Grid), ctypes.POINTER(_Dist),
                                        ctypes.POINTER(vp), i32, vp, ctypes.c_size_t, vp,
                                        ctypes.POINTER(vp)]
+        L.eg_solver_create_ex.argtypes = [ctypes.POINTER(_Grid), ctypes.POINTER(_Dist),
+                                          ctypes.POINTER(vp), i32, ctypes.c_uint32, vp, ctypes.c_size_t, vp,
+                                          ctypes.POINTER(vp)]
         L.eg_solver_set_operator.argtypes = [vp, ctypes.POINTER(vp)]
         L.eg_solver_set_preconditioner.argtypes = [vp, i32, i32, ctypes.c_double]
         L.eg_apply_operator.argtypes = [vp, vp, vp]
@@ -204,19 +208,19 @@ class Solver:
         assert tuple(bands.shape) == (7, self.n_local), (tuple(bands.shape), self.n_local)
         self._grid = _Grid(nx, ny, nz)
         nbytes = ctypes.c_size_t()
-        rc = lib().eg_workspace_bytes_ex(ctypes.byref(self._grid), dptr, self.mode,
-                                         (EG_FEATURE_TRISOR if trisor else 0) | (EG_FEATURE_BATCH if batch else 0),
+        self.features = (EG_FEATURE_TRISOR if trisor else 0) | (EG_FEATURE_BATCH if batch else 0)
+        rc = lib().eg_workspace_bytes_ex(ctypes.byref(self._grid), dptr, self.mode, self.features,
                                          ctypes.byref(nbytes))
         if rc:
             raise EgError(rc, "eg_workspace_bytes_ex")
         self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
         ptrs = (ctypes.c_void_p * 7)(*[bands[d].data_ptr() for d in range(7)])
         h = ctypes.c_void_p()
-        rc = lib().eg_solver_create(ctypes.byref(self._grid), dptr, ptrs, self.mode,
-                                    _ptr(self.workspace), nbytes.value,
-                                    ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        rc = lib().eg_solver_create_ex(ctypes.byref(self._grid), dptr, ptrs, self.mode, self.features,
+                                       _ptr(self.workspace), nbytes.value,
+                                       ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
         if rc:
-            raise EgError(rc, "eg_solver_create")
+            raise EgError(rc, "eg_solver_create_ex")
         self._h = h
 
     # ---- lifetime ----

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "egsolve.h"
@@ -315,6 +316,25 @@ Vecs<MODE> vecs(eg_solver* s, void* x_it) {
     return v;
 }
 
+// A cooperative launch (cudaLaunchAttributeCooperative, also as a captured graph kernel node): the
+// runtime guarantees every CTA of the grid is resident at once, or fails the launch
+// (cudaErrorCooperativeLaunchTooLarge) instead of letting CTAs that wait on other CTAs' ready flags
+// hang.  Used for the fused phase kernels, whose CTAs wait on their neighbours' rows.
+template <typename... Exp, typename... Act>
+cudaError_t launch_coop(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Act&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
+
 // -------- multi-GPU plumbing (latitude bands) --------
 // exchange the boundary rows of a ghosted array with the j-neighbours
 bool multi(const eg_solver* s) { return s->comm != nullptr || s->lb != nullptr; }
@@ -442,8 +462,8 @@ int iteration_fused(eg_solver* s, void* x_it) {
             // the first iteration after a (re)start has p = v = 0: phase A then reads r only
             ProfScope ps(s, KID_PHASE_A, s->next_fresh ? alg_bytes(s, KID_PHASE_A) - 2.0 * s->L.vsz * s->L.n : -1.0);
             s->next_fresh = false;
-            k_march<MODE, 1><<<grid, MA_THREADS, s->smem_march, s->st>>>(s->geo, v, s->mg, s->ready_flags, s->maps);
-            CK(cudaGetLastError());
+            CK(launch_coop(k_march<MODE, 1>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
+                           s->maps));
         }
 #ifdef MA_VERIFY
         {
@@ -466,8 +486,8 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
         {
             ProfScope ps(s, KID_PHASE_B);
-            k_march<MODE, 2><<<grid, MA_THREADS, s->smem_march, s->st>>>(s->geo, v, s->mg, s->ready_flags, s->maps);
-            CK(cudaGetLastError());
+            CK(launch_coop(k_march<MODE, 2>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
+                           s->maps));
         }
 #ifdef MA_VERIFY
         {
@@ -1239,9 +1259,16 @@ int eg_workspace_bytes_ex(const eg_grid* grid, const eg_dist* dist, eg_precision
 int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* const bands[7],
                      eg_precision prec, void* workspace, size_t workspace_bytes, void* stream,
                      eg_solver** out) {
+    return eg_solver_create_ex(grid, dist, bands, prec, 0u, workspace, workspace_bytes, stream, out);
+}
+
+int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* const bands[7],
+                        eg_precision prec, uint32_t features, void* workspace, size_t workspace_bytes,
+                        void* stream, eg_solver** out) {
     if (!out) return EG_ERR_ARG;
     *out = nullptr;
-    if (!valid_grid(grid) || !bands || prec < EG_FP64 || prec > EG_FP32 || !workspace)
+    if (!valid_grid(grid) || !bands || prec < EG_FP64 || prec > EG_FP32 || !workspace ||
+        (features & ~(EG_FEATURE_TRISOR | EG_FEATURE_BATCH)))
         return EG_ERR_ARG;
     for (int d = 0; d < 7; ++d)
         if (!bands[d]) return EG_ERR_ARG;
@@ -1254,22 +1281,12 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
         delete s;
         return EG_ERR_ARG;
     }
-    // optional regions, in layout order: the colour-split tri-SOR copies, then the batch staging
-    Layout Lt, Lb, Ltb;
-    make_layout(grid, s->j_end - s->j_begin, prec, &Lt, EG_FEATURE_TRISOR);
-    make_layout(grid, s->j_end - s->j_begin, prec, &Lb, EG_FEATURE_BATCH);
-    make_layout(grid, s->j_end - s->j_begin, prec, &Ltb, EG_FEATURE_TRISOR | EG_FEATURE_BATCH);
-    // the caller sized the workspace with eg_workspace_bytes_ex(features): recover the features
-    uint32_t feat = 0;
-    if (workspace_bytes >= Ltb.total) feat = EG_FEATURE_TRISOR | EG_FEATURE_BATCH;
-    else if (workspace_bytes >= Lt.total && workspace_bytes >= Lb.total)
-        feat = Lt.total >= Lb.total ? EG_FEATURE_TRISOR : EG_FEATURE_BATCH;
-    else if (workspace_bytes >= Lt.total) feat = EG_FEATURE_TRISOR;
-    else if (workspace_bytes >= Lb.total) feat = EG_FEATURE_BATCH;
-    const bool room_split = (feat & EG_FEATURE_TRISOR) && grid->nx % 2 == 0;
-    const bool room_batch = (feat & EG_FEATURE_BATCH) != 0;
-    make_layout(grid, s->j_end - s->j_begin, prec, &s->L, feat);
-    if (workspace_bytes < s->L.base_total || ((uintptr_t)workspace & 255)) {
+    // the optional regions are the ones the caller asked for (features), in layout order: the
+    // colour-split tri-SOR copies, then the batch staging; the workspace must hold them all
+    const bool room_split = (features & EG_FEATURE_TRISOR) && grid->nx % 2 == 0;
+    const bool room_batch = (features & EG_FEATURE_BATCH) != 0;
+    make_layout(grid, s->j_end - s->j_begin, prec, &s->L, features);
+    if (workspace_bytes < s->L.total || ((uintptr_t)workspace & 255)) {
         delete s;
         return EG_ERR_WORKSPACE;
     }
@@ -1395,6 +1412,10 @@ int eg_solver_create(const eg_grid* grid, const eg_dist* dist, const double* con
             s->mg.strips = (int)std::min<int64_t>(s->L.nyl, nsm / s->L.tiles);
             const char* fs = getenv("EG_MARCH_STRIPS");  // tests: fewer, longer strips
             if (fs && atoi(fs) >= 1) s->mg.strips = std::min(s->mg.strips, atoi(fs));
+            // tests only: more strips than SMs (a grid that cannot be co-resident; the cooperative
+            // launch must refuse it with EG_ERR_CUDA rather than hang)
+            const char* fo = getenv("EG_MARCH_STRIPS_UNSAFE");
+            if (fo && atoi(fo) >= 1) s->mg.strips = (int)std::min<int64_t>(s->L.nyl, atoi(fo));
             // at least ~116 KB so that exactly one CTA (and one 512-column TMEM allocation) fits an SM
             const size_t st_a = (size_t)(s->mg.fst_a + s->mg.sst_a) * ma_stage_bytes(1);
             const size_t st_b = (size_t)(s->mg.fst_b + s->mg.sst_b) * ma_stage_bytes(2);

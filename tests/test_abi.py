@@ -78,6 +78,11 @@ def test_workspace_bytes_and_argument_validation(egs):
     h = ctypes.c_void_p()
     assert L.eg_solver_create(None, None, None, 1, None, 0, None, ctypes.byref(h)) == 1
     assert not h.value
+    bands = (ctypes.c_void_p * 7)(*([1] * 7))
+    ws = ctypes.c_void_p(256)
+    # eg_solver_create_ex: an unknown feature bit is refused before any device work
+    assert L.eg_solver_create_ex(ctypes.byref(g), None, bands, 1, 4, ws, nbt.value, None, ctypes.byref(h)) == 1
+    assert not h.value
 
 
 def test_band_rows_partition(egs):
