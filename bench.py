@@ -113,6 +113,30 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def spawn_ranks(n):
+    """`--gpus N` without a launcher: re-exec this script under torch.distributed.run with N ranks on
+    this node (127.0.0.1 rendezvous), exactly as the driver launches it; rank 0 prints the line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -124,12 +148,16 @@ def dist_init(args):
             import torch
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
+        print(f"bench.py: rank {rank}/{ws} process group backend {dist.get_backend()}", file=sys.stderr, flush=True)
     return ws, rank, local
 
 
 def oracle_sample(prob, precision, target_s=12.0):
-    """Time the CPU oracle on a bounded latitude sample of the workload (same nx, nz, recipe).
-    Returns dict(value = iters/s scaled to the full grid, ...)."""
+    """Time the CPU oracle on a bounded latitude sample of the workload (same nx, nz, recipe): the
+    step (oracle_scale + oracle_solve(tol=0, maxit=8)) on the rows of a 2560 x R x 70 sample, R
+    chosen so the step takes ~target_s.  Per-iteration work is proportional to the points, so
+    value = iterations / wall * (sample points / grid points) is the full grid's iters/s.
+    Returns dict(value, seconds = the sample step's own wall time, ...)."""
     import gen
     import oracle
     rows = 8
@@ -152,33 +180,48 @@ def oracle_sample(prob, precision, target_s=12.0):
     frac = (prob.nx * rows * prob.nz) / prob.n
     return {
         "value": info.iters / dt * frac, "unit": "iter/s", "cores": oracle.threads(), "kind": "oracle",
+        "cpu_model": cpu_model(),
         "sample": (f"oracle_scale + oracle_solve({precision}, tol=0, maxit={ITERS_PER_STEP}) on a "
                    f"{prob.nx}x{rows}x{prob.nz} latitude sample ({frac:.4f} of the grid) generated "
                    f"with the same recipe; {dt:.2f} s wall; iters/s scaled by the point ratio"),
+        "sample_grid": [prob.nx, rows, prob.nz], "sample_fraction": frac,
         "seconds": dt,
     }
 
 
 def run_reference(args, prob, ws, rank):
+    """The reference arm: the CPU oracle as it stands, on this host's cores, each step a bounded
+    latitude sample of the workload (oracle_sample).  ms_per_step is the sample step's own wall
+    time (what this run spent), value the full grid's iters/s it implies (scaled by the point
+    ratio).  Under torchrun only rank 0 works and prints; the other ranks exit without work."""
     if rank != 0:
         return
     import oracle  # the reference arm is the CPU oracle (DESIGN.md §Benchmark)
     oracle.set_threads(os.cpu_count() or 1)  # all host cores, also under torchrun (OMP_NUM_THREADS=1)
+    t_run = time.perf_counter()
     for _ in range(args.warmup):
-        oracle_sample(prob, args.precision, target_s=1.0)
-    vals, secs = [], 0.0
+        oracle_sample(prob, args.precision, target_s=min(1.0, args.ref_seconds))
+    # each step ~ref_seconds, but the whole K-step run bounded to ~2 minutes
+    per_step = min(args.ref_seconds, max(0.5, 120.0 / max(args.steps, 1)))
+    vals, secs = [], []
     last = None
     for _ in range(args.steps):
-        last = oracle_sample(prob, args.precision, target_s=args.ref_seconds)
+        last = oracle_sample(prob, args.precision, target_s=per_step)
         vals.append(last["value"])
-        secs += last["seconds"]
+        secs.append(last["seconds"])
     v = statistics.median(vals)
+    cfg = config_dict(args, prob, ws)
+    cfg["reference_sample"] = (f"each step: the same step on a {last['sample_grid'][0]}x{last['sample_grid'][1]}x"
+                               f"{last['sample_grid'][2]} latitude sample ({last['sample_fraction']:.4f} of the grid); "
+                               "value scaled to the full grid by the point ratio")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * ITERS_PER_STEP / v,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.median(secs),
+        "full_grid_ms_per_step_extrapolated": 1000.0 * ITERS_PER_STEP / v,
+        "wall_s": time.perf_counter() - t_run,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision],
-        "data": "synthetic", "config": config_dict(args, prob, ws),
-        "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")},
         "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -416,7 +459,7 @@ def run_ours(args, prob, ws, rank, local):
     }
     if ws == 1 and not args.no_cpu_baseline:
         cb = oracle_sample(prob, args.precision, target_s=args.ref_seconds)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
     print(json.dumps(line), flush=True)
 
 
@@ -432,7 +475,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-trisor", action="store_true", help="skip the tri-SOR preconditioner block")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)           # does not return
     ws, rank, local = dist_init(args)
+    if ws != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; measuring {ws} rank(s)", file=sys.stderr)
     if rank == 0:  # one build, not one per rank racing on the same files
         subprocess.check_call(["make", "-s", "all"], cwd=ROOT, stdout=subprocess.DEVNULL)
     if ws > 1:

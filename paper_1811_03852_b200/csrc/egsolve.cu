@@ -31,11 +31,12 @@ namespace {
 
 enum KernelId {
     KID_SCALE = 0, KID_START, KID_FIN, KID_THOMAS_P, KID_STENCIL_A, KID_THOMAS_S, KID_STENCIL_B,
-    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_SOR, KID_COUNT
+    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_SOR, KID_VERIFY, KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"scale", "start", "finalize", "thomas_p", "stencil_dot_A",
                                        "thomas_s", "stencil_dot_B", "update_xr", "apply",
-                                       "precondition", "convert", "phase_A", "phase_B", "trisor_half"};
+                                       "precondition", "convert", "phase_A", "phase_B", "trisor_half",
+                                       "verify"};
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -259,6 +260,7 @@ cudaEvent_t take_event(eg_solver* s) {
 }
 
 double alg_bytes(const eg_solver* s, int kid);
+double start_bytes(const eg_solver* s, int entry, int xzero, bool write);
 double sor_alg_bytes(const eg_solver* s, int kind, int sweep, int colour);
 
 struct ProfScope {
@@ -715,8 +717,7 @@ int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero, const
     s->next_fresh = true;
     s->next_xzero = entry && xzero;
     {
-        // entry from x = 0 reads b, diag and writes bhat, r, rhat0 only (x is not stored)
-        ProfScope ps(s, KID_START, entry && xzero ? (24.0 + 2.0 * s->L.vsz) * s->L.n : -1.0);
+        ProfScope ps(s, KID_START, start_bytes(s, entry, xzero, true));
         if (entry && xzero) k_start<MODE, true, true><<<gr, RW, 0, s->st>>>(s->geo, v, b);
         else if (entry) k_start<MODE, true, false><<<gr, RW, 0, s->st>>>(s->geo, v, b);
         else k_start<MODE, false, false><<<gr, RW, 0, s->st>>>(s->geo, v, b);
@@ -743,7 +744,7 @@ int verify(eg_solver* s, void* x_it) {
     }
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     {
-        ProfScope ps(s, KID_START);
+        ProfScope ps(s, KID_VERIFY, start_bytes(s, 0, 0, false));
         k_start<MODE, false, false, false><<<gr, RW, 0, s->st>>>(s->geo, v, nullptr);
         CK(cudaGetLastError());
     }
@@ -1203,13 +1204,26 @@ double sor_alg_bytes(const eg_solver* s, int kind, int sweep, int colour) {
     return (fin + (colour == 0 ? 1.0 : 3.0 + 0.5) + out) * V * n + fin_z;  // red: (U,D) only; black: + (E,W,N,S), red x
 }
 
+// algorithmic HBM bytes of one k_start launch, by variant:
+//   entry from x0 = 0: b, diag in; bhat, r, rhat0 out (x is neither read nor stored)
+//   entry from x0:     b, diag, x, 6 bands in; bhat, r, rhat0 out
+//   restart:           bhat, x, 6 bands in; r, rhat0 out
+//   verification:      bhat, x, 6 bands in; nothing out (the true residual norm only)
+double start_bytes(const eg_solver* s, int entry, int xzero, bool write) {
+    const double V = (double)s->L.vsz, X = (double)s->L.xsz, n = (double)s->L.n;
+    const double out = write ? 2.0 * V : 0.0;
+    if (entry && xzero) return (8.0 + 8.0 + 8.0 + out) * n;
+    if (entry) return (8.0 + 8.0 + X + 6.0 * V + 8.0 + out) * n;
+    return (8.0 + X + 6.0 * V + out) * n;
+}
+
 // algorithmic HBM bytes of one launch, V = vector / band bytes, X = x bytes
 double alg_bytes(const eg_solver* s, int kid) {
     const double V = (double)s->L.vsz, X = (double)s->L.xsz, n = (double)s->L.n;
     double per = 0;
     switch (kid) {
         case KID_SCALE: per = 7 * 8 + 6 * V + 8; break;            // 7 fp64 in; 6 V + diag out
-        case KID_START: per = 8 + X + 6 * V + 2 * V; break;        // bhat, x, 6 bands; r, rhat0
+        case KID_START: per = 8 + X + 6 * V + 2 * V; break;        // restart (start_bytes has every variant)
         case KID_THOMAS_P: per = 5 * V + 2 * V; break;             // r,p,v,U,D; p,z
         case KID_STENCIL_A: per = 8 * V + V; break;                // z,6 bands,rhat0; v
         case KID_THOMAS_S: per = 4 * V + 2 * V; break;             // r,v,U,D; s,z_s
@@ -1218,6 +1232,7 @@ double alg_bytes(const eg_solver* s, int kid) {
         case KID_APPLY: per = 7 * V + V; break;
         case KID_PRECOND: per = 3 * V + V; break;
         case KID_CONVERT: per = 12; break;
+        case KID_VERIFY: return start_bytes(s, 0, 0, false);
         case KID_PHASE_A: per = 4 * V + 6 * V + 3 * V; break;      // r,p,v,rhat0 + B4,B2; p',z,v'
         case KID_PHASE_B: per = 2 * V + 6 * V + 3 * V; break;      // r,v' + B4,B2; s,z_s,t
         case KID_SOR: per = 5 * V; break;  // a later sweep's half: f, bands of one colour; all of x; x of one colour

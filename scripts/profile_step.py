@@ -27,6 +27,8 @@ with torch.cuda.stream(st):
     b = torch.empty(prob.n, dtype=torch.float64, device="cuda")
     gen.device(prob, bands, b, stream=st)
     s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, a.precision, stream=st)
+    s.set_operator(bands)                               # warm-up step (graph capture), as the bench does
+    s.solve(b, tol=0.0, maxit=a.maxit, flags=a.flags)
     s.set_operator(bands)
     x, info, hist = s.solve(b, tol=0.0, maxit=a.maxit, flags=a.flags)
 torch.cuda.synchronize()
