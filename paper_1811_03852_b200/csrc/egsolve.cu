@@ -31,12 +31,12 @@ namespace {
 
 enum KernelId {
     KID_SCALE = 0, KID_START, KID_FIN, KID_THOMAS_P, KID_STENCIL_A, KID_THOMAS_S, KID_STENCIL_B,
-    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_SOR, KID_VERIFY, KID_COUNT
+    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_SOR, KID_VERIFY, KID_UPDATE_X, KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"scale", "start", "finalize", "thomas_p", "stencil_dot_A",
                                        "thomas_s", "stencil_dot_B", "update_xr", "apply",
                                        "precondition", "convert", "phase_A", "phase_B", "trisor_half",
-                                       "verify"};
+                                       "verify", "update_x"};
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -205,6 +205,11 @@ struct eg_solver {
     // NCCL, or the loopback group (tests)
     ncclComm_t comm = nullptr;
     LoopGroup* lb = nullptr;
+    // latitude bands: the ghost-row exchange runs on cst beside the phase kernel (ev_edge: the edge
+    // rows are computed; ev_halo: the ghost rows have arrived); the x half of the update runs on xst
+    // beside reduction 3 (ev_b: reduction 2 done; ev_xu: x updated)
+    cudaStream_t cst = nullptr, xst = nullptr;
+    cudaEvent_t ev_edge = nullptr, ev_halo = nullptr, ev_b = nullptr, ev_xu = nullptr;
     // profiling
     bool profiling = false;
     std::vector<cudaEvent_t> evpool;
@@ -345,40 +350,89 @@ int lb_fail(eg_solver* s) {
     return fail(s, EG_ERR_NCCL, "loopback group: a rank failed or did not arrive within 120 s");
 }
 
-int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz) {
+// async: the exchange runs on the communication stream s->cst, ordered after everything enqueued on
+// s->st so far (ev_edge); the caller joins it (halo_join) before the first kernel that reads a
+// ghost row.  Otherwise it runs on s->st.
+int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz, bool async = false) {
     if (s->nranks == 1) return EG_OK;
     const size_t rowb = (size_t)s->L.row * esz;
     ncclDataType_t ty = esz == 8 ? ncclDouble : ncclFloat;
     unsigned char* first = (unsigned char*)row0;
     unsigned char* last = first + (size_t)(s->L.nyl - 1) * rowb;
+    cudaStream_t xs = async ? s->cst : s->st;
     if (s->lb) {
         LoopGroup* G = s->lb;
         G->first[s->rank] = first;
         G->last[s->rank] = last;
         if (!lb_barrier(G)) return lb_fail(s);
-        if (s->rank > 0) CK(cudaMemcpyAsync(ghost_lo, G->last[s->rank - 1], rowb, cudaMemcpyDeviceToDevice, s->st));
+        // every rank's edge rows are enqueued on the shared stream before this point
+        if (async) {
+            CK(cudaEventRecord(s->ev_edge, s->st));
+            CK(cudaStreamWaitEvent(xs, s->ev_edge, 0));
+        }
+        if (s->rank > 0) CK(cudaMemcpyAsync(ghost_lo, G->last[s->rank - 1], rowb, cudaMemcpyDeviceToDevice, xs));
         if (s->rank < s->nranks - 1)
-            CK(cudaMemcpyAsync(ghost_hi, G->first[s->rank + 1], rowb, cudaMemcpyDeviceToDevice, s->st));
+            CK(cudaMemcpyAsync(ghost_hi, G->first[s->rank + 1], rowb, cudaMemcpyDeviceToDevice, xs));
+        if (async) CK(cudaEventRecord(s->ev_halo, xs));
         if (!lb_barrier(G)) return lb_fail(s);
         return EG_OK;
     }
+    if (async) {
+        CK(cudaEventRecord(s->ev_edge, s->st));
+        CK(cudaStreamWaitEvent(xs, s->ev_edge, 0));
+    }
     NK(ncclGroupStart());
     if (s->rank > 0) {
-        NK(ncclSend(first, s->L.row, ty, s->rank - 1, s->comm, s->st));
-        NK(ncclRecv(ghost_lo, s->L.row, ty, s->rank - 1, s->comm, s->st));
+        NK(ncclSend(first, s->L.row, ty, s->rank - 1, s->comm, xs));
+        NK(ncclRecv(ghost_lo, s->L.row, ty, s->rank - 1, s->comm, xs));
     }
     if (s->rank < s->nranks - 1) {
-        NK(ncclSend(last, s->L.row, ty, s->rank + 1, s->comm, s->st));
-        NK(ncclRecv(ghost_hi, s->L.row, ty, s->rank + 1, s->comm, s->st));
+        NK(ncclSend(last, s->L.row, ty, s->rank + 1, s->comm, xs));
+        NK(ncclRecv(ghost_hi, s->L.row, ty, s->rank + 1, s->comm, xs));
     }
     NK(ncclGroupEnd());
+    if (async) CK(cudaEventRecord(s->ev_halo, xs));
     return EG_OK;
 }
 
-int halo_ghosted(eg_solver* s, void* zrow0) {
+int halo_ghosted(eg_solver* s, void* zrow0, bool async = false) {
     const size_t esz = s->L.vsz, rowb = (size_t)s->L.row * esz;
     unsigned char* r0 = (unsigned char*)zrow0;
-    return halo(s, r0, r0 - rowb, r0 + (size_t)s->L.nyl * rowb, esz);
+    return halo(s, r0, r0 - rowb, r0 + (size_t)s->L.nyl * rowb, esz, async);
+}
+
+int halo_join(eg_solver* s) {
+    if (s->nranks > 1) CK(cudaStreamWaitEvent(s->st, s->ev_halo, 0));
+    return EG_OK;
+}
+
+// the rows of a band whose stencil needs a neighbouring rank's ghost row (edge) or none (interior)
+int edge_rows(const eg_solver* s, RowMap* rm) {
+    const int lo = s->rank > 0, hi = s->rank < s->nranks - 1;
+    const int nyl = (int)s->L.nyl;
+    if (nyl == 1) { *rm = RowMap{0, 0}; return lo | hi; }
+    if (lo && hi) { *rm = RowMap{0, nyl - 1}; return 2; }
+    *rm = RowMap{lo ? 0 : nyl - 1, 0};
+    return lo | hi;
+}
+int interior_rows(const eg_solver* s, RowMap* rm) {
+    const int lo = s->rank > 0, hi = s->rank < s->nranks - 1;
+    *rm = RowMap{lo, 1};
+    return std::max(0, (int)s->L.nyl - lo - hi);
+}
+
+// stencil of the band-edge rows after their ghost rows arrived (the phase kernel / the interior
+// stencil launch left them out), same arithmetic and reduction slots as the full launch
+template <int MODE, int DOTS>
+int stencil_rows(eg_solver* s, const typename Prec<MODE>::V* z, typename Prec<MODE>::V* y,
+                 const typename Prec<MODE>::V* aux, bool edge) {
+    RowMap rm;
+    const int n = edge ? edge_rows(s, &rm) : interior_rows(s, &rm);
+    if (n == 0) return EG_OK;
+    Vecs<MODE> v = vecs<MODE>(s, s->x64);
+    k_stencil<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n), RW, 0, s->st>>>(s->geo, v, z, y, aux, rm);
+    CK(cudaGetLastError());
+    return EG_OK;
 }
 
 template <int MODE, int WHICH>
@@ -438,6 +492,48 @@ VfyBufs g_vfy{};
 #endif
 
 // -------- the iteration (rows a3-a10) --------
+// a9 + a10: the update and reduction 3.  One GPU: one k_update.  Latitude bands (and the 1-rank
+// NCCL path): the x half runs on s->xst beside the r half and reduction 3 (its all-gather), joined
+// at the end of the iteration — before anything reads x or overwrites z / z_s.
+template <int MODE>
+int update_and_reduce(eg_solver* s, Vecs<MODE>& v) {
+    const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
+    const double bx = 2.0 * s->L.xsz + 2.0 * s->L.vsz;     // x, z, z_s in; x out
+    const double xz_bytes = s->next_xzero ? (double)s->L.xsz * s->L.n : 0.0;
+    int rc;
+    if (!multi(s)) {
+        ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - xz_bytes : -1.0);
+        s->next_xzero = false;
+        if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
+        else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
+        CK(cudaGetLastError());
+        return finalize<MODE, W_C>(s, 0);
+    }
+    // (profiled solves keep both halves on s->st, where the CUDA events are)
+    cudaStream_t xs = s->profiling ? s->st : s->xst;
+    if (!s->profiling) {
+        CK(cudaEventRecord(s->ev_b, s->st));
+        CK(cudaStreamWaitEvent(xs, s->ev_b, 0));
+    }
+    {
+        ProfScope ps(s, KID_UPDATE_X, bx * s->L.n - xz_bytes);
+        s->next_xzero = false;
+        if (s->cpt == 2) k_update<MODE, 2, 2><<<gr, RW / 2, 0, xs>>>(s->geo, v);
+        else k_update<MODE, 1, 2><<<gr, RW, 0, xs>>>(s->geo, v);
+        CK(cudaGetLastError());
+    }
+    if (!s->profiling) CK(cudaEventRecord(s->ev_xu, xs));
+    {
+        ProfScope ps(s, KID_UPDATE, alg_bytes(s, KID_UPDATE) - bx * s->L.n);
+        if (s->cpt == 2) k_update<MODE, 2, 1><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
+        else k_update<MODE, 1, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
+        CK(cudaGetLastError());
+    }
+    if ((rc = finalize<MODE, W_C>(s, 0))) return rc;
+    if (!s->profiling) CK(cudaStreamWaitEvent(s->st, s->ev_xu, 0));
+    return EG_OK;
+}
+
 // fused schedule: phase A (a3 + a4), phase B (a6 + a7), update (a9), three finalisers
 template <int MODE>
 int iteration_fused(eg_solver* s, void* x_it) {
@@ -446,10 +542,11 @@ int iteration_fused(eg_solver* s, void* x_it) {
     if constexpr (MODE != 0) {
         const unsigned grid = (unsigned)(s->mg.strips * s->L.tiles);
         const dim3 gedge((unsigned)s->L.tiles, 2u);
-        if (multi(s)) {  // latitude bands: z of the band's edge rows -> the neighbours' ghost rows
+        if (multi(s)) {  // latitude bands: z of the band's edge rows -> the neighbours' ghost rows,
+            // exchanged on the communication stream while the phase kernel runs
             k_edge_rows<MODE, 1><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.z);
             CK(cudaGetLastError());
-            if ((rc = halo_ghosted(s, v.z))) return rc;
+            if ((rc = halo_ghosted(s, v.z, true))) return rc;
         }
 #ifdef MA_VERIFY
         const int64_t n = s->L.n;
@@ -467,12 +564,16 @@ int iteration_fused(eg_solver* s, void* x_it) {
             CK(launch_coop(k_march<MODE, 1>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
                            s->maps));
         }
+        if (s->nranks > 1) {  // the band-edge rows' stencil, once their ghost rows are in
+            if ((rc = halo_join(s))) return rc;
+            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true))) return rc;
+        }
 #ifdef MA_VERIFY
         {
             Vecs<MODE> w = v;
             w.p = (typename Prec<MODE>::V*)g_vfy.p; w.v = (typename Prec<MODE>::V*)g_vfy.v; w.slots = g_vfy.slots;
             k_thomas_tm<MODE, 1><<<gtm_, 128, s->smem_tm, s->st>>>(s->geo, w, nullptr, (typename Prec<MODE>::V*)g_vfy.z);
-            k_stencil<MODE, 1><<<gr_, RW, 0, s->st>>>(s->geo, w, (typename Prec<MODE>::V*)g_vfy.z, w.v, w.rh);
+            k_stencil<MODE, 1><<<gr_, RW, 0, s->st>>>(s->geo, w, (typename Prec<MODE>::V*)g_vfy.z, w.v, w.rh, ALL_ROWS);
             k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.z, g_vfy.z, n, 0);
             k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.p, g_vfy.p, n, 1);
             k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.v, g_vfy.v, n, 2);
@@ -484,12 +585,16 @@ int iteration_fused(eg_solver* s, void* x_it) {
         if (multi(s)) {
             k_edge_rows<MODE, 2><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.zs);
             CK(cudaGetLastError());
-            if ((rc = halo_ghosted(s, v.zs))) return rc;
+            if ((rc = halo_ghosted(s, v.zs, true))) return rc;
         }
         {
             ProfScope ps(s, KID_PHASE_B);
             CK(launch_coop(k_march<MODE, 2>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
                            s->maps));
+        }
+        if (s->nranks > 1) {
+            if ((rc = halo_join(s))) return rc;
+            if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true))) return rc;
         }
 #ifdef MA_VERIFY
         {
@@ -497,7 +602,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
             w.s = (typename Prec<MODE>::V*)g_vfy.s; w.slots = g_vfy.slots;
             k_thomas_tm<MODE, 2><<<gtm_, 128, s->smem_tm, s->st>>>(s->geo, w, nullptr, (typename Prec<MODE>::V*)g_vfy.zs);
             k_stencil<MODE, 2><<<gr_, RW, 0, s->st>>>(s->geo, w, (typename Prec<MODE>::V*)g_vfy.zs,
-                                                     (typename Prec<MODE>::V*)g_vfy.t, w.s);
+                                                     (typename Prec<MODE>::V*)g_vfy.t, w.s, ALL_ROWS);
             k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.s, g_vfy.s, n, 3);
             k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.zs, g_vfy.zs, n, 4);
             k_vfy_cmp<float><<<592, 256, 0, s->st>>>((const float*)v.t, g_vfy.t, n, 5);
@@ -506,15 +611,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
 #endif
         if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
-        const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
-        {
-            ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - (double)s->L.xsz * s->L.n : -1.0);
-            s->next_xzero = false;
-            if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
-            else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
-            CK(cudaGetLastError());
-        }
-        if ((rc = finalize<MODE, W_C>(s, 0))) return rc;
+        if ((rc = update_and_reduce<MODE>(s, v))) return rc;
     }
     return EG_OK;
 }
@@ -616,25 +713,18 @@ int iteration_trisor(eg_solver* s, void* x_it) {
     if ((rc = apply_trisor<MODE, 1>(s, v, nullptr, v.z))) return rc;
     {
         ProfScope ps(s, KID_STENCIL_A);
-        k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh);
+        k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh, ALL_ROWS);
         CK(cudaGetLastError());
     }
     if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
     if ((rc = apply_trisor<MODE, 2>(s, v, nullptr, v.zs))) return rc;
     {
         ProfScope ps(s, KID_STENCIL_B);
-        k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s);
+        k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s, ALL_ROWS);
         CK(cudaGetLastError());
     }
     if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
-    {
-        ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - (double)s->L.xsz * s->L.n : -1.0);
-        s->next_xzero = false;
-        if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
-        else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
-        CK(cudaGetLastError());
-    }
-    return finalize<MODE, W_C>(s, 0);
+    return update_and_reduce<MODE>(s, v);
 }
 
 template <int MODE>
@@ -662,11 +752,17 @@ int iteration(eg_solver* s, void* x_it) {
         }
         CK(cudaGetLastError());
     }
-    if ((rc = halo_ghosted(s, v.z))) return rc;
     {
         ProfScope ps(s, KID_STENCIL_A);
-        k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh);
-        CK(cudaGetLastError());
+        if (s->nranks > 1) {  // interior rows while the ghost rows travel, then the band-edge rows
+            if ((rc = halo_ghosted(s, v.z, true))) return rc;
+            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, false))) return rc;
+            if ((rc = halo_join(s))) return rc;
+            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true))) return rc;
+        } else {
+            k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh, ALL_ROWS);
+            CK(cudaGetLastError());
+        }
     }
     if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
     {
@@ -684,21 +780,20 @@ int iteration(eg_solver* s, void* x_it) {
         }
         CK(cudaGetLastError());
     }
-    if ((rc = halo_ghosted(s, v.zs))) return rc;
     {
         ProfScope ps(s, KID_STENCIL_B);
-        k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s);
-        CK(cudaGetLastError());
+        if (s->nranks > 1) {
+            if ((rc = halo_ghosted(s, v.zs, true))) return rc;
+            if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, false))) return rc;
+            if ((rc = halo_join(s))) return rc;
+            if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true))) return rc;
+        } else {
+            k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s, ALL_ROWS);
+            CK(cudaGetLastError());
+        }
     }
     if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
-    {
-        ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - (double)s->L.xsz * s->L.n : -1.0);
-        s->next_xzero = false;
-        if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
-        else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
-        CK(cudaGetLastError());
-    }
-    if ((rc = finalize<MODE, W_C>(s, 0))) return rc;
+    if ((rc = update_and_reduce<MODE>(s, v))) return rc;
     (void)sizeof(V);
     return EG_OK;
 }
@@ -1007,7 +1102,7 @@ int apply_impl(eg_solver* s, const void* x, void* y) {
     }
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     ProfScope ps(s, KID_APPLY);
-    k_stencil<MODE, 0><<<gr, RW, 0, s->st>>>(s->geo, v, zin, (V*)y, nullptr);
+    k_stencil<MODE, 0><<<gr, RW, 0, s->st>>>(s->geo, v, zin, (V*)y, nullptr, ALL_ROWS);
     CK(cudaGetLastError());
     return EG_OK;
 }
@@ -1392,6 +1487,15 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
         if (rc == EG_OK && r == ncclSuccess) r = ncclCommInitRank(&s->comm, s->nranks, id, s->rank);
         if (r != ncclSuccess) rc = fail(s, EG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
     }
+    if (rc == EG_OK && (s->comm || s->lb)) {  // latitude bands: the overlap streams and events
+        if (cudaStreamCreateWithFlags(&s->cst, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&s->xst, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_edge, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_halo, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_b, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_xu, cudaEventDisableTiming) != cudaSuccess)
+            rc = fail(s, EG_ERR_CUDA, "overlap streams / events");
+    }
     if (rc == EG_OK) {  // fused marching phases (march.cuh): fp32 vectors, one GPU; EG_NO_FUSE=1 disables
         const char* nf = getenv("EG_NO_FUSE");
         int dev = 0, nsm = 0;
@@ -1424,7 +1528,11 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
                 s->mg.fst_b = std::min(MA_MAX_STAGES, atoi(fb));
                 s->mg.sst_b = std::min(MA_MAX_STAGES, nb - atoi(fb));
             }
-            s->mg.strips = (int)std::min<int64_t>(s->L.nyl, nsm / s->L.tiles);
+            // with NCCL ranks, leave a few SMs to the ghost-row exchange that runs beside the phase kernel
+            const int sms = (s->comm && s->nranks > 1) ? std::max(s->L.tiles, nsm - 4) : nsm;
+            s->mg.strips = (int)std::min<int64_t>(s->L.nyl, sms / s->L.tiles);
+            s->mg.skip_lo = s->rank > 0;
+            s->mg.skip_hi = s->rank < s->nranks - 1;
             const char* fs = getenv("EG_MARCH_STRIPS");  // tests: fewer, longer strips
             if (fs && atoi(fs) >= 1) s->mg.strips = std::min(s->mg.strips, atoi(fs));
             // tests only: more strips than SMs (a grid that cannot be co-resident; the cooperative
@@ -1640,6 +1748,10 @@ void eg_solver_destroy(eg_solver* s) {
     if (s->cap_st) cudaStreamDestroy(s->cap_st);
     if (s->cin) cudaStreamDestroy(s->cin);
     if (s->cout) cudaStreamDestroy(s->cout);
+    if (s->cst) cudaStreamDestroy(s->cst);
+    if (s->xst) cudaStreamDestroy(s->xst);
+    for (cudaEvent_t e : {s->ev_edge, s->ev_halo, s->ev_b, s->ev_xu})
+        if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
         if (s->ev_in[i]) cudaEventDestroy(s->ev_in[i]);
         if (s->ev_x[i]) cudaEventDestroy(s->ev_x[i]);

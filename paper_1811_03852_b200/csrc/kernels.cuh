@@ -111,15 +111,23 @@ __device__ __forceinline__ void block_sum_d(double (&v)[NQ], double* sm, uint32_
 
 template <int NQ>
 __device__ __forceinline__ void write_slots(const Geo& g, double* slots, double (&acc)[NQ],
-                                            uint32_t r32) {
+                                            uint32_t r32, int64_t row = -1) {
     __shared__ double sm[32 * NQ];
     block_sum_d<NQ>(acc, sm, r32);
     if (threadIdx.x == 0) {
         const int64_t per_q = g.nyl * g.tiles;
+        const int64_t jl = row >= 0 ? row : (int64_t)blockIdx.y;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) slots[q * per_q + blockIdx.y * g.tiles + blockIdx.x] = acc[q];
+        for (int q = 0; q < NQ; ++q) slots[q * per_q + jl * g.tiles + blockIdx.x] = acc[q];
     }
 }
+
+// the local rows a row-tiled launch covers: row = lo + blockIdx.y * step (all rows: {0, 1}; the
+// band-edge rows of a latitude band: {0, nyl - 1}; the interior: {1, 1})
+struct RowMap {
+    int lo, step;
+};
+constexpr RowMap ALL_ROWS{0, 1};
 
 // product of two V values summed into an S accumulator held as double (exact product for fp32
 // operands; FP32 mode rounds product and sum to binary32 like the oracle)
@@ -974,7 +982,7 @@ template <int MODE, int DOTS>
 __global__ void __launch_bounds__(RW, 4) k_stencil(Geo g, Vecs<MODE> vv,
                                                 const typename Prec<MODE>::V* __restrict__ z,
                                                 typename Prec<MODE>::V* __restrict__ y,
-                                                const typename Prec<MODE>::V* __restrict__ aux) {
+                                                const typename Prec<MODE>::V* __restrict__ aux, RowMap rm) {
     using V = typename Prec<MODE>::V;
     if (DOTS != 0 && vv.st->halt != H_RUN) return;
     constexpr int NQ = DOTS == 2 ? 3 : 1;
@@ -984,7 +992,7 @@ __global__ void __launch_bounds__(RW, 4) k_stencil(Geo g, Vecs<MODE> vv,
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
     const int i = blockIdx.x * RW + threadIdx.x;
-    const int64_t jl = blockIdx.y, jg = g.j0 + jl;
+    const int64_t jl = rm.lo + (int64_t)blockIdx.y * rm.step, jg = g.j0 + jl;
     if (i < g.nx) {
         const int nx = (int)g.nx, nz = (int)g.nz;
         const int64_t rb = jl * g.row;
@@ -1064,24 +1072,30 @@ __global__ void __launch_bounds__(RW, 4) k_stencil(Geo g, Vecs<MODE> vv,
             zup_c = zup_n;
         }
     }
-    if (DOTS != 0) write_slots<NQ>(g, vv.slots, acc, MODE == 2 ? 0x7u : 0x0u);
+    if (DOTS != 0) write_slots<NQ>(g, vv.slots, acc, MODE == 2 ? 0x7u : 0x0u, jl);
 }
 
 // ---------------------------------------------------------------------------------------------
 // a9: x += alpha z + omega z_s (X precision, scalars unrounded, A-10); r = s - omega t;
 // partials rhat0 . r, r . r.  On an s-step exit only x += alpha z.  CPT columns per thread,
 // double-buffered register batches of KB levels.  grid (tiles, nyl), block RW / CPT.
-template <int MODE, int CPT>
+// PART 0: both updates.  Latitude bands split it so that the x half runs beside reduction 3
+// (its all-gather) on a side stream: PART 1 = r and its partials, PART 2 = x only, which reads the
+// control snapshot reduction 2 left (xs_*), because reduction 3 rewrites halt / sexit / xzero
+// while it runs.  The arithmetic of each half is PART 0's.
+template <int MODE, int CPT, int PART = 0>
 __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
     using V = typename Prec<MODE>::V;
     using X = typename Prec<MODE>::X;
     constexpr int KB = (sizeof(V) == 4 ? 8 : 4) / CPT > 0 ? (sizeof(V) == 4 ? 8 : 4) / CPT : 1;
+    constexpr bool DO_X = PART != 1, DO_R = PART != 2;
     using VC = VecN<V, CPT>;
     using XC = VecN<X, CPT>;
     const DevState* st = vv.st;
-    if (st->halt != H_RUN) return;
-    const bool sexit = st->sexit != 0;
-    const bool xz = st->xzero != 0;  // x = 0 (not stored): the first update after an x0 = 0 entry
+    if (PART == 2 ? st->xs_run == 0 : st->halt != H_RUN) return;
+    const bool sexit = (PART == 2 ? st->xs_sexit : st->sexit) != 0;
+    const bool xz = (PART == 2 ? st->xs_xzero : st->xzero) != 0;  // x = 0 (not stored): first update after x0 = 0
+    if (PART == 1 && sexit) return;
     const X alpha = (X)st->alpha, omega = (X)st->omega;
     const V omega_v = (V)st->omega_v;
     double acc[2] = {0.0, 0.0};
@@ -1096,7 +1110,7 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
         const V* __restrict__ tp = vv.t + base;
         const V* __restrict__ rhp = vv.rh + base;
         V* __restrict__ rp = vv.r + base;
-        if (sexit) {
+        if (sexit) {  // (PART 0 / 2)
             for (int k = 0; k < nz; ++k) {
                 XC xv;
 #pragma unroll
@@ -1124,16 +1138,19 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
 #pragma unroll
                 for (int e = 0; e < KB; ++e) {
                     const int o = min(k0 + e, nz - 1) * nx;  // tail levels re-read the last one
-                    if (!xz) x_[e] = ldv<CPT>(xp + o);  // else stays 0
-                    z_[e] = ldv<CPT>(zp + o); zs_[e] = ldv<CPT>(zsp + o);
-                    s_[e] = ldv<CPT>(sp + o); t_[e] = ldv<CPT>(tp + o); rh_[e] = ldv<CPT>(rhp + o);
+                    if (DO_X) {
+                        if (!xz) x_[e] = ldv<CPT>(xp + o);  // else stays 0
+                        z_[e] = ldv<CPT>(zp + o); zs_[e] = ldv<CPT>(zsp + o);
+                    }
+                    if (DO_R) { s_[e] = ldv<CPT>(sp + o); t_[e] = ldv<CPT>(tp + o); rh_[e] = ldv<CPT>(rhp + o); }
                     if (UP_PF > 0 && k0 + e + UP_PF < nz) {  // warp-uniform
                         const int of = (k0 + e + UP_PF) * nx;
                         const int l = threadIdx.x & 31;
                         if ((l * CPT * (int)sizeof(V)) % 32 == 0) {
-                            pf_l2(zp + of); pf_l2(zsp + of); pf_l2(sp + of); pf_l2(tp + of); pf_l2(rhp + of);
+                            if (DO_X) { pf_l2(zp + of); pf_l2(zsp + of); }
+                            if (DO_R) { pf_l2(sp + of); pf_l2(tp + of); pf_l2(rhp + of); }
                         }
-                        if ((l * CPT * (int)sizeof(X)) % 32 == 0) pf_l2(xp + of);
+                        if (DO_X && (l * CPT * (int)sizeof(X)) % 32 == 0) pf_l2(xp + of);
                     }
                 }
             };
@@ -1149,13 +1166,15 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
                         VC rv;
 #pragma unroll
                         for (int c = 0; c < CPT; ++c) {
-                            xv.v[c] = fma(omega, (X)czs[e].v[c], fma(alpha, (X)cz[e].v[c], cx[e].v[c]));
-                            rv.v[c] = fma(-omega_v, ct[e].v[c], cs[e].v[c]);
-                            acc_dot<MODE>(acc[0], crh[e].v[c], rv.v[c]);
-                            acc_dot<MODE>(acc[1], rv.v[c], rv.v[c]);
+                            if (DO_X) xv.v[c] = fma(omega, (X)czs[e].v[c], fma(alpha, (X)cz[e].v[c], cx[e].v[c]));
+                            if (DO_R) {
+                                rv.v[c] = fma(-omega_v, ct[e].v[c], cs[e].v[c]);
+                                acc_dot<MODE>(acc[0], crh[e].v[c], rv.v[c]);
+                                acc_dot<MODE>(acc[1], rv.v[c], rv.v[c]);
+                            }
                         }
-                        stv<CPT>(xp + o, xv);
-                        stv<CPT>(rp + o, rv);
+                        if (DO_X) stv<CPT>(xp + o, xv);
+                        if (DO_R) stv<CPT>(rp + o, rv);
                     }
                 }
 #pragma unroll
@@ -1165,7 +1184,7 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
             }
         }
     }
-    if (!sexit) write_slots<2>(g, vv.slots, acc, MODE == 2 ? 0x3u : 0x0u);
+    if (DO_R && !sexit) write_slots<2>(g, vv.slots, acc, MODE == 2 ? 0x3u : 0x0u);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1396,6 +1415,14 @@ __device__ __forceinline__ void fin_logic(const Geo& g, const double* __restrict
     }
 }
 
+// after reduction 2 (W_B): the control state the x half of a split update (k_update PART 2) runs on,
+// which reduction 3 does not touch (it rewrites halt / sexit / xzero while that half may still run)
+__device__ __forceinline__ void x_snapshot(DevState* st) {
+    st->xs_run = st->halt == H_RUN;
+    st->xs_sexit = st->sexit;
+    st->xs_xzero = st->xzero;
+}
+
 // single-GPU finaliser: groups + logic in one CTA (1024 threads)
 template <int MODE, int WHICH>
 __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __restrict__ slots, DevState* st,
@@ -1408,7 +1435,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __rest
     // CTA has read them) writes the state, so every CTA takes the same branch
     const int halt0 = *(volatile const int*)&st->halt;
     const int sexit0 = *(volatile const int*)&st->sexit;
-    if (WHICH != W_START && WHICH != W_VERIFY && halt0 != H_RUN) return;  // (then nobody writes)
+    if (WHICH != W_START && WHICH != W_VERIFY && halt0 != H_RUN) {  // (then nobody writes)
+        if (WHICH == W_B && blockIdx.x == 0 && threadIdx.x == 0) x_snapshot(st);
+        return;
+    }
     // s-step exit (W_C): no sums needed, but every CTA still arrives so that the counter is reset
     if (!(WHICH == W_C && sexit0)) fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
     __shared__ int last;
@@ -1422,6 +1452,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __rest
         __threadfence();
         st->fin_ctr = 0;
         fin_logic<MODE, WHICH>(g, gsum, st, first);
+        if (WHICH == W_B) x_snapshot(st);
     }
 }
 
@@ -1439,7 +1470,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin_groups(Geo g, const double*
 template <int MODE, int WHICH>
 __global__ void k_fin_logic(Geo g, const double* __restrict__ gall, DevState* st, int first) {
     if (threadIdx.x == 0) { st->epoch += 1; }
-    if (threadIdx.x == 0) fin_logic<MODE, WHICH>(g, gall, st, first);
+    if (threadIdx.x == 0) {
+        fin_logic<MODE, WHICH>(g, gall, st, first);
+        if (WHICH == W_B) x_snapshot(st);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------

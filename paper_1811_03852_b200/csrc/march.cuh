@@ -29,7 +29,9 @@
 // The producer issues one TMA box (128 columns x MA_KB levels) per array per stage.
 // Requires: nx % 4 == 0 (16-byte TMA strides), 7 * ceil8(nz) <= 512 TMEM columns, tiles <= #SMs.
 // Multi-GPU: the band's first / last rows' neighbours are the ghost rows -1 / nyl of z, which the
-// host fills (k_edge_rows + NCCL) before the launch.
+// exchange (k_edge_rows + NCCL on a communication stream) fills WHILE this kernel runs: the stencil
+// of those two rows (which read them) is computed but not stored (MarchGeo.skip_lo / skip_hi), and
+// k_stencil redoes the two rows after the exchange, bitwise the same arithmetic.
 #pragma once
 #include <cuda.h>  // CUtensorMap (the host encodes the maps through cudaGetDriverEntryPointByVersion)
 
@@ -213,6 +215,9 @@ struct MarchGeo {
     int strips;                  // latitude strips; grid = strips * tiles CTAs
     int fst_a, sst_a;            // phase A: stages of the elimination / stencil input rings
     int fst_b, sst_b;            // phase B
+    int skip_lo, skip_hi;        // latitude bands: local row 0 / nyl-1 has a neighbouring rank, whose
+                                 // ghost row arrives during the launch: its stencil is not stored
+                                 // here (k_stencil on the edge rows redoes it after the exchange)
 };
 constexpr int MA_MAX_CH = 9;     // chunks per column (nz <= 72)
 
@@ -583,6 +588,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             const float* zN = zN0 + 1 + col;
             const float* zS = zS0 + 1 + col;
             V* yw = Yw + (int64_t)j * g.row + i;
+            const bool keep = !((j == 0 && mg.skip_lo) || (j == nyl - 1 && mg.skip_hi));  // warp-uniform
             const int us = m & 1;
             double acc[NQ];
 #pragma unroll
@@ -658,7 +664,8 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
                     }
                 }
                 V* yk = yw + (int64_t)k0 * nx;
-                if (uni && k0 + KB <= nz) {
+                if (!keep) {
+                } else if (uni && k0 + KB <= nz) {
 #pragma unroll
                     for (int e = 0; e < KB; ++e) __stcg(yk + e * nx, av[e]);
                 } else {
@@ -670,7 +677,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             MA_ADD(6, t_st);
             MA_CLK(t_red);
             cons_sum_d<NQ>(acc, red, MODE == 2 ? 0x7u : 0x0u);  // contains cons_bar()
-            if (tid == 0) {
+            if (tid == 0 && keep) {
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) vv.slots[q * per_q + (int64_t)j * T + t] = acc[q];
             }
