@@ -1276,14 +1276,27 @@ __device__ __forceinline__ void fin_group_par(const Geo& g, const double* __rest
     const int gi = g.g_lo + gl;
     const int64_t rb = (int64_t)gi * g.ny / g.G - g.j0, re = (int64_t)(gi + 1) * g.ny / g.G - g.j0;
     const int64_t L = (re - rb) * g.tiles;
+    // a chain's slots are loaded FB at a time (independent loads in flight), then added in order
+    constexpr int FB = 8;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const double* src = slots + (int64_t)q * g.nyl * g.tiles + rb * g.tiles;
         const bool f = (r32 >> q) & 1u;
         double ac = 0.0;
-        for (int64_t e = lane + 32 * c; e < L; e += 32 * FC) {
-            ac += src[e];
-            if (f) ac = (double)(float)ac;
+        for (int64_t e0 = lane + 32 * c; e0 < L; e0 += (int64_t)32 * FC * FB) {
+            double v[FB];
+#pragma unroll
+            for (int u = 0; u < FB; ++u) {
+                const int64_t e = e0 + (int64_t)32 * FC * u;
+                v[u] = e < L ? src[e] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < FB; ++u) {
+                if (e0 + (int64_t)32 * FC * u < L) {
+                    ac += v[u];
+                    if (f) ac = (double)(float)ac;
+                }
+            }
         }
         chain[q][c][lane] = ac;
     }

@@ -47,8 +47,7 @@ for P in [int(a) for a in (args or ["1", "2", "4", "8"])]:
         s.profile_reset()
         s.solve(b, tol=0.0, maxit=8, out=x, flags=egs.EG_SOLVE_PROFILE)
         p = s.profile()
-        ks = ("phase_A", "phase_B") if p["phase_A"][1] else ("thomas_p", "stencil_dot_A")
-        kt = " ".join(f"{k} {p[k][0] / max(p[k][1], 1):.3f}" for k in ks)
+        kt = " ".join(f"{k} {p[k][0] / p[k][1]:.4f}" for k in p if p[k][1] > 0)
         print(f"P={P} ({prob.nx}x{prob.ny}x{prob.nz}) {name:18s}: solve(8) {best:.3f} ms, "
               f"{best / 8 * P:.3f} ms x P per iteration; {kt}", flush=True)
         s.close()
