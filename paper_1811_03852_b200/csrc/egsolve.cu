@@ -24,6 +24,7 @@
 #include "kernels.cuh"
 #include "march.cuh"
 #include "sor_tma.cuh"
+#include "march64.cuh"
 
 using namespace eg;
 
@@ -41,7 +42,7 @@ const char* kKernelNames[KID_COUNT] = {"scale", "start", "finalize", "thomas_p",
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-    size_t off_bands, off_diag, off_bhat, off_x64, off_x32, off_xg, off_vec, off_z, off_pv, off_slots,
+    size_t off_bands, off_diag, off_bhat, off_x64, off_x32, off_xg, off_vec, off_z, off_pv, off_slots, off_hslots,
         off_gsum, off_state, base_total, off_split, off_batch, total;
     size_t vsz;      // sizeof(V)
     size_t xsz;      // sizeof(X)
@@ -71,9 +72,12 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t fe
     L->off_xg = o;    o = align_up(o + 2 * row * 8, A);
     L->off_vec = o;   o = align_up(o + 6 * align_up(n * L->vsz, A), A);
     L->off_z = o;     o = align_up(o + 2 * align_up((n + 2 * row) * L->vsz, A), A);
-    L->off_pv = o;    o = align_up(o + (size_t)nyl * L->tiles * sizeof(int), A);  // ready flags of the fused phases
+    // ready flags of the fused phases: one per (row, tile) of 128 (fp32) or 64 (FP64) columns
+    L->off_pv = o;    o = align_up(o + (size_t)nyl * ((g->nx + 63) / 64) * sizeof(int), A);
     // reduction slots per row: 128-column tiles (unfused kernels) or 64-longitude strips (phases)
     L->off_slots = o; o = align_up(o + 3 * (size_t)nyl * L->tiles * 8, A);
+    // FP64 phase kernels: 4 warp sums per (row, 128-column slot) (march64.cuh)
+    L->off_hslots = o; o = align_up(o + (mode == EG_FP64 ? 3 * 4 * (size_t)nyl * L->tiles * 8 : 0), A);
     L->off_gsum = o;  o = align_up(o + 2 * 8 * 3 * 8, A);
     L->off_state = o; o = align_up(o + sizeof(DevState), A);
     L->base_total = o;
@@ -183,6 +187,8 @@ struct eg_solver {
     int sor_sweeps = 3;
     double sor_omega = 1.5;
     double* slots = nullptr;
+    double* hslots = nullptr;    // FP64 phase kernels' half-slots [3][nyl][tiles][4]
+    MarchMaps64 maps64{};        // TMA maps of the FP64 phase kernels
     double* gsum = nullptr;  // [G][3] local
     double* gall = nullptr;  // [G][3] all ranks
     DevState* dstate = nullptr;
@@ -435,18 +441,21 @@ int stencil_rows(eg_solver* s, const typename Prec<MODE>::V* z, typename Prec<MO
     return EG_OK;
 }
 
+// quad: the slots are the FP64 phase kernels' half-slots (4 warp sums each, Geo.quad)
 template <int MODE, int WHICH>
-int finalize(eg_solver* s, int first, int tiles = 0) {
+int finalize(eg_solver* s, int first, int tiles = 0, bool quad = false) {
     ProfScope ps(s, KID_FIN);
     Geo geo = s->geo;
     if (tiles > 0) geo.tiles = tiles;  // slots per row of the producing kernel
+    geo.quad = quad ? 1 : 0;
+    const double* slots = quad ? s->hslots : s->slots;
     if (!multi(s)) {  // one GPU: group sums and logic in one CTA
-        k_fin<MODE, WHICH><<<(unsigned)(geo.g_hi - geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum, first);
+        k_fin<MODE, WHICH><<<(unsigned)(geo.g_hi - geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, slots, s->dstate, s->gsum, first);
         CK(cudaGetLastError());
         return EG_OK;
     }
     constexpr int NQ = fin_nq(WHICH);
-    k_fin_groups<MODE, WHICH><<<(unsigned)(s->geo.g_hi - s->geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, s->slots, s->dstate, s->gsum);
+    k_fin_groups<MODE, WHICH><<<(unsigned)(s->geo.g_hi - s->geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, slots, s->dstate, s->gsum);
     CK(cudaGetLastError());
     const int gl = s->geo.g_hi - s->geo.g_lo;
     if (s->lb) {  // all-gather: rank r's block lands at gall + r * gl * NQ, as ncclAllGather places it
@@ -611,6 +620,22 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
 #endif
         if ((rc = finalize<MODE, W_B>(s, 0))) return rc;
+        if ((rc = update_and_reduce<MODE>(s, v))) return rc;
+    } else {  // FP64: march64.cuh (64-column tiles, half-slot dot partials), one GPU
+        const unsigned grid = (unsigned)(s->mg.strips * ((s->grid.nx + M6_TILE - 1) / M6_TILE));
+        {
+            ProfScope ps(s, KID_PHASE_A, s->next_fresh ? alg_bytes(s, KID_PHASE_A) - 2.0 * s->L.vsz * s->L.n : -1.0);
+            s->next_fresh = false;
+            CK(launch_coop(k_march64<1>, grid, M6_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
+                           s->hslots, s->maps64));
+        }
+        if ((rc = finalize<MODE, W_A>(s, 0, 0, true))) return rc;
+        {
+            ProfScope ps(s, KID_PHASE_B);
+            CK(launch_coop(k_march64<2>, grid, M6_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
+                           s->hslots, s->maps64));
+        }
+        if ((rc = finalize<MODE, W_B>(s, 0, 0, true))) return rc;
         if ((rc = update_and_reduce<MODE>(s, v))) return rc;
     }
     return EG_OK;
@@ -1207,6 +1232,24 @@ bool make_march_maps(eg_solver* s) {
     return ok;
 }
 
+bool make_march_maps64(eg_solver* s) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return false;
+    EncodeTiledFn enc = (EncodeTiledFn)fn;
+    const int64_t nx = s->grid.nx, nz = s->grid.nz, nyl = s->L.nyl;
+    MarchMaps64& m = s->maps64;
+    bool ok = encode_map_box(enc, &m.r, s->vec[0], nx, nz, nyl, 8, M6_TILE, M6_KS);
+    ok = ok && encode_map_box(enc, &m.rh, s->vec[1], nx, nz, nyl, 8, M6_TILE, M6_KS);
+    ok = ok && encode_map_box(enc, &m.p, s->vec[2], nx, nz, nyl, 8, M6_TILE, M6_KS);
+    ok = ok && encode_map_box(enc, &m.v, s->vec[3], nx, nz, nyl, 8, M6_TILE, M6_KS);
+    ok = ok && encode_map_box(enc, &m.b2, s->B2, 2 * nx, nz, nyl, 8, 2 * M6_TILE, M6_KS);  // (U, D)
+    ok = ok && encode_map_box(enc, &m.b4, s->B4, 4 * nx, nz, nyl, 8, 4 * M6_TILE, M6_KS);  // (E, W, N, S)
+    return ok;
+}
+
 bool make_sor_maps(eg_solver* s) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1416,6 +1459,7 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
     s->split = room_split ? (void*)(s->ws + L.off_split) : nullptr;
     s->batch = room_batch ? (double*)(s->ws + L.off_batch) : nullptr;
     s->slots = (double*)(s->ws + L.off_slots);
+    s->hslots = (double*)(s->ws + L.off_hslots);
     s->gsum = (double*)(s->ws + L.off_gsum);
     s->gall = s->gsum + 8 * 3;
     s->dstate = (DevState*)(s->ws + L.off_state);
@@ -1558,6 +1602,60 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
                 rc = fail(s, EG_ERR_CUDA, "march setup: %s", cudaGetErrorString(cudaGetLastError()));
             else if (occ != 1 || !make_march_maps(s))  // co-residency of every CTA makes the flag waits safe
                 s->use_march = false;
+        }
+    }
+    if (rc == EG_OK && prec == EG_FP64 && !(s->comm || s->lb)) {
+        // FP64 fused phases (march64.cuh): one GPU, nx even, 6 ceil4(nz) <= 512 TMEM columns, 64-column
+        // tiles <= #SMs; EG_NO_FUSE=1 disables, EG_FUSE=1 forces below 2^18 points
+        const char* nf = getenv("EG_NO_FUSE");
+        const char* ff = getenv("EG_FUSE");
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t nz4 = (grid->nz + M6_KS - 1) / M6_KS * M6_KS;
+        const int t64 = (int)((grid->nx + M6_TILE - 1) / M6_TILE);
+        const size_t ring = 3 * (size_t)nz4 * M6_RING_W * sizeof(double);
+        const size_t budget = 227 * 1024 - 4096 - 128;  // dynamic + static shared memory per CTA
+        const bool big = s->L.n >= (int64_t)1 << 18 || (ff && ff[0] == '1');
+        bool ok = grid->nx % 2 == 0 && nz4 <= M6_MAX_NZ4 && t64 <= nsm && ring < budget && big && !(nf && nf[0] == '1');
+        if (ok) {
+            // stage rings: as many stencil stages as elimination ones, the rest to the elimination ring
+            auto split = [&](int kind, int* nf_, int* ns_) {
+                const size_t room = budget - ring;
+                const int ns = (int)std::min<size_t>(M6_MAX_STAGES, room / (m6_f_bytes(kind) + m6_s_bytes(kind)));
+                const int nfs = (int)std::min<size_t>(M6_MAX_STAGES, (room - ns * (size_t)m6_s_bytes(kind)) / m6_f_bytes(kind));
+                *nf_ = nfs;
+                *ns_ = ns;
+            };
+            split(1, &s->mg.fst_a, &s->mg.sst_a);
+            split(2, &s->mg.fst_b, &s->mg.sst_b);
+            ok = s->mg.fst_a >= 2 && s->mg.sst_a >= 2 && s->mg.fst_b >= 2 && s->mg.sst_b >= 2;
+        }
+        // 64-column tiles x strips must keep >= 90 % of the SMs busy: one CTA per SM moves ~1/nsm of the
+        // bandwidth, and the fused kernel saves only 18 % of the 5-kernel bytes (measured: C4, 24 x 6 =
+        // 144 CTAs, 6 % faster; C5, 40 x 3 = 120 CTAs, 5 % slower).  EG_FUSE=1 forces it.
+        const int64_t ctas = (int64_t)t64 * std::min<int64_t>(s->L.nyl, nsm / t64);
+        if (ok && !(ff && ff[0] == '1') && ctas * 10 < (int64_t)nsm * 9) ok = false;
+        if (ok) {
+            s->mg.strips = (int)std::min<int64_t>(s->L.nyl, nsm / t64);
+            const char* fs = getenv("EG_MARCH_STRIPS");
+            if (fs && atoi(fs) >= 1) s->mg.strips = std::min(s->mg.strips, atoi(fs));
+            const char* fo = getenv("EG_MARCH_STRIPS_UNSAFE");
+            if (fo && atoi(fo) >= 1) s->mg.strips = (int)std::min<int64_t>(s->L.nyl, atoi(fo));
+            s->mg.skip_lo = s->mg.skip_hi = 0;
+            const size_t st_a = (size_t)s->mg.fst_a * m6_f_bytes(1) + (size_t)s->mg.sst_a * m6_s_bytes(1);
+            const size_t st_b = (size_t)s->mg.fst_b * m6_f_bytes(2) + (size_t)s->mg.sst_b * m6_s_bytes(2);
+            s->smem_march = std::max<size_t>(std::max(st_a, st_b) + ring + 128, 116 * 1024);
+            int occ = 0;
+            cudaError_t e1 = cudaFuncSetAttribute(k_march64<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_march);
+            cudaError_t e2 = cudaFuncSetAttribute(k_march64<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_march);
+            cudaError_t e3 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_march64<1>, M6_THREADS, s->smem_march);
+            cudaError_t e4 = cudaMemsetAsync(s->ready_flags, 0, (size_t)s->L.nyl * t64 * sizeof(int), s->st);
+            cudaError_t e5 = cudaMemsetAsync(s->hslots, 0, 3 * 4 * (size_t)s->L.nyl * s->L.tiles * sizeof(double), s->st);
+            if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess || e5 != cudaSuccess)
+                rc = fail(s, EG_ERR_CUDA, "FP64 march setup: %s", cudaGetErrorString(cudaGetLastError()));
+            else
+                s->use_march = occ == 1 && make_march_maps64(s);
         }
     }
     // The TMA box of the colour-split f starts at column nx/2 for the second colour: a TMA box must

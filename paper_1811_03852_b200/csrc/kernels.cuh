@@ -34,6 +34,8 @@ struct Geo {
     int64_t n;           // nyl*row
     int tiles;           // 128-column tiles per row (= reduction slots per row)
     int G, g_lo, g_hi;   // reduction row-groups: all, and this rank's [g_lo, g_hi)
+    int quad;            // finalisers: each slot is 4 warp sums ((w0 + w1) + w2) + w3 (the FP64 phase
+                         // kernels' 64-column half-slots, march64.cuh)
 };
 
 constexpr int RW = 128;  // columns per CTA of the row-tiled kernels (one reduction slot each)
@@ -1276,11 +1278,12 @@ __device__ __forceinline__ void fin_group_par(const Geo& g, const double* __rest
     const int gi = g.g_lo + gl;
     const int64_t rb = (int64_t)gi * g.ny / g.G - g.j0, re = (int64_t)(gi + 1) * g.ny / g.G - g.j0;
     const int64_t L = (re - rb) * g.tiles;
+    const int sw = g.quad ? 4 : 1;  // doubles per slot
     // a chain's slots are loaded FB at a time (independent loads in flight), then added in order
     constexpr int FB = 8;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        const double* src = slots + (int64_t)q * g.nyl * g.tiles + rb * g.tiles;
+        const double* src = slots + ((int64_t)q * g.nyl * g.tiles + rb * g.tiles) * sw;
         const bool f = (r32 >> q) & 1u;
         double ac = 0.0;
         for (int64_t e0 = lane + 32 * c; e0 < L; e0 += (int64_t)32 * FC * FB) {
@@ -1288,7 +1291,14 @@ __device__ __forceinline__ void fin_group_par(const Geo& g, const double* __rest
 #pragma unroll
             for (int u = 0; u < FB; ++u) {
                 const int64_t e = e0 + (int64_t)32 * FC * u;
-                v[u] = e < L ? src[e] : 0.0;
+                if (e >= L) {
+                    v[u] = 0.0;
+                } else if (sw == 4) {  // k_stencil's CTA order over its four warps
+                    const double4 h = *reinterpret_cast<const double4*>(src + 4 * e);
+                    v[u] = ((h.x + h.y) + h.z) + h.w;
+                } else {
+                    v[u] = src[e];
+                }
             }
 #pragma unroll
             for (int u = 0; u < FB; ++u) {

@@ -91,8 +91,7 @@ def _same_info(a, b):
 @pytest.mark.parametrize("mode", ["mixed", "fp64", "fp32"])
 @pytest.mark.parametrize("fuse", [True, False], ids=["fused", "5kernel"])
 def test_loopback_solve_bitwise_equal_any_P(prob, mode, fuse, monkeypatch):
-    if fuse and mode == "fp64":
-        pytest.skip("the fused phases are fp32-vector kernels")
+    # (FP64: P = 1 runs the fused FP64 phase kernels, P > 1 the 5-kernel schedule: bitwise equal too)
     monkeypatch.setenv("EG_FUSE" if fuse else "EG_NO_FUSE", "1")
     ref = Bands(prob, mode, 1)
     P_list = [p for p in (2, 4, 8) if min(8, prob.ny) % p == 0]

@@ -82,7 +82,7 @@ def test_precondition_parity(prob, mode):
 FUSED_ODD = gen.Problem(128, 37, 13, seed=11)   # one 128-column tile, odd ny / nz
 FUSED_THIN = gen.Problem(192, 3, 70, seed=12)   # fewer rows than the per-CTA row ranges
 # below 2^18 points the default is the 5-kernel schedule: these cases force the fused phase kernels
-# (fp32 vectors; FP64 has no fused schedule and runs the 5-kernel one regardless)
+# (march.cuh for fp32 vectors, march64.cuh for FP64)
 FORCE_FUSED = (FUSED_ODD, FUSED_THIN)
 
 
@@ -94,7 +94,7 @@ def test_solve_parity(prob, mode, tol, monkeypatch):
     fused = prob in FORCE_FUSED
     s, bands, b = _make(prob, mode, {"EG_FUSE": "1"} if fused else None, monkeypatch)
     if fused:
-        assert _uses_fused(s, torch.from_numpy(b).cuda()) == (mode != "fp64")
+        assert _uses_fused(s, torch.from_numpy(b).cuda())
     g = (prob.nx, prob.ny, prob.nz)
     ahat, diag = oracle.scale(g, bands, mode)
     xo, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=tol, maxit=200)
@@ -170,7 +170,7 @@ def test_warm_start_parity(mode, fused, monkeypatch):
     x0, _, _ = oracle.solve(g, mode, ahat, diag, 1.1 * b + 0.01, tol=0.0, maxit=2)
     bt, x0t = torch.from_numpy(b).cuda(), torch.from_numpy(x0).cuda()
     if fused:
-        assert _uses_fused(s, bt) == (mode != "fp64")
+        assert _uses_fused(s, bt)
     tol = 1e-5 if mode != "fp32" else 1e-4
     xo, ho, io = oracle.solve(g, mode, ahat, diag, b, x0=x0, tol=tol, maxit=200)
     x, info, h = s.solve(bt, x0=x0t, tol=tol, maxit=200)
@@ -328,14 +328,15 @@ MARCH_CASES = [gen.CONFIGS["C1"], RAGGED, FUSED_ODD, FUSED_THIN, gen.CONFIGS["C2
 
 
 @pytest.mark.parametrize("prob", MARCH_CASES, ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
-@pytest.mark.parametrize("mode", ["mixed", "fp32"])
+@pytest.mark.parametrize("mode", ["mixed", "fp32", "fp64"])
 @pytest.mark.parametrize("strips", [None, 1, 2, 3])
 def test_fused_phases_match_unfused_schedule(prob, mode, strips, monkeypatch):
-    """The fused marching phase kernels (march.cuh: Thomas + stencil of a latitude strip per CTA,
-    the default for fp32 vectors from 2^18 local points; EG_FUSE=1 forces them here) compute z, v, s, t with the same operations as the
-    5-kernel schedule (EG_NO_FUSE=1) and write the same reduction slots, so the solve is bitwise
-    identical, whatever the number of strips (EG_MARCH_STRIPS: one-row strips, one strip per tile
-    column, odd counts whose strips alternate direction)."""
+    """The fused marching phase kernels (march.cuh for fp32 vectors, march64.cuh for FP64: Thomas +
+    stencil of a latitude strip per CTA, the default from 2^18 local points; EG_FUSE=1 forces them
+    here) compute z, v, s, t with the same operations as the 5-kernel schedule (EG_NO_FUSE=1) and
+    write the same reduction sums (FP64: 64-column half-slots combined in k_stencil's warp order), so
+    the solve is bitwise identical, whatever the number of strips (EG_MARCH_STRIPS: one-row strips,
+    one strip per tile column, odd counts whose strips alternate direction)."""
     bands, b = gen.host(prob)
     g = (prob.nx, prob.ny, prob.nz)
     bd = torch.from_numpy(bands).cuda()
