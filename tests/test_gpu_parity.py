@@ -563,7 +563,9 @@ def test_concurrent_fused_solves_on_two_streams(monkeypatch):
                          ids=lambda p: f"{p.nx}x{p.ny}x{p.nz}")
 def test_fp64_thomas_tma_matches_tmem_kernel(prob, monkeypatch):
     """The FP64 iteration's Thomas solves on the TMA-fed kernel (k_thomas_tma64, the default for
-    nz <= 72) give bitwise the results of the TMEM-factor kernel (EG_NO_THOMAS_TMA=1)."""
+    nz <= 72) give bitwise the results of the TMEM-factor kernel (EG_NO_THOMAS_TMA=1).  (5-kernel
+    schedule: the FP64 fused phase kernels take over some of these grids by default.)"""
+    monkeypatch.setenv("EG_NO_FUSE", "1")
     bands, b = gen.host(prob)
     g = (prob.nx, prob.ny, prob.nz)
     bd = torch.from_numpy(bands).cuda()
