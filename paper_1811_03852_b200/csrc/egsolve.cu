@@ -196,6 +196,7 @@ struct eg_solver {
     void* hstate_dev = nullptr;  // its device address
     int wth = 128;               // Thomas CTA width (columns)
     int cpt = 1;                 // columns per thread of the Thomas / update kernels (2 if nx even)
+    bool update_kb2 = false;     // k_update with 2-level batches (more CTAs per SM; few-wave grids)
     size_t smem_th = 0;
     bool use_tm = false;         // fp32 Thomas with TMEM-resident factors (nz <= 128)
     bool use_tm64 = false;       // fp64 Thomas with TMEM-resident factors (nz <= 80)
@@ -513,7 +514,8 @@ int update_and_reduce(eg_solver* s, Vecs<MODE>& v) {
     if (!multi(s)) {
         ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - xz_bytes : -1.0);
         s->next_xzero = false;
-        if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
+        if (s->cpt == 2 && s->update_kb2) k_update<MODE, 2, 0, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
+        else if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
         else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
         CK(cudaGetLastError());
         return finalize<MODE, W_C>(s, 0);
@@ -1480,6 +1482,15 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
     while (s->wth > 32 && 2 * (size_t)grid->nz * s->wth * L.vsz > 77824) s->wth /= 2;
     s->smem_th = 2 * (size_t)grid->nz * s->wth * L.vsz;
     s->cpt = (grid->nx % 2 == 0) ? 2 : 1;
+    {
+        // grids of < ~4 waves (8 CTAs of the default update per SM): 2-level batches, 12 CTAs per SM
+        // (measured: C4 band of 144 rows -4 % update time, C3 -1 %; C4 / C5 whole grids +1 %)
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const char* ukb = getenv("EG_UPDATE_KB2");  // A/B knob: 1 = on, 0 = off
+        s->update_kb2 = ukb ? ukb[0] == '1' : (int64_t)L.tiles * L.nyl < (int64_t)4 * 8 * nsm;
+    }
     // TMEM-factor Thomas (fp32 working precision, nz <= 128); EG_NO_TMEM=1 selects the shared-memory one
     {
         const char* no_tm = getenv("EG_NO_TMEM");

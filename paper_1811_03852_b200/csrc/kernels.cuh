@@ -189,6 +189,11 @@ __global__ void __launch_bounds__(256) k_scale(Geo g, Bands7 in, V* __restrict__
 #ifndef ST_KB
 #define ST_KB 2
 #endif
+// L2 prefetch distance (levels) of k_start's operator pass (restart / verification / warm entry):
+// (measured slower at 8 / 16 / 32 levels: 0 = off)
+#ifndef START_PF
+#define START_PF 0
+#endif
 template <int MODE, bool ENTRY, bool XZERO, bool WRITE = true>
 __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double* __restrict__ b) {
     using V = typename Prec<MODE>::V;
@@ -243,6 +248,14 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
                         cb[e][4] = h2.v[0]; cb[e][5] = h2.v[1];
                         c[e][2] = (double)xc[o]; c[e][3] = (double)xE[o]; c[e][4] = (double)xW[o];
                         c[e][5] = (double)xN[o]; c[e][6] = (double)xS[o];
+                        if (START_PF > 0 && k + START_PF < nz) {  // warp-uniform
+                            const int of = (k + START_PF) * nx;
+                            const int l = threadIdx.x & 31;
+                            if ((l * (int)sizeof(X)) % 32 == 0) pf_l2(xc + of);
+                            if ((l * 8) % 32 == 0) pf_l2(bp + of);
+                            if ((l * 4 * (int)sizeof(V)) % 32 == 0) pf_l2(b4 + 4 * of);
+                            if ((l * 2 * (int)sizeof(V)) % 32 == 0) pf_l2(b2 + 2 * of);
+                        }
                     }
                 }
             }
@@ -1085,11 +1098,14 @@ __global__ void __launch_bounds__(RW, 4) k_stencil(Geo g, Vecs<MODE> vv,
 // (its all-gather) on a side stream: PART 1 = r and its partials, PART 2 = x only, which reads the
 // control snapshot reduction 2 left (xs_*), because reduction 3 rewrites halt / sexit / xzero
 // while it runs.  The arithmetic of each half is PART 0's.
-template <int MODE, int CPT, int PART = 0>
+// KBX > 0 overrides the batch depth (levels per register batch; same operations in the same order):
+// shallower batches use fewer registers, so more CTAs fit an SM when the grid is only a few waves.
+template <int MODE, int CPT, int PART = 0, int KBX = 0>
 __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
     using V = typename Prec<MODE>::V;
     using X = typename Prec<MODE>::X;
-    constexpr int KB = (sizeof(V) == 4 ? 8 : 4) / CPT > 0 ? (sizeof(V) == 4 ? 8 : 4) / CPT : 1;
+    constexpr int KB0 = (sizeof(V) == 4 ? 8 : 4) / CPT > 0 ? (sizeof(V) == 4 ? 8 : 4) / CPT : 1;
+    constexpr int KB = KBX > 0 ? KBX : KB0;
     constexpr bool DO_X = PART != 1, DO_R = PART != 2;
     using VC = VecN<V, CPT>;
     using XC = VecN<X, CPT>;
