@@ -58,6 +58,10 @@ def test_workspace_bytes_and_argument_validation(egs):
     assert nb64.value > nb.value
     bad = egs._Grid(2, 10, 10)          # nx < 3 (reading A-19)
     assert L.eg_workspace_bytes(ctypes.byref(bad), None, egs.EG_MIXED, ctypes.byref(nb)) == 1
+    for dims in ((8, 0, 4), (8, 4, 0), (-8, 4, 4), (1 << 26, 4, 64)):   # empty grids; nx*nz >= 2^31
+        bad = egs._Grid(*dims)
+        assert L.eg_workspace_bytes(ctypes.byref(bad), None, egs.EG_MIXED, ctypes.byref(nb)) == 1, dims
+    assert L.eg_workspace_bytes(ctypes.byref(g), None, 3, ctypes.byref(nb)) == 1     # unknown precision
     # decomposition must align with the 8 reduction row-groups
     d = egs._Dist(0, 960, 0, 2, None)
     assert L.eg_workspace_bytes(ctypes.byref(g), ctypes.byref(d), egs.EG_MIXED, ctypes.byref(nb)) == 0
