@@ -320,6 +320,117 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
 }
 
 // ---------------------------------------------------------------------------------------------
+// a11 verification (the true residual norm of the current x, nothing written), two columns per
+// thread (nx even): k_start<MODE, false, false, false>'s per-point arithmetic (res = bhat - Ahat x
+// with fp64 accumulation, the same operation order per point) with 16-byte loads of x, bhat and the
+// (U, D) pairs and 32 bytes of (E, W, N, S) per level, half the load instructions per byte.  Each
+// thread sums its two columns level by level (a fixed order; the sum differs from the one-column
+// kernel's only in rounding).  grid (tiles, nyl), RW / 2 threads.
+template <int MODE>
+__global__ void __launch_bounds__(RW / 2) k_verify2(Geo g, Vecs<MODE> vv) {
+    using V = typename Prec<MODE>::V;
+    using X = typename Prec<MODE>::X;
+    constexpr int KB = 2;
+    double acc[3] = {0.0, 0.0, 0.0};
+    const int i = blockIdx.x * RW + 2 * threadIdx.x;
+    const int64_t jl = blockIdx.y, jg = g.j0 + jl;
+    if (i < g.nx) {
+        const int nx = (int)g.nx, nz = (int)g.nz;
+        const int64_t rb = jl * g.row;
+        const int iE = (i + 2 == nx) ? 0 : i + 2, iW = (i == 0) ? nx - 1 : i - 1;
+        const X* __restrict__ xc = vv.x + rb + i;
+        const X* __restrict__ xE = vv.x + rb + iE;
+        const X* __restrict__ xW = vv.x + rb + iW;
+        const X* __restrict__ xN = (jg == g.ny - 1) ? xc : (jl + 1 < g.nyl ? xc + g.row : vv.xg_hi + i);
+        const X* __restrict__ xS = (jg == 0) ? xc : (jl > 0 ? xc - g.row : vv.xg_lo + i);
+        const V* __restrict__ b4 = vv.B4 + 4 * (rb + i);
+        const V* __restrict__ b2 = vv.B2 + 2 * (rb + i);
+        const double* __restrict__ bp = vv.bhat + rb + i;
+        // per level: bhat[2], x[2], xE, xW, xN[2], xS[2] (fp64) and 2 x 6 bands (working precision)
+        double cd[KB][10], nd[KB][10];
+        V cb[KB][12], nb[KB][12];
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+#pragma unroll
+            for (int a = 0; a < 10; ++a) cd[e][a] = nd[e][a] = 0.0;
+#pragma unroll
+            for (int a = 0; a < 12; ++a) cb[e][a] = nb[e][a] = (V)0;
+        }
+        double xup_c[2] = {0.0, 0.0}, xup_n[2] = {0.0, 0.0};
+        auto load = [&](int k0, double (&c)[KB][10], V (&bb)[KB][12], double (&xup)[2]) {
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {
+                const int k = k0 + e;
+                if (k < nz) {
+                    const int o = k * nx;
+                    const VecN<double, 2> bh = ldv<2>(bp + o);
+                    const VecN<X, 2> x2 = ldv<2>(xc + o);
+                    const VecN<X, 2> n2 = ldv<2>(xN + o);
+                    const VecN<X, 2> s2 = ldv<2>(xS + o);
+                    const VecN<V, 4> h0 = ldv<4>(b4 + 4 * o), h1 = ldv<4>(b4 + 4 * o + 4);
+                    const VecN<V, 4> u2 = ldv<4>(b2 + 2 * o);
+                    c[e][0] = bh.v[0]; c[e][1] = bh.v[1];
+                    c[e][2] = (double)x2.v[0]; c[e][3] = (double)x2.v[1];
+                    c[e][4] = (double)xE[o]; c[e][5] = (double)xW[o];
+                    c[e][6] = (double)n2.v[0]; c[e][7] = (double)n2.v[1];
+                    c[e][8] = (double)s2.v[0]; c[e][9] = (double)s2.v[1];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) { bb[e][a] = h0.v[a]; bb[e][6 + a] = h1.v[a]; }
+                    bb[e][4] = u2.v[0]; bb[e][5] = u2.v[1]; bb[e][10] = u2.v[2]; bb[e][11] = u2.v[3];
+                }
+            }
+            if (k0 + KB < nz) {
+                const VecN<X, 2> up = ldv<2>(xc + (k0 + KB) * nx);
+                xup[0] = (double)up.v[0];
+                xup[1] = (double)up.v[1];
+            } else {
+                xup[0] = xup[1] = 0.0;
+            }
+        };
+        load(0, cd, cb, xup_c);
+        double xprev[2] = {0.0, 0.0};
+        for (int k0 = 0; k0 < nz; k0 += KB) {
+            if (k0 + KB < nz) load(k0 + KB, nd, nb, xup_n);
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {
+                const int k = k0 + e;
+                if (k < nz) {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const double xm = e == 0 ? xprev[c] : cd[e - 1][2 + c];
+                        const double xp = e + 1 < KB ? (k + 1 < nz ? cd[e + 1][2 + c] : 0.0) : xup_c[c];
+                        const double xe = c == 0 ? cd[e][3] : cd[e][4];   // column i+1 / i+2
+                        const double xw = c == 0 ? cd[e][5] : cd[e][2];   // column i-1 / i
+                        const V* bb = cb[e] + 6 * c;
+                        double ax = cd[e][2 + c];
+                        ax += (double)bb[0] * xe;
+                        ax += (double)bb[1] * xw;
+                        ax += (double)bb[2] * cd[e][6 + c];
+                        ax += (double)bb[3] * cd[e][8 + c];
+                        ax += (double)bb[4] * xp;
+                        ax += (double)bb[5] * xm;
+                        const double res = cd[e][c] - ax;
+                        acc[1] += res * res;
+                    }
+                }
+            }
+            xprev[0] = cd[KB - 1][2];
+            xprev[1] = cd[KB - 1][3];
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {
+#pragma unroll
+                for (int a = 0; a < 10; ++a) cd[e][a] = nd[e][a];
+#pragma unroll
+                for (int a = 0; a < 12; ++a) cb[e][a] = nb[e][a];
+            }
+            xup_c[0] = xup_n[0];
+            xup_c[1] = xup_n[1];
+        }
+    }
+    write_slots<3>(g, vv.slots, acc, MODE == 2 ? 0x5u : 0x0u);
+}
+
+// ---------------------------------------------------------------------------------------------
 // a3 / a6 / precondition: per-column Thomas solve fused with the vector update that
 // produces its right-hand side.  KIND 0: f = fin;  1: p = r + beta (p - omega v), f = p;
 // 2: s = r - alpha v, f = s.  Each thread owns CPT consecutive columns (independent recurrences,
