@@ -15,7 +15,7 @@
  * Laplacian", "non-symmetric and ... not constant coefficient", vertical
  * coupling much stronger than horizontal.  DESIGN.md §"Input recipe" states
  * every reading taken here (cell-centred latitudes, one c_h/c_v per point for both directions,
- * zeros at absent neighbours, Irwin-Hall(12) for the N(0,1) right-hand side).
+ * zeros at absent neighbours, b by Box-Muller with a portable logarithm and cosine).
  *
  * Layout of every field ("IKJ", longitude fastest):  q = i + nx*(k + nz*j)
  *   i in [0,nx)  longitude, periodic;  k in [0,nz) level;  j in [0,ny) latitude.
@@ -23,7 +23,8 @@
  *
  * Bitwise contract: eggen_host and eggen_device produce IDENTICAL bits for identical params,
  * because every value is built from exact integer hashing plus correctly rounded IEEE
- * +,-,* (no fused multiply-add on either side) and one host-computed cos(lat) table.
+ * +,-,*,/,sqrt (no fused multiply-add on either side; ln and cos from fixed-length series of those)
+ * and one host-computed cos(lat) table.
  */
 #ifndef EGGEN_H
 #define EGGEN_H

@@ -114,3 +114,19 @@ def test_device_generator_band_equals_host_rows(rows):
     hb, hr = gen.host(prob)
     assert np.array_equal(bands.cpu().numpy(), hb[:, j0 * row:j1 * row])
     assert np.array_equal(b.cpu().numpy(), hr[j0 * row:j1 * row])
+
+
+def test_rhs_is_box_muller_normal():
+    """b = sqrt(-2 ln(1 - u3)) cos(2 pi u4) from streams 3 and 4 (BASELINE.json's b ~ N(0,1),
+    SURVEY.md §8(d)): the generator's portable ln / cos agree with numpy's libm to a few ulp, and
+    the sample moments are those of N(0,1)."""
+    prob = gen.Problem(64, 48, 10, seed=0)
+    _, b = gen.host(prob)
+    q = np.arange(0, prob.n, 7)
+    u3 = np.array([gen.uniform(prob.seed, 3, int(t)) for t in q])
+    u4 = np.array([gen.uniform(prob.seed, 4, int(t)) for t in q])
+    ref = np.sqrt(-2.0 * np.log(1.0 - u3)) * np.cos(2.0 * np.pi * u4)
+    assert np.max(np.abs(b[q] - ref)) <= 1e-14
+    big = gen.host(gen.Problem(192, 144, 70, seed=1))[1]
+    assert abs(big.mean()) < 5e-3 and abs(big.var() - 1.0) < 5e-3
+    assert abs(np.mean(big ** 3)) < 1e-2 and abs(np.mean(big ** 4) - 3.0) < 2e-2   # skew 0, kurtosis 3

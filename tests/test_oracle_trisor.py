@@ -99,4 +99,13 @@ def test_solve_with_trisor_preconditioner(mode):
                               sor_sweeps=3, sor_omega=1.5)
     assert i1.converged and i3.converged
     assert i3.iters <= i1.iters
-    assert np.linalg.norm(x3 - x1) <= 1e-4 * np.linalg.norm(x1)
+    # the same solution: both within 50 tol of the direct (SuperLU) solve.  The error of a solve
+    # stopped at R < tol is bounded by cond(Ahat) R, loose here (delta down to 1e-3); the T^-1 solve
+    # of this seed sits at 12 tol, the tri-SOR one at 0.5 tol
+    import scipy.sparse.linalg as spla
+    from _dense import sparse_from_bands
+    bands, _ = gen.host(prob)
+    xd = spla.spsolve(sparse_from_bands(g, bands[0], bands[1:]).tocsc(), b)
+    tol = 1e-6 if mode == "fp64" else 1e-5
+    for x in (x1, x3):
+        assert np.linalg.norm(x - xd) <= 50 * tol * np.linalg.norm(xd)
