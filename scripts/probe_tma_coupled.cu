@@ -34,12 +34,12 @@ struct Maps { CUtensorMap r, p, v, rh, b2, b4; };
 __global__ void __launch_bounds__(MA_THREADS, 1) k_probe(int nx, int nz, int nyl, int T, int strips, int NSF,
                                                          int NSS, float* __restrict__ po, float* __restrict__ zo,
                                                          float* __restrict__ vo, const __grid_constant__ Maps maps,
-                                                         float* sink, int split, int dF, int dS, int couple) {
+                                                         float* sink, int split, int dF, int dS, int couple, int lead) {
     constexpr int SF = ma_stage_floats(1), KS = MA_KS;
     extern __shared__ __align__(128) unsigned char smraw[];
     __shared__ __align__(8) uint64_t fullF[MA_MAX_STAGES], emptyF[MA_MAX_STAGES];
     __shared__ __align__(8) uint64_t fullS[MA_MAX_STAGES], emptyS[MA_MAX_STAGES];
-    __shared__ __align__(8) uint64_t sreadq[32], zreadyq[2];
+    __shared__ __align__(8) uint64_t sreadq[2][32], zreadyq[4];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t = blockIdx.x % T, strip = blockIdx.x / T;
     const int ja = (int)((int64_t)strip * nyl / strips), jb = (int)((int64_t)(strip + 1) * nyl / strips);
@@ -51,8 +51,8 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_probe(int nx, int nz, int nyl
     if (tid == 0) {
         for (int s = 0; s < NSF; ++s) { mbar_init(&fullF[s], 1); mbar_init(&emptyF[s], MA_CONS); }
         for (int s = 0; s < NSS; ++s) { mbar_init(&fullS[s], 1); mbar_init(&emptyS[s], MA_CONS); }
-        for (int q = 0; q < 32; ++q) mbar_init(&sreadq[q], MA_CONS);
-        for (int q = 0; q < 2; ++q) mbar_init(&zreadyq[q], MA_CONS);
+        for (int q = 0; q < 32; ++q) { mbar_init(&sreadq[0][q], MA_CONS); mbar_init(&sreadq[1][q], MA_CONS); }
+        for (int q = 0; q < 4; ++q) mbar_init(&zreadyq[q], MA_CONS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -99,13 +99,14 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_probe(int nx, int nz, int nyl
     for (int m = 0; m < L; ++m) {
         const int64_t rowoff = (int64_t)(ja + m) * nz * nx + i0 + col;
         if ((couple & 1) && !isF) {  // S: z(r_m) and z(r_{m+1}) complete
+            // sets of 4 rows: F is at most `lead` rows ahead, so a set's phase never runs 2 ahead
             if (m == 0) mbar_wait(&zreadyq[0], 0u);
-            if (m + 1 < L) mbar_wait(&zreadyq[(m + 1) & 1], (uint32_t)(((m + 1) >> 1) & 1));
+            if (m + 1 < L) mbar_wait(&zreadyq[(m + 1) & 3], (uint32_t)(((m + 1) >> 2) & 1));
         }
         for (int k0 = 0; k0 < NZ8; k0 += KS) {
             const int q = k0 / KS;
             if (isF) {
-                if ((couple & 2) && m >= 2) mbar_wait(&sreadq[q], (uint32_t)((m - 2) & 1));
+                if ((couple & 2) && m >= lead) mbar_wait(&sreadq[(m - lead) & 1][q], (uint32_t)(((m - lead) >> 1) & 1));
                 mbar_wait(&fullF[slot], ph);
                 const float* sb = stF + (size_t)slot * SF;
                 float a[KS], b[KS];
@@ -137,14 +138,14 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_probe(int nx, int nz, int nyl
                 fence_proxy_async_smem();
                 mbar_arrive(&emptyS[slot]);
                 if (++slot == NSS) { slot = 0; ph ^= 1u; }
-                if (couple & 2) mbar_arrive(&sreadq[q]);
+                if (couple & 2) mbar_arrive(&sreadq[m & 1][q]);
                 spin(dS);
 #pragma unroll
                 for (int l = 0; l < KS; ++l)
                     if (k0 + l < nz) __stcg(vo + rowoff + (int64_t)(k0 + l) * nx, a[l]);
             }
         }
-        if ((couple & 1) && isF) mbar_arrive(&zreadyq[m & 1]);  // F: row m done
+        if ((couple & 1) && isF) mbar_arrive(&zreadyq[m & 3]);  // F: row m done
     }
     if (acc != 0.f) sink[0] = acc;
 }
@@ -170,7 +171,8 @@ int main(int argc, char** argv) {
     const int NSS = argc > 3 ? atoi(argv[3]) : 5;
     const int ring_kb = argc > 4 ? atoi(argv[4]) : 0;  // extra smem to mimic the z ring
     const int split = 1;                               // one producer warp per ring (as the phase kernels)
-    const int dF = argc > 5 ? atoi(argv[5]) : 0, dS = argc > 6 ? atoi(argv[6]) : 0, couple = argc > 7 ? atoi(argv[7]) : 1;
+    const int dF = argc > 5 ? atoi(argv[5]) : 0, dS = argc > 6 ? atoi(argv[6]) : 0, couple = argc > 7 ? atoi(argv[7]) : 3;
+    const int lead = argc > 8 ? atoi(argv[8]) : 2;  // rows the F consumers run ahead of the S consumers
     const int64_t n = (int64_t)nx * ny * nz;
     const int T = nx / 128;
     float *r, *p, *v, *rh, *b2, *b4, *po, *zo, *vo, *sink;
@@ -195,17 +197,17 @@ int main(int argc, char** argv) {
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     for (int it = 0; it < 2; ++it)
-        k_probe<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, sink, split, dF, dS, couple);
+        k_probe<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, sink, split, dF, dS, couple, lead);
     cudaEventRecord(a);
     const int reps = 10;
     for (int it = 0; it < reps; ++it)
-        k_probe<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, sink, split, dF, dS, couple);
+        k_probe<<<grid, MA_THREADS, smem>>>(nx, nz, ny, T, strips, NSF, NSS, po, zo, vo, maps, sink, split, dF, dS, couple, lead);
     cudaEventRecord(b);
     cudaError_t e = cudaEventSynchronize(b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
     ms /= reps;
-    printf("couple=%d dF=%d dS=%d strips=%d stagesF=%d stagesS=%d smem=%zu KB: %.3f ms  %.0f GB/s (52 B/pt)  %s\n", couple,
-           dF, dS, strips, NSF, NSS, smem / 1024, ms, 52.0 * n / (ms * 1e-3) / 1e9, cudaGetErrorString(e));
+    printf("lead=%d couple=%d dF=%d dS=%d strips=%d stagesF=%d stagesS=%d smem=%zu KB: %.3f ms  %.0f GB/s (52 B/pt)  %s\n", lead,
+           couple, dF, dS, strips, NSF, NSS, smem / 1024, ms, 52.0 * n / (ms * 1e-3) / 1e9, cudaGetErrorString(e));
     return e == cudaSuccess ? 0 : 1;
 }
