@@ -197,6 +197,7 @@ struct eg_solver {
     int wth = 128;               // Thomas CTA width (columns)
     int cpt = 1;                 // columns per thread of the Thomas / update kernels (2 if nx even)
     bool update_kb2 = false;     // k_update with 2-level batches (more CTAs per SM; few-wave grids)
+    bool pdl = false;            // programmatic dependent launches in the iteration (EG_PDL=1)
     size_t smem_th = 0;
     bool use_tm = false;         // fp32 Thomas with TMEM-resident factors (nz <= 128)
     bool use_tm64 = false;       // fp64 Thomas with TMEM-resident factors (nz <= 80)
@@ -335,18 +336,33 @@ Vecs<MODE> vecs(eg_solver* s, void* x_it) {
 // (cudaErrorCooperativeLaunchTooLarge) instead of letting CTAs that wait on other CTAs' ready flags
 // hang.  Used for the fused phase kernels, whose CTAs wait on their neighbours' rows.
 template <typename... Exp, typename... Act>
-cudaError_t launch_coop(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Act&&... args) {
+cudaError_t launch_ex(bool coop, bool pdl, void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Act&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
+    if (pdl) {  // programmatic dependent launch: may start before the previous kernel finished; the
+                // kernel waits for it (griddepcontrol.wait) before touching its results
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
+template <typename... Exp, typename... Act>
+cudaError_t launch_coop(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Act&&... args) {
+    return launch_ex(true, false, kernel, grid, block, smem, st, std::forward<Act>(args)...);
 }
 
 // -------- multi-GPU plumbing (latitude bands) --------
@@ -454,8 +470,8 @@ int finalize(eg_solver* s, int first, int tiles = 0, bool quad = false) {
     geo.quad = quad ? 1 : 0;
     const double* slots = quad ? s->hslots : s->slots;
     if (!multi(s)) {  // one GPU: group sums and logic in one CTA
-        k_fin<MODE, WHICH><<<(unsigned)(geo.g_hi - geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, slots, s->dstate, s->gsum, first);
-        CK(cudaGetLastError());
+        CK(launch_ex(false, s->pdl, k_fin<MODE, WHICH>, dim3((unsigned)(geo.g_hi - geo.g_lo)), dim3(FIN_THREADS), 0, s->st,
+                     geo, slots, s->dstate, s->gsum, first));
         return EG_OK;
     }
     constexpr int NQ = fin_nq(WHICH);
@@ -517,10 +533,9 @@ int update_and_reduce(eg_solver* s, Vecs<MODE>& v) {
     if (!multi(s)) {
         ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - xz_bytes : -1.0);
         s->next_xzero = false;
-        if (s->cpt == 2 && s->update_kb2) k_update<MODE, 2, 0, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
-        else if (s->cpt == 2) k_update<MODE, 2><<<gr, RW / 2, 0, s->st>>>(s->geo, v);
-        else k_update<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v);
-        CK(cudaGetLastError());
+        if (s->cpt == 2 && s->update_kb2) CK(launch_ex(false, s->pdl, k_update<MODE, 2, 0, 2>, gr, dim3(RW / 2), 0, s->st, s->geo, v));
+        else if (s->cpt == 2) CK(launch_ex(false, s->pdl, k_update<MODE, 2, 0, 0>, gr, dim3(RW / 2), 0, s->st, s->geo, v));
+        else CK(launch_ex(false, s->pdl, k_update<MODE, 1, 0, 0>, gr, dim3(RW), 0, s->st, s->geo, v));
         return finalize<MODE, W_C>(s, 0);
     }
     // (profiled solves keep both halves on s->st, where the CUDA events are)
@@ -575,7 +590,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
             // the first iteration after a (re)start has p = v = 0: phase A then reads r only
             ProfScope ps(s, KID_PHASE_A, s->next_fresh ? alg_bytes(s, KID_PHASE_A) - 2.0 * s->L.vsz * s->L.n : -1.0);
             s->next_fresh = false;
-            CK(launch_coop(k_march<MODE, 1>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
+            CK(launch_ex(true, s->pdl, k_march<MODE, 1>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
                            s->maps));
         }
         if (s->nranks > 1) {  // the band-edge rows' stencil, once their ghost rows are in
@@ -603,7 +618,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
         {
             ProfScope ps(s, KID_PHASE_B);
-            CK(launch_coop(k_march<MODE, 2>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
+            CK(launch_ex(true, s->pdl, k_march<MODE, 2>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
                            s->maps));
         }
         if (s->nranks > 1) {
@@ -1493,6 +1508,8 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const char* pd = getenv("EG_PDL");
+        s->pdl = pd && pd[0] == '1';
         const char* ukb = getenv("EG_UPDATE_KB2");  // A/B knob: 1 = on, 0 = off
         s->update_kb2 = ukb ? ukb[0] == '1' : (int64_t)L.tiles * L.nyl < (int64_t)4 * 8 * nsm;
     }

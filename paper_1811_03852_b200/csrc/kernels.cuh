@@ -66,6 +66,12 @@ __device__ __forceinline__ VecN<T, N> ldv(const T* p) { return *reinterpret_cast
 template <int N, class T>
 __device__ __forceinline__ void stv(T* p, const VecN<T, N>& a) { *reinterpret_cast<VecN<T, N>*>(p) = a; }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream serialization may
+// start while the previous kernel in the stream still runs; it waits here (a no-op otherwise)
+// before it reads anything that kernel writes, and lets its own dependents launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // L2 prefetch of a future level (no register cost): the register batches then see L2 latency
 __device__ __forceinline__ void pf_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -1221,6 +1227,7 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
     using VC = VecN<V, CPT>;
     using XC = VecN<X, CPT>;
     const DevState* st = vv.st;
+    pdl_wait();
     if (PART == 2 ? st->xs_run == 0 : st->halt != H_RUN) return;
     const bool sexit = (PART == 2 ? st->xs_sexit : st->sexit) != 0;
     const bool xz = (PART == 2 ? st->xs_xzero : st->xzero) != 0;  // x = 0 (not stored): first update after x0 = 0
@@ -1580,6 +1587,8 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __rest
     // grid: one CTA per reduction group; the last CTA to finish runs the logic
     constexpr int NQ = fin_nq(WHICH);
     const uint32_t r32 = fin_r32<MODE>(WHICH);
+    pdl_wait();
+    pdl_launch_dependents();  // the next kernel may launch (and wait) while this small grid runs
     if (blockIdx.x == 0 && threadIdx.x == 0) { st->epoch += 1; }  // stamps the next fused phase launch
     // halt / sexit are read once, before this CTA's arrival: only the last CTA to arrive (after every
     // CTA has read them) writes the state, so every CTA takes the same branch

@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     __shared__ uint32_t tm_slot;
     __shared__ double red[32 * 3];
     DevState* st = vv.st;
+    pdl_wait();  // (programmatic dependent launch: the finaliser before has finished)
     if (st->halt != H_RUN) return;  // uniform
     const int epoch = st->epoch;
     const bool fresh = KIND == 1 && st->fresh != 0;
