@@ -172,14 +172,15 @@ int eg_solver_set_preconditioner(eg_solver* s, int kind, int sweeps, double omeg
 /* y = Ahat x, the scaled operator the solver iterates with (unit diagonal + 6 bands; periodic in i,
  * absent neighbours contribute 0).  x, y: DEVICE arrays of the local rows in the working precision
  * (float for EG_MIXED / EG_FP32, double for EG_FP64).  Exchanges halo rows when distributed
- * (collective).  Stream-ordered; returns without synchronising. */
+ * (collective).  Stream-ordered; returns without synchronising.  x and y must not overlap (EG_ERR_ARG). */
 int eg_apply_operator(eg_solver* s, const void* x, void* y);
 
 /* z = C^-1 r, the applied preconditioner, in the working precision.  EG_PRECOND_TRIDIAG (default):
  * z = T^-1 r per column (reading A-3), T = tridiag(D_k, 1, U_k) of the scaled vertical bands,
  * Thomas recurrence without pivoting (A-14), no communication (no vertical decomposition,
  * P:263-264).  EG_PRECOND_TRISOR: the red-black tri-SOR sweeps from z = 0, which exchange halo rows
- * after every half-sweep when distributed (collective).  Stream-ordered. */
+ * after every half-sweep when distributed (collective).  Stream-ordered.  r and z must not overlap
+ * (EG_ERR_ARG). */
 int eg_precondition(eg_solver* s, const void* r, void* z);
 
 /* Solve Ahat x = D_g^-1 b by right-preconditioned BiCGStab (algorithm in DESIGN.md).

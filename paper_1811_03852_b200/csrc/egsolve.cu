@@ -1790,14 +1790,24 @@ int eg_solver_set_preconditioner(eg_solver* s, int kind, int sweeps, double omeg
     return EG_OK;
 }
 
+// the [p, p + bytes) ranges of two buffers overlap
+bool overlaps(const void* a, const void* b, size_t bytes) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + bytes && y < x + bytes;
+}
+
 int eg_apply_operator(eg_solver* s, const void* x, void* y) {
     if (!s || !x || !y) return EG_ERR_ARG;
+    if (overlaps(x, y, (size_t)s->L.n * s->L.vsz))  // the stencil reads x's neighbours while y is written
+        return fail(s, EG_ERR_ARG, "eg_apply_operator: x and y overlap");
     s->profiling = false;
     return s->mode == EG_FP64 ? apply_impl<0>(s, x, y) : s->mode == EG_MIXED ? apply_impl<1>(s, x, y) : apply_impl<2>(s, x, y);
 }
 
 int eg_precondition(eg_solver* s, const void* r, void* z) {
     if (!s || !r || !z) return EG_ERR_ARG;
+    if (overlaps(r, z, (size_t)s->L.n * s->L.vsz))
+        return fail(s, EG_ERR_ARG, "eg_precondition: r and z overlap");
     s->profiling = false;
     return s->mode == EG_FP64 ? precond_impl<0>(s, r, z) : s->mode == EG_MIXED ? precond_impl<1>(s, r, z) : precond_impl<2>(s, r, z);
 }

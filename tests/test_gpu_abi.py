@@ -86,3 +86,25 @@ def test_non_coresident_fused_grid_fails_cleanly(monkeypatch):
     s_ref = egs.Solver(g, bd, "mixed")
     xr, ir, _ = s_ref.solve(bt, tol=1e-6, maxit=20)
     assert torch.equal(x, xr)
+
+
+def test_aliasing_and_in_place_warm_start():
+    """apply / precondition refuse overlapping input and output (EG_ERR_ARG); a warm start whose x0
+    is the output buffer (in place) gives the same result as a separate x0."""
+    prob = gen.Problem(64, 16, 10, seed=9)
+    bands, b = gen.host(prob)
+    s = egs.Solver((prob.nx, prob.ny, prob.nz), torch.from_numpy(bands).cuda(), "mixed")
+    v = torch.randn(prob.n, device="cuda", dtype=torch.float32)
+    for fn in (s.apply, s.precondition):
+        with pytest.raises(egs.EgError) as e:
+            fn(v, out=v)
+        assert e.value.status == 1
+    y = s.apply(v)                      # the handle keeps working
+    assert torch.isfinite(y).all()
+    bt = torch.from_numpy(b).cuda()
+    x1, _, _ = s.solve(bt, tol=0.0, maxit=3)
+    x0 = x1.clone()
+    xa, ia, ha = s.solve(bt, x0=x0, tol=1e-7, maxit=50)
+    xin = x1.clone()
+    xb, ib, hb = s.solve(bt, x0=xin, tol=1e-7, maxit=50, out=xin)   # x0 is the output
+    assert ia.iters == ib.iters and np.array_equal(ha, hb) and torch.equal(xa, xb) and xb.data_ptr() == xin.data_ptr()
