@@ -104,6 +104,21 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, int ns) {
     while (!mbar_test(b, parity)) __nanosleep(ns);
 }
+// A/B knob (build flag MA_WAIT_MODE): 0 = the producers / publisher poll with a back-off sleep;
+// 1 = producers wait with try_wait (suspended in hardware until the phase completes); 2 = both
+#ifndef MA_WAIT_MODE
+#define MA_WAIT_MODE 0
+#endif
+#if MA_WAIT_MODE >= 1
+#define MA_PROD_WAIT(b, p) mbar_wait((b), (p))
+#else
+#define MA_PROD_WAIT(b, p) mbar_wait_sleep((b), (p), 32)
+#endif
+#if MA_WAIT_MODE >= 2
+#define MA_PUB_WAIT(b, p) mbar_wait((b), (p))
+#else
+#define MA_PUB_WAIT(b, p) mbar_wait_sleep((b), (p), 256)
+#endif
 // a consumer's generic-proxy reads of a stage must be ordered before the TMA (async proxy) that
 // refills it: without this fence the refill can land before the reads are performed (observed as a
 // rare run-to-run difference at full size; scripts/repro_t1.py)
@@ -318,7 +333,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             // elimination inputs of row jr, levels k0..k0+7: r, (p, v) or v, (U, D)
             auto fwd_stage = [&](int jr, int k0) {
                 MA_CLK(t0);
-                if (fround > 0) mbar_wait_sleep(&emptyF[fslot], (uint32_t)((fround - 1) & 1), 32);
+                if (fround > 0) MA_PROD_WAIT(&emptyF[fslot], (uint32_t)((fround - 1) & 1));
                 MA_ADD(9, t0);
                 uint64_t* fb = &fullF[fslot];
                 MA_J(1);
@@ -333,7 +348,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
             // stencil inputs of row jr: (E, W, N, S), rhat0 (phase A)
             auto sten_stage = [&](int jr, int k0) {
                 MA_CLK(t0);
-                if (sround > 0) mbar_wait_sleep(&emptyS[sslot], (uint32_t)((sround - 1) & 1), 32);
+                if (sround > 0) MA_PROD_WAIT(&emptyS[sslot], (uint32_t)((sround - 1) & 1));
                 MA_ADD(9, t0);
                 uint64_t* fb = &fullS[sslot];
                 MA_J(2);
@@ -361,7 +376,7 @@ __global__ void __launch_bounds__(MA_THREADS, 1) k_march(Geo g, Vecs<MODE> vv, M
     if (warp == 9) {
         if (lane == 0)
             for (int x = 0; x < L; ++x) {
-                mbar_wait_sleep(&zdone[x & 1], (uint32_t)((x >> 1) & 1), 256);
+                MA_PUB_WAIT(&zdone[x & 1], (uint32_t)((x >> 1) & 1));
                 MA_J(3);
                 st_release(flags + (int64_t)row_of(x) * T + t, epoch);  // gpu-scope release: z(r_x)
                 mbar_arrive(&pubd[x & 1]);
