@@ -604,3 +604,47 @@ def test_trisor_split_bands_from_set_operator_bitwise(mode):
     x3, i3, h3 = s2.solve(bt, tol=1e-8, maxit=40, flags=egs.EG_SOLVE_NO_GRAPH)
     assert i1.iters == i2.iters == i3.iters and np.array_equal(h1, h2) and np.array_equal(h1, h3)
     assert torch.equal(x1, x2) and torch.equal(x1, x3)
+
+
+# seeded random shapes (ragged tiles, odd / tiny rows and levels, both schedules): apply, precondition
+# and a short solve against the oracle; FP64 / MIXED / FP32 in turn
+_RNG = np.random.default_rng(2026)
+RANDOM_SHAPES = [gen.Problem(int(_RNG.integers(3, 300)), int(_RNG.integers(1, 40)), int(_RNG.integers(1, 90)),
+                             seed=100 + k) for k in range(12)]
+
+
+@pytest.mark.parametrize("k", range(len(RANDOM_SHAPES)))
+def test_random_shapes_parity(k, monkeypatch):
+    prob = RANDOM_SHAPES[k]
+    mode = MODES[k % 3]
+    env = {"EG_FUSE": "1"} if k % 2 == 0 else {"EG_NO_FUSE": "1"}
+    s, bands, b = _make(prob, mode, env, monkeypatch)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, diag = oracle.scale(g, bands, mode)
+    x = np.random.default_rng(k).standard_normal(prob.n).astype(_vnp(mode))
+    y = s.apply(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    assert _rel(y, oracle.apply(g, ahat, x.astype(np.float64))) <= (1e-13 if mode == "fp64" else 1e-6)
+    z = s.precondition(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    assert _rel(z, oracle.thomas(g, "fp64", ahat, x.astype(np.float64))) <= (1e-12 if mode == "fp64" else 1e-5)
+    tol = 1e-4
+    xo, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=tol, maxit=200)
+    xg, info, h = s.solve(torch.from_numpy(b).cuda(), tol=tol, maxit=200)
+    assert io.converged and info.converged and abs(info.iters - io.iters) <= 2 and info.true_R < tol
+    assert _rel(xg.cpu().numpy(), xo) <= 10 * tol
+
+
+@pytest.mark.parametrize("mode", ["mixed", "fp32"])
+def test_programmatic_dependent_launch_bitwise(mode, monkeypatch):
+    """EG_PDL=1 (programmatic dependent launches in the fused iteration) changes no result."""
+    prob = gen.Problem(256, 40, 30, seed=33)
+    bands, b = gen.host(prob)
+    g = (prob.nx, prob.ny, prob.nz)
+    bd, bt = torch.from_numpy(bands).cuda(), torch.from_numpy(b).cuda()
+    monkeypatch.setenv("EG_FUSE", "1")
+    s1 = egs.Solver(g, bd, mode)
+    monkeypatch.setenv("EG_PDL", "1")
+    s2 = egs.Solver(g, bd, mode)
+    for kw in (dict(tol=0.0, maxit=8), dict(tol=1e-6, maxit=100, restart_every=4)):
+        x1, i1, h1 = s1.solve(bt, **kw)
+        x2, i2, h2 = s2.solve(bt, **kw)
+        assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
