@@ -235,6 +235,38 @@ int eg_nccl_unique_id(char out[128]);
  * not be reused after that.  Errors: EG_ERR_ARG (out NULL, nranks < 1). */
 int eg_loopback_id(int nranks, char out[128]);
 
+/* ---- the transport of a latitude-band decomposition ----
+ * EG_TRANSPORT_P2P (the default for nranks > 1): the kernels that produce the band-edge rows of
+ * z / z_s and the reduction groups' sums store them straight into the neighbours' ghost rows and
+ * every rank's gather buffer through peer memory (CUDA IPC handles of the workspaces, exchanged at
+ * create over NCCL; NVLink / NVSwitch peer access), then stamp flags the consuming kernels wait
+ * on: no NCCL call and no copy inside an iteration, which is then one CUDA graph of kernels only.
+ * It needs every rank's workspace to be IPC-exportable (cudaMalloc memory, as PyTorch's default
+ * allocator gives) and peer access between all ranks; otherwise — or with the environment variable
+ * EG_P2P=0 — the handle keeps EG_TRANSPORT_NCCL (send / recv of ghost rows on a side stream,
+ * ncclAllGather of the group sums).  All ranks agree on the choice (collective at create).  A wait
+ * that a peer never satisfies ends the solve with EG_ERR_NCCL after EG_P2P_TIMEOUT_MS (default
+ * 60000) instead of hanging.  The loopback test transport uses the same P2P kernels on one GPU
+ * (EG_TRANSPORT_LOOPBACK_P2P, built at the first solve) or host-barrier copies (EG_P2P=0,
+ * EG_TRANSPORT_LOOPBACK).  Results are bitwise identical under every transport.  The restart /
+ * verification ghost rows of x, eg_apply_operator and the tri-SOR sweeps keep the NCCL exchange. */
+#define EG_TRANSPORT_NONE 0          /* one GPU, no exchange                               */
+#define EG_TRANSPORT_NCCL 1
+#define EG_TRANSPORT_P2P 2
+#define EG_TRANSPORT_LOOPBACK 3
+#define EG_TRANSPORT_LOOPBACK_P2P 4
+int eg_solver_transport(const eg_solver* s);
+
+/* Test hooks for the P2P transport's CUDA IPC step (the one part of it a single-GPU box can check
+ * across processes).  eg_debug_ipc_export: the 80-byte record (IPC handle of the allocation that
+ * contains ptr, ptr's offset in it) that the NCCL ranks all-gather at create; EG_ERR_CUDA if the
+ * memory cannot be exported (e.g. cuMemCreate-backed).  eg_debug_ipc_open, in another process:
+ * *ptr = the same bytes as mapped here (peer access enabled lazily), *opened = the mapping to pass
+ * to eg_debug_ipc_close.  Errors: EG_ERR_ARG, EG_ERR_CUDA. */
+int eg_debug_ipc_export(const void* ptr, unsigned char out[80]);
+int eg_debug_ipc_open(const unsigned char in[80], void** ptr, void** opened);
+int eg_debug_ipc_close(void* opened);
+
 /* ---- kernel-level profiling (EG_SOLVE_PROFILE): CUDA events on the solver's stream ---- */
 int eg_num_kernels(void);
 const char* eg_kernel_name(int kernel_id);

@@ -30,7 +30,8 @@ ABI_SYMBOLS = ("eg_workspace_bytes", "eg_workspace_bytes_ex", "eg_solver_create"
                "eg_solver_set_preconditioner", "eg_apply_operator", "eg_precondition",
                "eg_solve", "eg_solve_batch", "eg_solver_destroy", "eg_last_error", "eg_status_str",
                "eg_nccl_unique_id", "eg_loopback_id", "eg_num_kernels", "eg_kernel_name", "eg_profile_get",
-               "eg_profile_reset")
+               "eg_profile_reset", "eg_solver_transport", "eg_debug_ipc_export", "eg_debug_ipc_open",
+               "eg_debug_ipc_close")
 
 
 class EgError(RuntimeError):
@@ -114,6 +115,11 @@ def lib():
         L.eg_profile_get.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]
         L.eg_profile_reset.argtypes = [vp]
+        L.eg_solver_transport.argtypes = [vp]
+        L.eg_solver_transport.restype = i32
+        L.eg_debug_ipc_export.argtypes = [vp, ctypes.c_char_p]
+        L.eg_debug_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp), ctypes.POINTER(vp)]
+        L.eg_debug_ipc_close.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -330,3 +336,11 @@ class Solver:
 
     def profile_reset(self):
         lib().eg_profile_reset(self._h)
+
+    TRANSPORTS = {0: "none", 1: "nccl", 2: "p2p", 3: "loopback", 4: "loopback-p2p"}
+
+    @property
+    def transport(self) -> str:
+        """How the latitude bands exchange ghost rows and group sums (include/egsolve.h
+        eg_solver_transport): "none" (one GPU), "nccl", "p2p", "loopback", "loopback-p2p"."""
+        return self.TRANSPORTS[lib().eg_solver_transport(self._h)]

@@ -32,23 +32,26 @@ namespace {
 
 enum KernelId {
     KID_SCALE = 0, KID_START, KID_FIN, KID_THOMAS_P, KID_STENCIL_A, KID_THOMAS_S, KID_STENCIL_B,
-    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_SOR, KID_VERIFY, KID_UPDATE_X, KID_COUNT
+    KID_UPDATE, KID_APPLY, KID_PRECOND, KID_CONVERT, KID_PHASE_A, KID_PHASE_B, KID_SOR, KID_VERIFY, KID_UPDATE_X, KID_EDGE,
+    KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"scale", "start", "finalize", "thomas_p", "stencil_dot_A",
                                        "thomas_s", "stencil_dot_B", "update_xr", "apply",
                                        "precondition", "convert", "phase_A", "phase_B", "trisor_half",
-                                       "verify", "update_x"};
+                                       "verify", "update_x", "edge_rows"};
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
     size_t off_bands, off_diag, off_bhat, off_x64, off_x32, off_xg, off_vec, off_z, off_pv, off_slots, off_hslots,
-        off_gsum, off_state, base_total, off_split, off_batch, total;
+        off_gsum, off_edge, off_p2p, off_state, base_total, off_split, off_batch, total;
     size_t vsz;      // sizeof(V)
     size_t xsz;      // sizeof(X)
     int64_t n, row, nyl;
     int tiles, G;
 };
+
+constexpr size_t kP2PGall = 2 * 48 * sizeof(unsigned long long);  // gather words [2][8][3][2]
 
 int vsize(int mode) { return mode == EG_FP64 ? 8 : 4; }
 int xsize(int mode) { return mode == EG_FP32 ? 4 : 8; }
@@ -79,6 +82,11 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t fe
     // FP64 phase kernels: 4 warp sums per (row, 128-column slot) (march64.cuh)
     L->off_hslots = o; o = align_up(o + (mode == EG_FP64 ? 3 * 4 * (size_t)nyl * L->tiles * 8 : 0), A);
     L->off_gsum = o;  o = align_up(o + 2 * 8 * 3 * 8, A);
+    // P2P transport (latitude bands): gather buffers [2][8][3][2] epoch-stamped words and the
+    // ghost-row flags [z, z_s][side][tiles] — written by the other ranks through peer memory
+    L->off_p2p = o;   o = align_up(o + kP2PGall + 4 * (size_t)L->tiles * sizeof(int), A);
+    // latitude bands, fused schedule: k_edge_rows' scratch rows [z, z_s][row 0, row nyl-1][row]
+    L->off_edge = o;  o = align_up(o + 4 * row * L->vsz, A);
     L->off_state = o; o = align_up(o + sizeof(DevState), A);
     L->base_total = o;
     // EG_FEATURE_TRISOR: colour-split (E,W,N,S), (U,D) and f for the red-black tri-SOR sweeps
@@ -112,6 +120,7 @@ struct LoopGroup {
     cudaStream_t st = nullptr;
     std::vector<const unsigned char*> first, last;  // posted edge rows
     std::vector<const double*> gsum;                // posted group sums
+    std::vector<unsigned char*> ws;                 // the ranks' workspaces (P2P transport)
 };
 constexpr int kMaxIt = 1 << 26;  // epochs (8 per iteration at most) stay far below 2^31
 constexpr char kLoopMagic[8] = {'E', 'G', 'L', 'O', 'O', 'P', 'B', 'K'};
@@ -198,6 +207,7 @@ struct eg_solver {
     int cpt = 1;                 // columns per thread of the Thomas / update kernels (2 if nx even)
     bool update_kb2 = false;     // k_update with 2-level batches (more CTAs per SM; few-wave grids)
     bool pdl = false;            // programmatic dependent launches in the iteration (EG_PDL=1)
+    bool split_update = false;   // x half of the update beside reduction 3 (NCCL / loopback-copy bands)
     size_t smem_th = 0;
     bool use_tm = false;         // fp32 Thomas with TMEM-resident factors (nz <= 128)
     bool use_tm64 = false;       // fp64 Thomas with TMEM-resident factors (nz <= 80)
@@ -213,6 +223,13 @@ struct eg_solver {
     // NCCL, or the loopback group (tests)
     ncclComm_t comm = nullptr;
     LoopGroup* lb = nullptr;
+    // P2P transport: the producing kernels store ghost rows and group sums straight
+    // into the other ranks' workspaces (NVLink peer memory opened by CUDA IPC, or the loopback
+    // group's own buffers) and the consumers wait on epoch-stamped flags; no NCCL call, no copy in
+    // the iteration.  p2p_want: EG_P2P != 0; pp.on once the peer table is built.
+    bool p2p_want = false;
+    P2P pp{};
+    std::vector<void*> ipc_open;  // peer workspaces this handle opened (closed at destroy)
     // latitude bands: the ghost-row exchange runs on cst beside the phase kernel (ev_edge: the edge
     // rows are computed; ev_halo: the ghost rows have arrived); the x half of the update runs on xst
     // beside reduction 3 (ev_b: reduction 2 done; ev_xu: x updated)
@@ -373,15 +390,189 @@ int lb_fail(eg_solver* s) {
     return fail(s, EG_ERR_NCCL, "loopback group: a rank failed or did not arrive within 120 s");
 }
 
+// ---- P2P transport: the peer table ----
+// base[r]: rank r's workspace as this process addresses it.  Every rank's layout follows from the
+// grid, the precision and its band (valid_dist's group-aligned split), so only the bases travel.
+void p2p_table(eg_solver* s, unsigned char* const* base) {
+    P2P& pp = s->pp;
+    pp = P2P{};
+    pp.rank = s->rank;
+    pp.nranks = s->nranks;
+    pp.tiles = s->L.tiles;
+    const char* tm = getenv("EG_P2P_TIMEOUT_MS");  // tests: a short limit for the fault-injection case
+    pp.timeout_ns = (long long)(tm && atoll(tm) > 0 ? atoll(tm) : 60000) * 1000000ll;
+    const char* fl = getenv("EG_P2P_FAULT");
+    pp.fault = fl && fl[0] == '1';
+    const int G = s->L.G, per = G / s->nranks;
+    auto layout_of = [&](int r, Layout* Lr) {
+        const int64_t b0 = (int64_t)(r * per) * s->grid.ny / G, b1 = (int64_t)((r + 1) * per) * s->grid.ny / G;
+        make_layout(&s->grid, b1 - b0, s->mode, Lr);
+    };
+    auto zext_of = [&](int r, const Layout& Lr, int a) {
+        return base[r] + Lr.off_z + (size_t)a * align_up((Lr.n + 2 * Lr.row) * Lr.vsz, 256);
+    };
+    for (int r = 0; r < s->nranks; ++r) {
+        Layout Lr;
+        layout_of(r, &Lr);
+        pp.gall[r] = (unsigned long long*)(base[r] + Lr.off_p2p);
+        if (r == s->rank - 1) {  // our row 0 -> its ghost row nyl
+            pp.fdst_lo = (int*)(base[r] + Lr.off_p2p + kP2PGall);
+            for (int a = 0; a < 2; ++a) pp.dst_lo[a] = zext_of(r, Lr, a) + (size_t)(Lr.row + Lr.n) * Lr.vsz;
+        }
+        if (r == s->rank + 1) {  // our row nyl-1 -> its ghost row -1
+            pp.fdst_hi = (int*)(base[r] + Lr.off_p2p + kP2PGall);
+            for (int a = 0; a < 2; ++a) pp.dst_hi[a] = zext_of(r, Lr, a);
+        }
+    }
+    pp.hflag = (const int*)(s->ws + s->L.off_p2p + kP2PGall);
+    pp.on = 1;
+}
+
+typedef CUresult (*MemGetAddressRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+// CUDA IPC of a pointer INSIDE an allocation (a PyTorch caching-allocator block): the handle names
+// the allocation's base (cuMemGetAddressRange), the offset travels beside it
+struct IpcRec {
+    cudaIpcMemHandle_t h;
+    uint64_t off;
+    int32_t ok, pad;
+};
+static_assert(sizeof(IpcRec) == 80, "IpcRec is the 80-byte record of eg_debug_ipc_export");
+IpcRec ipc_export(const void* ptr) {
+    IpcRec r{};
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUdeviceptr a0 = 0;
+    size_t sz = 0;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &fn, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn && ((MemGetAddressRangeFn)fn)(&a0, &sz, (CUdeviceptr)ptr) == CUDA_SUCCESS &&
+        cudaIpcGetMemHandle(&r.h, (void*)a0) == cudaSuccess) {
+        r.off = (uint64_t)((CUdeviceptr)ptr - a0);
+        r.ok = 1;
+    }
+    cudaGetLastError();
+    return r;
+}
+// -> the peer's pointer in this process (base opened with lazy peer access + offset), or NULL;
+// *opened: the base to pass to cudaIpcCloseMemHandle
+unsigned char* ipc_open(const IpcRec& r, void** opened) {
+    *opened = nullptr;
+    if (!r.ok) return nullptr;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, r.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    *opened = p;
+    return (unsigned char*)p + r.off;
+}
+
+// NCCL ranks (separate processes, one GPU each): export the workspace's allocation by CUDA IPC,
+// all-gather the handles, open the peers' (NVLink peer access enabled lazily).  Every rank must
+// succeed or all keep the NCCL exchange (the result is agreed by an all-reduce).  Collective.
+int p2p_setup_nccl(eg_solver* s) {
+    using Rec = IpcRec;
+    const int P = s->nranks;
+    std::vector<unsigned char*> base(P, nullptr);
+    base[s->rank] = s->ws;
+    int ok = 1;
+    if (P > 1) {
+        const Rec mine = ipc_export(s->ws);
+        std::vector<Rec> all(P);
+        Rec* d = nullptr;
+        CK(cudaMalloc(&d, sizeof(Rec) * (P + 1)));
+        int rc = EG_OK;
+        if (cudaMemcpy(d + P, &mine, sizeof(Rec), cudaMemcpyHostToDevice) != cudaSuccess) rc = EG_ERR_CUDA;
+        if (rc == EG_OK && ncclAllGather(d + P, d, sizeof(Rec), ncclChar, s->comm, s->st) != ncclSuccess) rc = EG_ERR_NCCL;
+        if (rc == EG_OK && (cudaStreamSynchronize(s->st) != cudaSuccess ||
+                            cudaMemcpy(all.data(), d, sizeof(Rec) * P, cudaMemcpyDeviceToHost) != cudaSuccess))
+            rc = EG_ERR_CUDA;
+        for (int r = 0; rc == EG_OK && r < P; ++r) {
+            if (!all[r].ok) { ok = 0; continue; }
+            if (r == s->rank || !ok) continue;
+            void* p = nullptr;
+            base[r] = ipc_open(all[r], &p);
+            if (!base[r]) { ok = 0; continue; }
+            s->ipc_open.push_back(p);
+        }
+        // agree: P2P only if every rank opened every peer
+        int* dok = (int*)(d + P);
+        if (rc == EG_OK && cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) rc = EG_ERR_CUDA;
+        if (rc == EG_OK && ncclAllReduce(dok, dok, 1, ncclInt, ncclMin, s->comm, s->st) != ncclSuccess) rc = EG_ERR_NCCL;
+        if (rc == EG_OK && (cudaStreamSynchronize(s->st) != cudaSuccess ||
+                            cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess))
+            rc = EG_ERR_CUDA;
+        cudaFree(d);
+        if (rc != EG_OK) return fail(s, rc, "P2P setup: handle exchange failed");
+    }
+    if (!ok) {  // keep the NCCL exchange
+        for (void* p : s->ipc_open) cudaIpcCloseMemHandle(p);
+        s->ipc_open.clear();
+        return EG_OK;
+    }
+    CK(cudaMemsetAsync(s->ws + s->L.off_p2p, 0, s->L.off_state - s->L.off_p2p, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    p2p_table(s, base.data());
+    // every rank has cleared its flags before any rank's first push (which comes after this barrier)
+    int* one = nullptr;
+    CK(cudaMalloc(&one, sizeof(int)));
+    ncclResult_t nr = ncclAllReduce(one, one, 1, ncclInt, ncclSum, s->comm, s->st);
+    cudaError_t ce = cudaStreamSynchronize(s->st);
+    cudaFree(one);
+    if (nr != ncclSuccess || ce != cudaSuccess) return fail(s, EG_ERR_NCCL, "P2P setup: barrier failed");
+    return EG_OK;
+}
+
+// loopback ranks (one process): the table is built at the first solve, when every rank exists
+int p2p_setup_loop(eg_solver* s) {
+    LoopGroup* G = s->lb;
+    G->ws[s->rank] = s->ws;
+    CK(cudaMemsetAsync(s->ws + s->L.off_p2p, 0, s->L.off_state - s->L.off_p2p, s->st));
+    if (!lb_barrier(G)) return lb_fail(s);  // every rank's clear is enqueued before any push
+    p2p_table(s, G->ws.data());
+    return EG_OK;
+}
+
+// the flag reset at an epoch wrap-around (solve_impl), with every rank's pushes of earlier solves
+// done before it and none of the next solve's before it: a collective
+int p2p_reset_flags(eg_solver* s) {
+    if (s->lb) {
+        if (!lb_barrier(s->lb)) return lb_fail(s);
+    } else {
+        CK(cudaStreamSynchronize(s->st));
+        int* one = nullptr;
+        CK(cudaMalloc(&one, sizeof(int)));
+        ncclResult_t nr = ncclAllReduce(one, one, 1, ncclInt, ncclSum, s->comm, s->st);
+        cudaError_t ce = cudaStreamSynchronize(s->st);
+        cudaFree(one);
+        if (nr != ncclSuccess || ce != cudaSuccess) return fail(s, EG_ERR_NCCL, "P2P flag reset: barrier failed");
+    }
+    CK(cudaMemsetAsync(s->ws + s->L.off_p2p, 0, s->L.off_state - s->L.off_p2p, s->st));
+    if (s->lb) {
+        if (!lb_barrier(s->lb)) return lb_fail(s);
+    } else {
+        CK(cudaStreamSynchronize(s->st));
+        int* one = nullptr;
+        CK(cudaMalloc(&one, sizeof(int)));
+        ncclResult_t nr = ncclAllReduce(one, one, 1, ncclInt, ncclSum, s->comm, s->st);
+        cudaError_t ce = cudaStreamSynchronize(s->st);
+        cudaFree(one);
+        if (nr != ncclSuccess || ce != cudaSuccess) return fail(s, EG_ERR_NCCL, "P2P flag reset: barrier failed");
+    }
+    return EG_OK;
+}
+
 // async: the exchange runs on the communication stream s->cst, ordered after everything enqueued on
-// s->st so far (ev_edge); the caller joins it (halo_join) before the first kernel that reads a
+// s->st so far (ev_edge); the caller joins it (edge_join) before the first kernel that reads a
 // ghost row.  Otherwise it runs on s->st.
-int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz, bool async = false) {
+// row0 / last_row: the band's row 0 and row nyl-1 as sent (last_row = NULL: row nyl-1 of row0's array)
+int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz, bool async = false,
+         void* last_row = nullptr) {
     if (s->nranks == 1) return EG_OK;
     const size_t rowb = (size_t)s->L.row * esz;
     ncclDataType_t ty = esz == 8 ? ncclDouble : ncclFloat;
     unsigned char* first = (unsigned char*)row0;
-    unsigned char* last = first + (size_t)(s->L.nyl - 1) * rowb;
+    unsigned char* last = last_row ? (unsigned char*)last_row : first + (size_t)(s->L.nyl - 1) * rowb;
     cudaStream_t xs = async ? s->cst : s->st;
     if (s->lb) {
         LoopGroup* G = s->lb;
@@ -424,10 +615,6 @@ int halo_ghosted(eg_solver* s, void* zrow0, bool async = false) {
     return halo(s, r0, r0 - rowb, r0 + (size_t)s->L.nyl * rowb, esz, async);
 }
 
-int halo_join(eg_solver* s) {
-    if (s->nranks > 1) CK(cudaStreamWaitEvent(s->st, s->ev_halo, 0));
-    return EG_OK;
-}
 
 // the rows of a band whose stencil needs a neighbouring rank's ghost row (edge) or none (interior)
 int edge_rows(const eg_solver* s, RowMap* rm) {
@@ -442,6 +629,19 @@ int interior_rows(const eg_solver* s, RowMap* rm) {
     const int lo = s->rank > 0, hi = s->rank < s->nranks - 1;
     *rm = RowMap{lo, 1};
     return std::max(0, (int)s->L.nyl - lo - hi);
+}
+
+// P2P transport: the neighbours' pushes of this epoch into the ghost rows of z (a = 0) / z_s (a = 1)
+// have landed (k_p2p_wait), so that the edge-row stencil can read them.  Loopback: meet the other
+// ranks first, so that their pushes are enqueued on the shared stream ahead of this wait.
+int p2p_push_join(eg_solver* s) {
+    if (s->lb && !lb_barrier(s->lb)) return lb_fail(s);
+    return EG_OK;
+}
+int p2p_wait_halo(eg_solver* s, int a) {
+    k_p2p_wait<<<1, 256, 0, s->st>>>(s->dstate, s->pp, a, s->rank > 0, s->rank < s->nranks - 1);
+    CK(cudaGetLastError());
+    return EG_OK;
 }
 
 // stencil of the band-edge rows after their ghost rows arrived (the phase kernel / the interior
@@ -469,16 +669,20 @@ int finalize(eg_solver* s, int first, int tiles = 0, bool quad = false) {
     if (tiles > 0) geo.tiles = tiles;  // slots per row of the producing kernel
     geo.quad = quad ? 1 : 0;
     const double* slots = quad ? s->hslots : s->slots;
-    if (!multi(s)) {  // one GPU: group sums and logic in one CTA
+    if (!multi(s) || (s->pp.on && !s->lb)) {  // one launch: group sums (+ P2P all-gather) and logic
         CK(launch_ex(false, s->pdl, k_fin<MODE, WHICH>, dim3((unsigned)(geo.g_hi - geo.g_lo)), dim3(FIN_THREADS), 0, s->st,
-                     geo, slots, s->dstate, s->gsum, first));
+                     geo, slots, s->dstate, s->gsum, first, s->pp));
         return EG_OK;
     }
     constexpr int NQ = fin_nq(WHICH);
-    k_fin_groups<MODE, WHICH><<<(unsigned)(s->geo.g_hi - s->geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, slots, s->dstate, s->gsum);
+    k_fin_groups<MODE, WHICH><<<(unsigned)(s->geo.g_hi - s->geo.g_lo), FIN_THREADS, 0, s->st>>>(geo, slots, s->dstate, s->gsum,
+                                                                                                  s->pp);
     CK(cudaGetLastError());
     const int gl = s->geo.g_hi - s->geo.g_lo;
-    if (s->lb) {  // all-gather: rank r's block lands at gall + r * gl * NQ, as ncclAllGather places it
+    if (s->pp.on) {  // the group kernels pushed the sums; the logic kernel waits for all of them
+        // (loopback: every rank's pushes are enqueued on the shared stream before any wait)
+        if (s->lb && !lb_barrier(s->lb)) return lb_fail(s);
+    } else if (s->lb) {  // all-gather: rank r's block lands at gall + r * gl * NQ, as ncclAllGather places it
         LoopGroup* G = s->lb;
         G->gsum[s->rank] = s->gsum;
         if (!lb_barrier(G)) return lb_fail(s);
@@ -489,7 +693,7 @@ int finalize(eg_solver* s, int first, int tiles = 0, bool quad = false) {
     } else {
         NK(ncclAllGather(s->gsum, s->gall, (size_t)gl * NQ, ncclDouble, s->comm, s->st));
     }
-    k_fin_logic<MODE, WHICH><<<1, 32, 0, s->st>>>(geo, s->gall, s->dstate, first);
+    k_fin_logic<MODE, WHICH><<<1, 32, 0, s->st>>>(geo, s->gall, s->dstate, first, s->pp);
     CK(cudaGetLastError());
     return EG_OK;
 }
@@ -520,17 +724,76 @@ struct VfyBufs { float *p, *v, *z, *s, *zs, *t; double* slots; int64_t n; };
 VfyBufs g_vfy{};
 #endif
 
+// the ghost-row exchange of z (a = 0) / z_s (a = 1) after the Thomas kernel wrote all rows: a push
+// kernel (P2P) or the overlapped NCCL / loopback exchange (joined by halo_join)
+template <class V>
+int halo_start_t(eg_solver* s, V* z, int a) {
+    if (!s->pp.on) return halo_ghosted(s, z, true);
+    k_push_rows<V><<<dim3((unsigned)((s->grid.nx + 127) / 128), 2u), 128, 0, s->st>>>(s->geo, z, s->dstate, s->pp, a);
+    CK(cudaGetLastError());
+    return p2p_push_join(s);
+}
+int halo_start(eg_solver* s, float* z, int a) { return halo_start_t<float>(s, z, a); }
+int halo_start(eg_solver* s, double* z, int a) { return halo_start_t<double>(s, z, a); }
+
+// Fused schedule, latitude bands: z (KIND 1) / z_s (KIND 2) of the band's edge rows, k_edge_rows
+// into the scratch rows, then either its own pushes into the neighbours' ghost rows (P2P) or the
+// NCCL / loopback exchange of the scratch rows on s->cst (ev_halo marks the end), beside the phase
+// kernel that s->st launches next.  z_s: k_edge_rows itself runs on s->cst too, beside phase B
+// (which writes s, z_s, t and reads r, v: nothing k_edge_rows reads).  z: on s->st ahead of phase A,
+// which updates p in place and rewrites v, the inputs of k_edge_rows' p update.  Profiled solves
+// keep everything on s->st, where the CUDA events are (and so does the loopback copy transport).
+template <int MODE, int KIND>
+int edge_exchange(eg_solver* s, Vecs<MODE>& v, typename Prec<MODE>::V* z) {
+    using V = typename Prec<MODE>::V;
+    const dim3 gedge((unsigned)s->L.tiles, 2u);
+    V* scratch = (V*)(s->ws + s->L.off_edge) + (size_t)(KIND - 1) * 2 * s->L.row;
+    // (loopback copies: the copies read the neighbours' scratch rows, ordered after their
+    // k_edge_rows only if those ran on the one shared stream)
+    cudaStream_t xs = (s->profiling || KIND == 1 || (s->lb && !s->pp.on)) ? s->st : s->cst;
+    if (xs != s->st) {
+        CK(cudaEventRecord(s->ev_edge, s->st));  // after the finaliser that set beta / omega / alpha
+        CK(cudaStreamWaitEvent(xs, s->ev_edge, 0));
+    }
+    {
+        ProfScope ps(s, KID_EDGE, 0.0);
+        k_edge_rows<MODE, KIND><<<gedge, 128, s->smem_tm, xs>>>(s->geo, v, (float*)scratch, s->pp);
+        CK(cudaGetLastError());
+    }
+    int rc;
+    if (s->pp.on) {
+        if (!s->profiling) CK(cudaEventRecord(s->ev_halo, xs));
+        return p2p_push_join(s);
+    }
+    // (from s->st: halo() orders the exchange on s->cst after k_edge_rows itself)
+    const size_t rowb = (size_t)s->L.row * sizeof(V);
+    unsigned char* zr = (unsigned char*)z;
+    if ((rc = halo(s, scratch, zr - rowb, zr + (size_t)s->L.nyl * rowb, sizeof(V), !s->profiling, scratch + s->L.row)))
+        return rc;
+    return EG_OK;
+}
+// before the band-edge rows' stencil: the P2P wait for the neighbours' pushes of z (a = 0) / z_s
+// (a = 1), and the join of the communication stream (cst_used: the exchange or k_edge_rows ran there)
+int edge_join(eg_solver* s, int a, bool cst_used) {
+    int rc;
+    if (s->pp.on && (rc = p2p_wait_halo(s, a))) return rc;
+    if (cst_used && !s->profiling && s->nranks > 1) CK(cudaStreamWaitEvent(s->st, s->ev_halo, 0));
+    return EG_OK;
+}
+
 // -------- the iteration (rows a3-a10) --------
-// a9 + a10: the update and reduction 3.  One GPU: one k_update.  Latitude bands (and the 1-rank
-// NCCL path): the x half runs on s->xst beside the r half and reduction 3 (its all-gather), joined
-// at the end of the iteration — before anything reads x or overwrites z / z_s.
+// a9 + a10: the update and reduction 3.  One GPU and the P2P transport: one k_update.  Latitude
+// bands over NCCL / loopback copies (split_update): the x half runs on s->xst beside the r half and
+// reduction 3 (its all-gather), joined at the end of the iteration — before anything reads x or
+// overwrites z / z_s.  (The P2P all-gather costs a few microseconds: hiding it does not pay for
+// the second kernel's tail and the stream fork / join, profiles/r02_transport_cost.txt.)
 template <int MODE>
 int update_and_reduce(eg_solver* s, Vecs<MODE>& v) {
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     const double bx = 2.0 * s->L.xsz + 2.0 * s->L.vsz;     // x, z, z_s in; x out
     const double xz_bytes = s->next_xzero ? (double)s->L.xsz * s->L.n : 0.0;
     int rc;
-    if (!multi(s)) {
+    if (!s->split_update) {
         ProfScope ps(s, KID_UPDATE, s->next_xzero ? alg_bytes(s, KID_UPDATE) - xz_bytes : -1.0);
         s->next_xzero = false;
         if (s->cpt == 2 && s->update_kb2) CK(launch_ex(false, s->pdl, k_update<MODE, 2, 0, 2>, gr, dim3(RW / 2), 0, s->st, s->geo, v));
@@ -570,13 +833,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
     int rc;
     if constexpr (MODE != 0) {
         const unsigned grid = (unsigned)(s->mg.strips * s->L.tiles);
-        const dim3 gedge((unsigned)s->L.tiles, 2u);
-        if (multi(s)) {  // latitude bands: z of the band's edge rows -> the neighbours' ghost rows,
-            // exchanged on the communication stream while the phase kernel runs
-            k_edge_rows<MODE, 1><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.z);
-            CK(cudaGetLastError());
-            if ((rc = halo_ghosted(s, v.z, true))) return rc;
-        }
+        if (s->nranks > 1 && (rc = edge_exchange<MODE, 1>(s, v, v.z))) return rc;
 #ifdef MA_VERIFY
         const int64_t n = s->L.n;
         if (g_vfy.n != n) return fail(s, EG_ERR_CUDA, "MA_VERIFY buffers not allocated for this size");
@@ -594,7 +851,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
                            s->maps));
         }
         if (s->nranks > 1) {  // the band-edge rows' stencil, once their ghost rows are in
-            if ((rc = halo_join(s))) return rc;
+            if ((rc = edge_join(s, 0, true))) return rc;
             if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true))) return rc;
         }
 #ifdef MA_VERIFY
@@ -611,18 +868,14 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
 #endif
         if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
-        if (multi(s)) {
-            k_edge_rows<MODE, 2><<<gedge, 128, s->smem_tm, s->st>>>(s->geo, v, v.zs);
-            CK(cudaGetLastError());
-            if ((rc = halo_ghosted(s, v.zs, true))) return rc;
-        }
+        if (s->nranks > 1 && (rc = edge_exchange<MODE, 2>(s, v, v.zs))) return rc;
         {
             ProfScope ps(s, KID_PHASE_B);
             CK(launch_ex(true, s->pdl, k_march<MODE, 2>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
                            s->maps));
         }
         if (s->nranks > 1) {
-            if ((rc = halo_join(s))) return rc;
+            if ((rc = edge_join(s, 1, true))) return rc;
             if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true))) return rc;
         }
 #ifdef MA_VERIFY
@@ -800,9 +1053,9 @@ int iteration(eg_solver* s, void* x_it) {
     {
         ProfScope ps(s, KID_STENCIL_A);
         if (s->nranks > 1) {  // interior rows while the ghost rows travel, then the band-edge rows
-            if ((rc = halo_ghosted(s, v.z, true))) return rc;
+            if ((rc = halo_start(s, v.z, 0))) return rc;
             if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, false))) return rc;
-            if ((rc = halo_join(s))) return rc;
+            if ((rc = edge_join(s, 0, !s->pp.on))) return rc;
             if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true))) return rc;
         } else {
             k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh, ALL_ROWS);
@@ -828,9 +1081,9 @@ int iteration(eg_solver* s, void* x_it) {
     {
         ProfScope ps(s, KID_STENCIL_B);
         if (s->nranks > 1) {
-            if ((rc = halo_ghosted(s, v.zs, true))) return rc;
+            if ((rc = halo_start(s, v.zs, 1))) return rc;
             if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, false))) return rc;
-            if ((rc = halo_join(s))) return rc;
+            if ((rc = edge_join(s, 1, !s->pp.on))) return rc;
             if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true))) return rc;
         } else {
             k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s, ALL_ROWS);
@@ -913,6 +1166,9 @@ int read_state(eg_solver* s) {
     if (rc) return rc;
     CK(cudaStreamSynchronize(s->st));
     if (s->profiling) drain_profile(s);
+    if (s->hstate->halt == H_PEER_TIMEOUT)
+        return fail(s, EG_ERR_NCCL, "P2P transport: a neighbouring rank's push did not arrive within %lld ms",
+                    (long long)(s->pp.timeout_ns / 1000000));
     return EG_OK;
 }
 
@@ -985,8 +1241,11 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     // (at most ~5 finalisers per iteration) and wrap around with a flag reset well before overflow
     // (eg_solve sets epoch_base past the last epoch used; the reservation covers error exits)
     const int64_t reserve = 8 * ((int64_t)prm->maxit + 4);
-    if (s->epoch_base + reserve > ((int64_t)1 << 30)) {
-        CK(cudaMemsetAsync(s->ready_flags, 0, (size_t)s->L.nyl * s->L.tiles * sizeof(int), s->st));
+    if (s->lb && s->p2p_want && !s->pp.on && (rc = p2p_setup_loop(s))) return rc;
+    const char* ew = getenv("EG_EPOCH_WRAP_TEST");  // tests: force the wrap-around path now
+    if (s->epoch_base + reserve > ((int64_t)1 << 30) || (ew && ew[0] == '1')) {
+        CK(cudaMemsetAsync(s->ready_flags, 0, (size_t)s->L.nyl * ((s->grid.nx + 63) / 64) * sizeof(int), s->st));
+        if (s->pp.on && (rc = p2p_reset_flags(s))) return rc;
         s->epoch_base = 1;
     }
     h->epoch = (int)s->epoch_base;
@@ -1564,6 +1823,13 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
         if (rc == EG_OK && r == ncclSuccess) r = ncclCommInitRank(&s->comm, s->nranks, id, s->rank);
         if (r != ncclSuccess) rc = fail(s, EG_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
     }
+    {  // P2P transport for latitude bands (and the 1-rank NCCL path); EG_P2P=0 keeps NCCL / copies
+        const char* pe = getenv("EG_P2P");
+        s->p2p_want = (s->comm || s->lb) && !(pe && pe[0] == '0');
+        if (rc == EG_OK && s->p2p_want && s->comm) rc = p2p_setup_nccl(s);
+        const char* su = getenv("EG_SPLIT_UPDATE");  // A/B knob: 1 = split, 0 = one kernel
+        s->split_update = su ? (su[0] == '1' && (s->comm || s->lb)) : ((s->comm || s->lb) && !s->pp.on && !(s->lb && s->p2p_want));
+    }
     if (rc == EG_OK && (s->comm || s->lb)) {  // latitude bands: the overlap streams and events
         if (cudaStreamCreateWithFlags(&s->cst, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&s->xst, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1606,7 +1872,9 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
                 s->mg.sst_b = std::min(MA_MAX_STAGES, nb - atoi(fb));
             }
             // with NCCL ranks, leave a few SMs to the ghost-row exchange that runs beside the phase kernel
-            const int sms = (s->comm && s->nranks > 1) ? std::max(s->L.tiles, nsm - 4) : nsm;
+            // latitude bands: leave a few SMs to k_edge_rows (and NCCL's kernels), which run beside the
+            // phase kernel on the communication stream
+            const int sms = s->nranks > 1 ? std::max(s->L.tiles, nsm - 4) : nsm;
             s->mg.strips = (int)std::min<int64_t>(s->L.nyl, sms / s->L.tiles);
             s->mg.skip_lo = s->rank > 0;
             s->mg.skip_hi = s->rank < s->nranks - 1;
@@ -1898,6 +2166,7 @@ void eg_solver_destroy(eg_solver* s) {
         if (s->ev_x[i]) cudaEventDestroy(s->ev_x[i]);
         if (s->ev_out[i]) cudaEventDestroy(s->ev_out[i]);
     }
+    for (void* p : s->ipc_open) cudaIpcCloseMemHandle(p);
     if (s->comm) ncclCommDestroy(s->comm);
     if (s->lb) {  // the last member frees the group
         LoopGroup* G = s->lb;
@@ -1947,12 +2216,37 @@ int eg_loopback_id(int nranks, char out[128]) {
     G->first.assign(nranks, nullptr);
     G->last.assign(nranks, nullptr);
     G->gsum.assign(nranks, nullptr);
+    G->ws.assign(nranks, nullptr);
     memset(out, 0, 128);
     memcpy(out, kLoopMagic, sizeof kLoopMagic);
     memcpy(out + 8, &G, sizeof G);
     const int32_t n32 = nranks;
     memcpy(out + 16, &n32, sizeof n32);
     return EG_OK;
+}
+
+int eg_debug_ipc_export(const void* ptr, unsigned char out[80]) {
+    if (!ptr || !out) return EG_ERR_ARG;
+    const IpcRec r = ipc_export(ptr);
+    memcpy(out, &r, sizeof r);
+    return r.ok ? EG_OK : EG_ERR_CUDA;
+}
+int eg_debug_ipc_open(const unsigned char in[80], void** ptr, void** opened) {
+    if (!in || !ptr || !opened) return EG_ERR_ARG;
+    IpcRec r;
+    memcpy(&r, in, sizeof r);
+    *ptr = ipc_open(r, opened);
+    return *ptr ? EG_OK : EG_ERR_CUDA;
+}
+int eg_debug_ipc_close(void* opened) {
+    return cudaIpcCloseMemHandle(opened) == cudaSuccess ? EG_OK : EG_ERR_CUDA;
+}
+
+int eg_solver_transport(const eg_solver* s) {
+    if (!s) return -EG_ERR_ARG;
+    if (s->lb) return s->p2p_want ? EG_TRANSPORT_LOOPBACK_P2P : EG_TRANSPORT_LOOPBACK;
+    if (s->comm) return s->pp.on ? EG_TRANSPORT_P2P : EG_TRANSPORT_NCCL;
+    return EG_TRANSPORT_NONE;
 }
 
 int eg_num_kernels(void) { return KID_COUNT; }

@@ -901,12 +901,36 @@ __global__ void __launch_bounds__(128, 2) k_thomas_tm64(Geo g, Vecs<0> vv, const
 }
 
 // Multi-GPU fused schedule: z of the band's first and last local rows (those with a neighbouring
-// rank) ahead of the phase kernel, so that the rows can be exchanged into the neighbours' ghost
-// rows before it runs.  Same arithmetic as the phase kernel's elimination (which recomputes these
-// rows bitwise identically); p / s are not written here (phase A updates p in place).
+// rank), computed on the communication stream beside the phase kernel (which recomputes these rows
+// bitwise identically and is the one that writes them to z, and p / s), so that they reach the
+// neighbours' ghost rows while it runs.  zout: a scratch pair of rows [2][row] (row 0, row nyl-1).
 // grid (ceil(nx/128), 2): blockIdx.y 0 -> local row 0, 1 -> local row nyl-1.
+// P2P transport (pp.on): this CTA's 128 columns of the band's edge row go straight into the
+// neighbour's ghost row through peer memory (side 0: local row 0 -> rank-1's ghost row nyl; side 1:
+// row nyl-1 -> rank+1's ghost row -1), then the tile's flag in the neighbour's workspace is stamped
+// with the epoch (release, system scope).  a: 0 = z, 1 = z_s.  zrow: the local row (written by this
+// CTA's own threads, column by column, before the call).
+template <class V>
+__device__ __forceinline__ void push_edge_tile(const Geo& g, const P2P& pp, int a, int side, const V* zrow,
+                                               int epoch) {
+    V* dst = (V*)(side == 0 ? pp.dst_lo[a] : pp.dst_hi[a]);
+    int* fl = side == 0 ? pp.fdst_lo : pp.fdst_hi;
+    if (dst == nullptr || fl == nullptr) return;  // no neighbour on this side (uniform per CTA)
+    const int i = blockIdx.x * 128 + threadIdx.x;
+#ifndef EG_MUTATE_NO_HALO_PUSH  // mutation check of the P2P tests (scripts/build_variant.sh): flags only
+    if (i < g.nx)
+        for (int k = 0; k < (int)g.nz; ++k) dst[(int64_t)k * g.nx + i] = zrow[(int64_t)k * g.nx + i];
+#endif
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        // the receiver's flags [a][side'][tile]: our row 0 is its ghost row nyl (side' 1), and back
+        st_release_sys(fl + (a * 2 + (side == 0 ? 1 : 0)) * pp.tiles + blockIdx.x, epoch);
+    }
+}
+
 template <int MODE, int KIND>
-__global__ void __launch_bounds__(128, 4) k_edge_rows(Geo g, Vecs<MODE> vv, float* __restrict__ zout) {
+__global__ void __launch_bounds__(128, 4) k_edge_rows(Geo g, Vecs<MODE> vv, float* __restrict__ zout, P2P pp) {
     static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ uint32_t tm_base;
@@ -928,9 +952,41 @@ __global__ void __launch_bounds__(128, 4) k_edge_rows(Geo g, Vecs<MODE> vv, floa
     const bool act = i_raw < nx;
     const int i = act ? i_raw : nx - 1;
     const int64_t row = blockIdx.y == 0 ? 0 : g.nyl - 1;
+    float* zrow = zout + (int64_t)blockIdx.y * g.row;
+    // thomas_tm_tile stores z at zout + row * g.row + (k, i): shift the base so that it lands in zrow
+    float* zo = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(zrow) - (uintptr_t)(row * g.row * sizeof(float)));
     thomas_tm_tile<MODE, KIND, false>(g, vv, row * g.row, i, act, base + ((uint32_t)(warp * 32) << 16),
-                                      reinterpret_cast<float*>(smraw), beta, omega, alpha, fresh, nullptr, zout);
+                                      reinterpret_cast<float*>(smraw), beta, omega, alpha, fresh, nullptr, zo);
     tm_free128(base);
+    if (pp.on) {
+        __syncthreads();
+        push_edge_tile<float>(g, pp, KIND - 1, (int)blockIdx.y, zrow, *(volatile const int*)&st->epoch);
+    }
+}
+
+// P2P transport, 5-kernel schedule: push the edge rows of z (a = 0) / z_s (a = 1) that the Thomas
+// kernel just wrote.  grid (ceil(nx/128), 2), 128 threads; blockIdx.y = side as in push_edge_tile.
+template <class V>
+__global__ void __launch_bounds__(128) k_push_rows(Geo g, const V* __restrict__ z, const DevState* st, P2P pp, int a) {
+    if (st->halt != H_RUN) return;
+    const int64_t row = blockIdx.y == 0 ? 0 : g.nyl - 1;
+    push_edge_tile<V>(g, pp, a, (int)blockIdx.y, z + row * g.row, *(volatile const int*)&st->epoch);
+}
+
+// P2P transport: wait until the neighbours' pushes of this epoch have landed in the ghost rows of z
+// (a = 0) / z_s (a = 1): flags [a][side][tile], side 0 from rank-1 (wlo), 1 from rank+1 (whi).  A
+// kernel of its own, so that the edge-row stencil launched after it reads ghost rows no write can
+// still be in flight to (its loads may take the read-only path).  One CTA, any width.
+__global__ void __launch_bounds__(256) k_p2p_wait(DevState* st, P2P pp, int a, int wlo, int whi) {
+    if (st->halt != H_RUN) return;
+    const int epoch = *(volatile const int*)&st->epoch;
+    bool bad = false;
+    for (int t = threadIdx.x; t < 2 * pp.tiles; t += blockDim.x) {
+        const int side = t / pp.tiles;
+        if (side == 0 ? !wlo : !whi) continue;
+        if (!wait_flag_sys(pp.hflag + a * 2 * pp.tiles + t, epoch, pp.timeout_ns)) bad = true;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) st->halt = H_PEER_TIMEOUT;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1580,57 +1636,150 @@ __device__ __forceinline__ void x_snapshot(DevState* st) {
     st->xs_xzero = st->xzero;
 }
 
-// single-GPU finaliser: groups + logic in one CTA (1024 threads)
+// one-kernel finaliser: one CTA per (local) reduction group, the last CTA to finish runs the logic.
+// One GPU: all G groups are local.  Latitude bands with the P2P transport (pp.on, NCCL ranks):
+// every CTA also pushes its group's sums to every rank (p2p_push_group) and the last CTA waits for
+// all G groups' words of this epoch (p2p_gather) before the logic — the all-gather inside the
+// finaliser, one launch per reduction as on one GPU.
+template <int WHICH> __device__ __forceinline__ bool fin_no_sums(const DevState* st);
+template <int WHICH>
+__device__ __forceinline__ void p2p_push_group(const Geo& g, const P2P& pp, const double* gsum, int gl, int epoch);
+template <int WHICH>
+__device__ __forceinline__ bool p2p_gather(const Geo& g, const P2P& pp, int epoch, double* gs);
+
 template <int MODE, int WHICH>
 __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __restrict__ slots, DevState* st,
-                                                     double* __restrict__ gsum, int first) {
-    // grid: one CTA per reduction group; the last CTA to finish runs the logic
+                                                     double* __restrict__ gsum, int first, P2P pp) {
     constexpr int NQ = fin_nq(WHICH);
     const uint32_t r32 = fin_r32<MODE>(WHICH);
     pdl_wait();
     pdl_launch_dependents();  // the next kernel may launch (and wait) while this small grid runs
-    if (blockIdx.x == 0 && threadIdx.x == 0) { st->epoch += 1; }  // stamps the next fused phase launch
-    // halt / sexit are read once, before this CTA's arrival: only the last CTA to arrive (after every
-    // CTA has read them) writes the state, so every CTA takes the same branch
+    // halt / sexit / epoch are read once, before this CTA's arrival: only the last CTA to arrive
+    // (after every CTA has read them) writes the state, so every CTA takes the same branch and
+    // stamps its pushes with the same epoch
     const int halt0 = *(volatile const int*)&st->halt;
     const int sexit0 = *(volatile const int*)&st->sexit;
-    if (WHICH != W_START && WHICH != W_VERIFY && halt0 != H_RUN) {  // (then nobody writes)
-        if (WHICH == W_B && blockIdx.x == 0 && threadIdx.x == 0) x_snapshot(st);
+    const int epoch = *(volatile const int*)&st->epoch;
+    if (WHICH != W_START && WHICH != W_VERIFY && halt0 != H_RUN) {  // (then nobody writes but this)
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            st->epoch = epoch + 1;  // every finaliser launch bumps the epoch (stamps the next phase launch)
+            if (WHICH == W_B) x_snapshot(st);
+        }
         return;
     }
     // s-step exit (W_C): no sums needed, but every CTA still arrives so that the counter is reset
-    if (!(WHICH == W_C && sexit0)) fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
+    const bool sums = !(WHICH == W_C && sexit0);
+    if (sums) fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
     __shared__ int last;
+    __shared__ double gs[8 * 3];
     __syncthreads();
+    if (pp.on && sums) p2p_push_group<WHICH>(g, pp, gsum, blockIdx.x, epoch);
     if (threadIdx.x == 0) {
         __threadfence();  // this group's sums before the arrival
         last = atomicAdd(&st->fin_ctr, 1) == (int)gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (!last) return;
+    bool ok = true;
+    if (pp.on && sums) ok = p2p_gather<WHICH>(g, pp, epoch, gs);
+    if (threadIdx.x == 0) {
         __threadfence();
         st->fin_ctr = 0;
-        fin_logic<MODE, WHICH>(g, gsum, st, first);
+        st->epoch = epoch + 1;
+        if (!ok) {
+            st->halt = H_PEER_TIMEOUT;
+        } else {
+            fin_logic<MODE, WHICH>(g, pp.on && sums ? gs : gsum, st, first);
+        }
         if (WHICH == W_B) x_snapshot(st);
     }
 }
 
-// multi-GPU: local groups -> (NCCL all-gather) -> logic.  grid: one CTA per local group.
+// The P2P all-gather of the group sums (pp.on): every fp64 sum travels as two 64-bit words
+// (epoch << 32 | one 32-bit half) into every rank's gather buffer (its own included) at
+// [epoch & 1][global group][q][half].  No fence: an aligned 64-bit store is single-copy atomic, so
+// a word whose epoch matches holds this epoch's half.  Two buffers: a rank can run at most one
+// reduction ahead of a slower one (DESIGN.md §7 P2P).
+template <int WHICH>
+__device__ __forceinline__ bool fin_no_sums(const DevState* st) {  // k_fin_groups' early exits
+    return (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) || (WHICH == W_C && st->sexit);
+}
+constexpr int P2P_GWORDS = 8 * 3 * 2;  // words per parity buffer: [group][q][half]
+// after fin_group_par + __syncthreads: this CTA's group (local index gl) to every rank
+template <int WHICH>
+__device__ __forceinline__ void p2p_push_group(const Geo& g, const P2P& pp, const double* gsum, int gl, int epoch) {
+    constexpr int NQ = fin_nq(WHICH);
+    const int t = threadIdx.x;
+    if (t < pp.nranks * NQ * 2) {  // one word per thread: rank r, sum q, half h
+        const int r = t / (NQ * 2), q = (t >> 1) % NQ, h = t & 1;
+        const unsigned e = (unsigned)epoch + (pp.fault ? 1u : 0u);  // fault injection: a wrong stamp
+        const unsigned long long bits =
+            (unsigned long long)__double_as_longlong(((volatile const double*)gsum)[gl * NQ + q]);
+        const unsigned half = h ? (unsigned)(bits >> 32) : (unsigned)bits;
+        st_relaxed_sys_u64(pp.gall[r] + (e & 1u) * P2P_GWORDS + ((g.g_lo + gl) * 3 + q) * 2 + h,
+                           ((unsigned long long)e << 32) | half);
+    }
+}
+// all G groups' sums of this epoch from this rank's gather buffer into gs[G * NQ] (shared), the
+// words polled by the CTA's threads in parallel; false if one did not arrive within the timeout.
+// Called by every thread of the CTA.
+template <int WHICH>
+__device__ __forceinline__ bool p2p_gather(const Geo& g, const P2P& pp, int epoch, double* gs) {
+    constexpr int NQ = fin_nq(WHICH);
+    __shared__ unsigned gw[P2P_GWORDS];
+    const unsigned long long* b = pp.gall[pp.rank] + (unsigned)(epoch & 1) * P2P_GWORDS;
+    bool bad = false;
+    for (int w = threadIdx.x; w < g.G * NQ * 2; w += blockDim.x) {
+        const int gi = w / (NQ * 2), rem = w % (NQ * 2);
+        const unsigned long long* src = b + (gi * 3 + (rem >> 1)) * 2 + (rem & 1);
+        unsigned long long v = ld_relaxed_sys_u64(src);
+        if ((unsigned)(v >> 32) != (unsigned)epoch) {
+            const unsigned long long t0 = globaltimer_ns();
+            while ((unsigned)((v = ld_relaxed_sys_u64(src)) >> 32) != (unsigned)epoch) {
+                __nanosleep(100);
+                if ((long long)(globaltimer_ns() - t0) > pp.timeout_ns) { bad = true; break; }
+            }
+        }
+        gw[w] = (unsigned)v;
+    }
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0 && !bad)
+        for (int e = 0; e < g.G * NQ; ++e)
+            gs[e] = __longlong_as_double((long long)(((unsigned long long)gw[2 * e + 1] << 32) | gw[2 * e]));
+    __syncthreads();
+    return !bad;
+}
+
+// two-kernel finaliser of the NCCL / loopback transports: local groups -> (ncclAllGather, or the
+// loopback copies) -> logic; with the loopback P2P transport the group kernel pushes and the logic
+// kernel gathers, a host barrier between them ordering every rank's pushes ahead of every wait on
+// the one shared stream.  grid: one CTA per local group.
 template <int MODE, int WHICH>
 __global__ void __launch_bounds__(FIN_THREADS) k_fin_groups(Geo g, const double* __restrict__ slots,
-                                                            const DevState* st, double* __restrict__ gsum) {
+                                                            const DevState* st, double* __restrict__ gsum, P2P pp) {
     constexpr int NQ = fin_nq(WHICH);
     const uint32_t r32 = fin_r32<MODE>(WHICH);
-    if (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) return;
-    if (WHICH == W_C && st->sexit) return;
+    if (fin_no_sums<WHICH>(st)) return;
     fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
+    if (pp.on) {
+        __syncthreads();
+        p2p_push_group<WHICH>(g, pp, gsum, blockIdx.x, *(volatile const int*)&st->epoch);
+    }
 }
 
 template <int MODE, int WHICH>
-__global__ void k_fin_logic(Geo g, const double* __restrict__ gall, DevState* st, int first) {
-    if (threadIdx.x == 0) { st->epoch += 1; }
+__global__ void k_fin_logic(Geo g, const double* __restrict__ gall, DevState* st, int first, P2P pp) {
+    __shared__ double gs[8 * 3];
+    const int epoch = *(volatile const int*)&st->epoch;
+    const bool p2p = pp.on && !fin_no_sums<WHICH>(st);
+    const bool ok = p2p ? p2p_gather<WHICH>(g, pp, epoch, gs) : true;
     if (threadIdx.x == 0) {
-        fin_logic<MODE, WHICH>(g, gall, st, first);
+        st->epoch = epoch + 1;
+        if (!ok) {
+            st->halt = H_PEER_TIMEOUT;
+        } else {
+            fin_logic<MODE, WHICH>(g, p2p ? gs : gall, st, first);
+        }
         if (WHICH == W_B) x_snapshot(st);
     }
 }

@@ -295,10 +295,12 @@ def test_profile_counts_kernels():
 
 
 @pytest.mark.parametrize("mode", ["mixed", "fp64"])
-def test_multirank_finaliser_path_bitwise_equal(mode, monkeypatch):
-    """EG_FORCE_NCCL=1 runs one GPU through the multi-rank path (local row-group sums ->
-    ncclAllGather -> logic kernel, captured in the iteration graph).  The fixed grouping makes it
-    bitwise identical to the single-GPU finaliser."""
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_multirank_finaliser_path_bitwise_equal(mode, transport, monkeypatch):
+    """EG_FORCE_NCCL=1 runs one GPU through the multi-rank path (local row-group sums -> the
+    all-gather -> logic kernel, captured in the iteration graph): by the group kernels' own pushes
+    and flags (P2P transport, the default) or ncclAllGather (EG_P2P=0).  The fixed grouping makes
+    it bitwise identical to the single-GPU finaliser."""
     prob = RAGGED
     bands, b = gen.host(prob)
     g = (prob.nx, prob.ny, prob.nz)
@@ -307,9 +309,13 @@ def test_multirank_finaliser_path_bitwise_equal(mode, monkeypatch):
     x1, i1, h1 = s1.solve(torch.from_numpy(b).cuda(), tol=1e-6, maxit=100)
     monkeypatch.setenv("EG_FORCE_NCCL", "1")
     monkeypatch.setenv("EG_FUSE", "1")
+    if transport == "nccl":
+        monkeypatch.setenv("EG_P2P", "0")
     s2 = egs.Solver(g, bd, mode)
     monkeypatch.delenv("EG_FORCE_NCCL")
     monkeypatch.delenv("EG_FUSE")
+    monkeypatch.delenv("EG_P2P", raising=False)
+    assert s2.transport == transport and s1.transport == "none"
     x2, i2, h2 = s2.solve(torch.from_numpy(b).cuda(), tol=1e-6, maxit=100)
     assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
     if mode == "mixed":  # the fused phases run on the multi-rank path too (edge rows + ghost rows)
