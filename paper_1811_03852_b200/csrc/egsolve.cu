@@ -83,8 +83,8 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t fe
     L->off_hslots = o; o = align_up(o + (mode == EG_FP64 ? 3 * 4 * (size_t)nyl * L->tiles * 8 : 0), A);
     L->off_gsum = o;  o = align_up(o + 2 * 8 * 3 * 8, A);
     // P2P transport (latitude bands): gather buffers [2][8][3][2] epoch-stamped words and the
-    // ghost-row flags [z, z_s][side][tiles] — written by the other ranks through peer memory
-    L->off_p2p = o;   o = align_up(o + kP2PGall + 4 * (size_t)L->tiles * sizeof(int), A);
+    // ghost-row flags [z, z_s][side][64-column tiles] — written by the other ranks through peer memory
+    L->off_p2p = o;   o = align_up(o + kP2PGall + 4 * (size_t)((g->nx + 63) / 64) * sizeof(int), A);
     // latitude bands, fused schedule: k_edge_rows' scratch rows [z, z_s][row 0, row nyl-1][row]
     L->off_edge = o;  o = align_up(o + 4 * row * L->vsz, A);
     L->off_state = o; o = align_up(o + sizeof(DevState), A);
@@ -398,7 +398,7 @@ void p2p_table(eg_solver* s, unsigned char* const* base) {
     pp = P2P{};
     pp.rank = s->rank;
     pp.nranks = s->nranks;
-    pp.tiles = s->L.tiles;
+    pp.tiles = (int)((s->grid.nx + ER_COLS - 1) / ER_COLS);  // one flag per edge-row CTA
     const char* tm = getenv("EG_P2P_TIMEOUT_MS");  // tests: a short limit for the fault-injection case
     pp.timeout_ns = (long long)(tm && atoll(tm) > 0 ? atoll(tm) : 60000) * 1000000ll;
     const char* fl = getenv("EG_P2P_FAULT");
@@ -631,24 +631,21 @@ int interior_rows(const eg_solver* s, RowMap* rm) {
     return std::max(0, (int)s->L.nyl - lo - hi);
 }
 
-// P2P transport: the neighbours' pushes of this epoch into the ghost rows of z (a = 0) / z_s (a = 1)
-// have landed (k_p2p_wait), so that the edge-row stencil can read them.  Loopback: meet the other
-// ranks first, so that their pushes are enqueued on the shared stream ahead of this wait.
+// P2P transport, loopback ranks: after the pushes, meet the other ranks, so that every rank's
+// pushes are enqueued on the shared stream ahead of any rank's wait (no kernel then ever spins on
+// another rank's kernel on the one GPU)
 int p2p_push_join(eg_solver* s) {
     if (s->lb && !lb_barrier(s->lb)) return lb_fail(s);
     return EG_OK;
 }
-int p2p_wait_halo(eg_solver* s, int a) {
-    k_p2p_wait<<<1, 256, 0, s->st>>>(s->dstate, s->pp, a, s->rank > 0, s->rank < s->nranks - 1);
-    CK(cudaGetLastError());
-    return EG_OK;
-}
 
-// stencil of the band-edge rows after their ghost rows arrived (the phase kernel / the interior
-// stencil launch left them out), same arithmetic and reduction slots as the full launch
+// stencil of the interior rows (edge = false: the 5-kernel schedule while the ghost rows travel) or
+// of the band-edge rows after their ghost rows arrived (the phase kernel / the interior launch left
+// them out: k_stencil_rows, which with the P2P transport first waits for the neighbours' pushes of
+// array a: 0 = z, 1 = z_s), same arithmetic and reduction slots as the full launch
 template <int MODE, int DOTS>
 int stencil_rows(eg_solver* s, const typename Prec<MODE>::V* z, typename Prec<MODE>::V* y,
-                 const typename Prec<MODE>::V* aux, bool edge) {
+                 const typename Prec<MODE>::V* aux, bool edge, int a = 0) {
     RowMap rm;
     const int n = edge ? edge_rows(s, &rm) : interior_rows(s, &rm);
     if (n == 0) return EG_OK;
@@ -656,7 +653,20 @@ int stencil_rows(eg_solver* s, const typename Prec<MODE>::V* z, typename Prec<MO
     if (edge) return EG_OK;
 #endif
     Vecs<MODE> v = vecs<MODE>(s, s->x64);
-    k_stencil<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n), RW, 0, s->st>>>(s->geo, v, z, y, aux, rm);
+#ifdef EG_DEBUG_OLD_EDGE_STENCIL
+    if (false) {
+#else
+    if (edge) {
+#endif
+        HWait hw{nullptr, 0, 0, 0, 0};
+        if (s->pp.on)
+            hw = HWait{s->pp.hflag + a * 2 * s->pp.tiles, s->pp.tiles, s->rank > 0, s->rank < s->nranks - 1,
+                       s->pp.timeout_ns};
+        k_stencil_rows<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n), SR_THREADS, 0, s->st>>>(s->geo, v, z, y, aux,
+                                                                                                     rm, hw);
+    } else {
+        k_stencil<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n), RW, 0, s->st>>>(s->geo, v, z, y, aux, rm);
+    }
     CK(cudaGetLastError());
     return EG_OK;
 }
@@ -729,7 +739,7 @@ VfyBufs g_vfy{};
 template <class V>
 int halo_start_t(eg_solver* s, V* z, int a) {
     if (!s->pp.on) return halo_ghosted(s, z, true);
-    k_push_rows<V><<<dim3((unsigned)((s->grid.nx + 127) / 128), 2u), 128, 0, s->st>>>(s->geo, z, s->dstate, s->pp, a);
+    k_push_rows<V><<<dim3((unsigned)((s->grid.nx + ER_COLS - 1) / ER_COLS), 2u), 256, 0, s->st>>>(s->geo, z, s->dstate, s->pp, a);
     CK(cudaGetLastError());
     return p2p_push_join(s);
 }
@@ -746,7 +756,7 @@ int halo_start(eg_solver* s, double* z, int a) { return halo_start_t<double>(s, 
 template <int MODE, int KIND>
 int edge_exchange(eg_solver* s, Vecs<MODE>& v, typename Prec<MODE>::V* z) {
     using V = typename Prec<MODE>::V;
-    const dim3 gedge((unsigned)s->L.tiles, 2u);
+    const dim3 gedge((unsigned)((s->grid.nx + ER_COLS - 1) / ER_COLS), 2u);
     V* scratch = (V*)(s->ws + s->L.off_edge) + (size_t)(KIND - 1) * 2 * s->L.row;
     // (loopback copies: the copies read the neighbours' scratch rows, ordered after their
     // k_edge_rows only if those ran on the one shared stream)
@@ -757,7 +767,7 @@ int edge_exchange(eg_solver* s, Vecs<MODE>& v, typename Prec<MODE>::V* z) {
     }
     {
         ProfScope ps(s, KID_EDGE, 0.0);
-        k_edge_rows<MODE, KIND><<<gedge, 128, s->smem_tm, xs>>>(s->geo, v, (float*)scratch, s->pp);
+        k_edge_rows<MODE, KIND><<<gedge, ER_THREADS, er_smem_bytes(s->grid.nz), xs>>>(s->geo, v, (float*)scratch, s->pp);
         CK(cudaGetLastError());
     }
     int rc;
@@ -772,11 +782,10 @@ int edge_exchange(eg_solver* s, Vecs<MODE>& v, typename Prec<MODE>::V* z) {
         return rc;
     return EG_OK;
 }
-// before the band-edge rows' stencil: the P2P wait for the neighbours' pushes of z (a = 0) / z_s
-// (a = 1), and the join of the communication stream (cst_used: the exchange or k_edge_rows ran there)
+// before the band-edge rows' stencil: the join of the communication stream (cst_used: the
+// exchange or k_edge_rows ran there).  (The P2P wait is the stencil kernel's own.)
 int edge_join(eg_solver* s, int a, bool cst_used) {
-    int rc;
-    if (s->pp.on && (rc = p2p_wait_halo(s, a))) return rc;
+    (void)a;
     if (cst_used && !s->profiling && s->nranks > 1) CK(cudaStreamWaitEvent(s->st, s->ev_halo, 0));
     return EG_OK;
 }
@@ -852,7 +861,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
         if (s->nranks > 1) {  // the band-edge rows' stencil, once their ghost rows are in
             if ((rc = edge_join(s, 0, true))) return rc;
-            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true))) return rc;
+            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true, 0))) return rc;
         }
 #ifdef MA_VERIFY
         {
@@ -876,7 +885,7 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
         if (s->nranks > 1) {
             if ((rc = edge_join(s, 1, true))) return rc;
-            if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true))) return rc;
+            if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true, 1))) return rc;
         }
 #ifdef MA_VERIFY
         {
@@ -1056,7 +1065,7 @@ int iteration(eg_solver* s, void* x_it) {
             if ((rc = halo_start(s, v.z, 0))) return rc;
             if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, false))) return rc;
             if ((rc = edge_join(s, 0, !s->pp.on))) return rc;
-            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true))) return rc;
+            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true, 0))) return rc;
         } else {
             k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh, ALL_ROWS);
             CK(cudaGetLastError());
@@ -1084,7 +1093,7 @@ int iteration(eg_solver* s, void* x_it) {
             if ((rc = halo_start(s, v.zs, 1))) return rc;
             if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, false))) return rc;
             if ((rc = edge_join(s, 1, !s->pp.on))) return rc;
-            if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true))) return rc;
+            if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true, 1))) return rc;
         } else {
             k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s, ALL_ROWS);
             CK(cudaGetLastError());
@@ -1468,8 +1477,8 @@ int set_thomas_smem(eg_solver* s) {
             CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
             CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
             CK(cudaFuncSetAttribute(k_thomas_tm<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
-            CK(cudaFuncSetAttribute(k_edge_rows<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
-            CK(cudaFuncSetAttribute(k_edge_rows<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_tm));
+            CK(cudaFuncSetAttribute(k_edge_rows<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)er_smem_bytes(s->grid.nz)));
+            CK(cudaFuncSetAttribute(k_edge_rows<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)er_smem_bytes(s->grid.nz)));
         }
     }
     return rc;

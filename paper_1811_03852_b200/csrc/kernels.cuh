@@ -137,12 +137,16 @@ struct RowMap {
 };
 constexpr RowMap ALL_ROWS{0, 1};
 
-// product of two V values summed into an S accumulator held as double (exact product for fp32
-// operands; FP32 mode rounds product and sum to binary32 like the oracle)
+// product of two V values summed into an S accumulator held as double: the product rounded, then
+// the sum rounded (oracle_dot's s = rs(s + rs(a b))) — in binary32 for FP32 mode, binary64 otherwise
+// (exact product for fp32 operands).  Written with the _rn intrinsics, which the compiler never
+// contracts into an FMA: a contraction (legal for a plain a * b + s) would skip the product's
+// rounding in some kernels and not in others, and the kernels that compute the same partials
+// (phase kernels, the 5-kernel stencil, the band-edge stencil) must agree bitwise.
 template <int MODE, class V>
 __device__ __forceinline__ void acc_dot(double& acc, V a, V b) {
-    if (MODE == 2) acc = rs<MODE>(acc + (double)(float)((double)a * (double)b));
-    else acc += (double)a * (double)b;
+    if (MODE == 2) acc = (double)__fadd_rn((float)acc, __fmul_rn((float)a, (float)b));
+    else acc = __dadd_rn(acc, __dmul_rn((double)a, (double)b));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -281,10 +285,10 @@ __global__ void __launch_bounds__(RW) k_start(Geo g, Vecs<MODE> vv, const double
                         bh = bh / cd[e][1];
                         bh_out[o] = bh;
                         if (MODE == 2) {
-                            const double b32 = (double)(float)bh;
-                            acc[0] = rs<MODE>(acc[0] + (double)(float)(b32 * b32));
+                            const float b32 = (float)bh;
+                            acc[0] = (double)__fadd_rn((float)acc[0], __fmul_rn(b32, b32));
                         } else {
-                            acc[0] += bh * bh;
+                            acc[0] = __dadd_rn(acc[0], __dmul_rn(bh, bh));
                         }
                     }
                     double res;
@@ -900,26 +904,32 @@ __global__ void __launch_bounds__(128, 2) k_thomas_tm64(Geo g, Vecs<0> vv, const
     }
 }
 
-// Multi-GPU fused schedule: z of the band's first and last local rows (those with a neighbouring
-// rank), computed on the communication stream beside the phase kernel (which recomputes these rows
-// bitwise identically and is the one that writes them to z, and p / s), so that they reach the
-// neighbours' ghost rows while it runs.  zout: a scratch pair of rows [2][row] (row 0, row nyl-1).
-// grid (ceil(nx/128), 2): blockIdx.y 0 -> local row 0, 1 -> local row nyl-1.
-// P2P transport (pp.on): this CTA's 128 columns of the band's edge row go straight into the
+// ---- latitude bands: the band-edge rows ----
+// Only two rows per band, so these kernels are latency-bound, not bandwidth-bound: a column walk
+// over nz levels issues nz dependent rounds of loads.  They stage instead: every thread of a wide
+// CTA loads its share of the levels at once into shared memory, a few threads then run the serial
+// part from shared memory, and the results leave in parallel.  Same arithmetic as the full-band
+// kernels, operation for operation (bitwise equal results).
+constexpr int ER_COLS = 64;       // columns per CTA of the edge-row kernels (one P2P flag each)
+constexpr int ER_THREADS = 512;   // 8 level lanes x 64 columns
+inline size_t er_smem_bytes(int64_t nz) { return (size_t)3 * nz * ER_COLS * sizeof(float); }
+
+// P2P transport (pp.on): this CTA's ER_COLS columns of the band's edge row go straight into the
 // neighbour's ghost row through peer memory (side 0: local row 0 -> rank-1's ghost row nyl; side 1:
 // row nyl-1 -> rank+1's ghost row -1), then the tile's flag in the neighbour's workspace is stamped
-// with the epoch (release, system scope).  a: 0 = z, 1 = z_s.  zrow: the local row (written by this
-// CTA's own threads, column by column, before the call).
+// with the epoch (release, system scope).  a: 0 = z, 1 = z_s.  zrow: the local row, written by this
+// CTA before the call (a __syncthreads precedes).  Columns ER_COLS * blockIdx.x + [0, ER_COLS).
 template <class V>
 __device__ __forceinline__ void push_edge_tile(const Geo& g, const P2P& pp, int a, int side, const V* zrow,
                                                int epoch) {
     V* dst = (V*)(side == 0 ? pp.dst_lo[a] : pp.dst_hi[a]);
     int* fl = side == 0 ? pp.fdst_lo : pp.fdst_hi;
     if (dst == nullptr || fl == nullptr) return;  // no neighbour on this side (uniform per CTA)
-    const int i = blockIdx.x * 128 + threadIdx.x;
+    const int c = threadIdx.x % ER_COLS, kl = threadIdx.x / ER_COLS, nl = blockDim.x / ER_COLS;
+    const int i = blockIdx.x * ER_COLS + c;
 #ifndef EG_MUTATE_NO_HALO_PUSH  // mutation check of the P2P tests (scripts/build_variant.sh): flags only
     if (i < g.nx)
-        for (int k = 0; k < (int)g.nz; ++k) dst[(int64_t)k * g.nx + i] = zrow[(int64_t)k * g.nx + i];
+        for (int k = kl; k < (int)g.nz; k += nl) dst[(int64_t)k * g.nx + i] = zrow[(int64_t)k * g.nx + i];
 #endif
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -929,11 +939,18 @@ __device__ __forceinline__ void push_edge_tile(const Geo& g, const P2P& pp, int 
     }
 }
 
+// Fused schedule, latitude bands: z (KIND 1) / z_s (KIND 2) of the band's first and last rows,
+// ahead of / beside the phase kernel (which recomputes these rows bitwise identically and is the
+// one that writes z, p / s for them), so that they reach the neighbours' ghost rows while it runs.
+// zout: scratch rows [2][row] (row 0, row nyl-1); P2P: pushed to the neighbours from here.
+// The update f and the Thomas solve of thomas_tm_tile, operation for operation: 512 threads load
+// f and (U, D) of all levels of 64 columns into shared memory (8 levels at a time), 64 threads run
+// the elimination and back substitution there, 512 threads store.
+// grid (ceil(nx/64), 2): blockIdx.y 0 -> local row 0, 1 -> local row nyl-1.  smem er_smem_bytes.
 template <int MODE, int KIND>
-__global__ void __launch_bounds__(128, 4) k_edge_rows(Geo g, Vecs<MODE> vv, float* __restrict__ zout, P2P pp) {
+__global__ void __launch_bounds__(ER_THREADS) k_edge_rows(Geo g, Vecs<MODE> vv, float* __restrict__ zout, P2P pp) {
     static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
-    extern __shared__ __align__(16) unsigned char smraw[];
-    __shared__ uint32_t tm_base;
+    extern __shared__ __align__(16) float ersm[];
     const DevState* st = vv.st;
     if (st->halt != H_RUN) return;
     float beta = 0.f, omega = 0.f, alpha = 0.f;
@@ -945,19 +962,62 @@ __global__ void __launch_bounds__(128, 4) k_edge_rows(Geo g, Vecs<MODE> vv, floa
     } else {
         alpha = (float)st->alpha_v;
     }
-    const uint32_t base = tm_alloc128(&tm_base);
-    const int warp = threadIdx.x >> 5;
-    const int nx = (int)g.nx;
-    const int i_raw = blockIdx.x * 128 + threadIdx.x;
+    const int nx = (int)g.nx, nz = (int)g.nz;
+    float* F = ersm;                      // f, then y, then z   [nz][64]
+    float* U = ersm + nz * ER_COLS;       // U, then c'
+    float* D = U + nz * ER_COLS;
+    const int c = threadIdx.x % ER_COLS, kl = threadIdx.x / ER_COLS;
+    constexpr int NL = ER_THREADS / ER_COLS;
+    const int i_raw = blockIdx.x * ER_COLS + c;
     const bool act = i_raw < nx;
-    const int i = act ? i_raw : nx - 1;
+    const int i = act ? i_raw : nx - 1;  // inactive lanes read a valid column, never store
     const int64_t row = blockIdx.y == 0 ? 0 : g.nyl - 1;
+    const int64_t base = row * g.row + i;
+    const float* __restrict__ A0 = vv.r + base;
+    // p = v = 0 after a (re)start: read r in their place with beta = 0 (as thomas_tm_tile)
+    const float* __restrict__ Pp = (KIND == 1 && fresh ? vv.r : vv.p) + base;
+    const float* __restrict__ Vv = (KIND == 1 && fresh ? vv.r : vv.v) + base;
+    if (KIND == 1 && fresh) beta = 0.f;
+    const float* __restrict__ UD = vv.B2 + 2 * base;
+    for (int k = kl; k < nz; k += NL) {
+        const int64_t o = (int64_t)k * nx;
+        float f;
+        if (KIND == 1) f = fmaf(beta, fmaf(-omega, Vv[o], Pp[o]), A0[o]);
+        else f = fmaf(-alpha, Vv[o], A0[o]);
+        const VecN<float, 2> ud = ldv<2>(UD + 2 * o);
+        F[k * ER_COLS + c] = f;
+        U[k * ER_COLS + c] = ud.v[0];
+        D[k * ER_COLS + c] = ud.v[1];
+    }
+    __syncthreads();
+    if (threadIdx.x < ER_COLS) {
+        float cprev = 0.f, yprev = 0.f;
+        for (int k = 0; k < nz; ++k) {
+            const float u = U[k * ER_COLS + c], d = D[k * ER_COLS + c], f = F[k * ER_COLS + c];
+            float cc, y;
+            if (k == 0) {
+                cc = u;
+                y = f;
+            } else {
+                const float inv = rcp_fast<float>(fmaf(-d, cprev, 1.f));
+                cc = u * inv;
+                y = fmaf(-d, yprev, f) * inv;
+            }
+            U[k * ER_COLS + c] = cc;
+            F[k * ER_COLS + c] = y;
+            cprev = cc;
+            yprev = y;
+        }
+        float zn = yprev;
+        for (int k = nz - 2; k >= 0; --k) {
+            zn = fmaf(-U[k * ER_COLS + c], zn, F[k * ER_COLS + c]);
+            F[k * ER_COLS + c] = zn;
+        }
+    }
+    __syncthreads();
     float* zrow = zout + (int64_t)blockIdx.y * g.row;
-    // thomas_tm_tile stores z at zout + row * g.row + (k, i): shift the base so that it lands in zrow
-    float* zo = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(zrow) - (uintptr_t)(row * g.row * sizeof(float)));
-    thomas_tm_tile<MODE, KIND, false>(g, vv, row * g.row, i, act, base + ((uint32_t)(warp * 32) << 16),
-                                      reinterpret_cast<float*>(smraw), beta, omega, alpha, fresh, nullptr, zo);
-    tm_free128(base);
+    if (act)
+        for (int k = kl; k < nz; k += NL) zrow[(int64_t)k * nx + i] = F[k * ER_COLS + c];
     if (pp.on) {
         __syncthreads();
         push_edge_tile<float>(g, pp, KIND - 1, (int)blockIdx.y, zrow, *(volatile const int*)&st->epoch);
@@ -965,28 +1025,32 @@ __global__ void __launch_bounds__(128, 4) k_edge_rows(Geo g, Vecs<MODE> vv, floa
 }
 
 // P2P transport, 5-kernel schedule: push the edge rows of z (a = 0) / z_s (a = 1) that the Thomas
-// kernel just wrote.  grid (ceil(nx/128), 2), 128 threads; blockIdx.y = side as in push_edge_tile.
+// kernel just wrote.  grid (ceil(nx/64), 2), 256 threads; blockIdx.y = side as in push_edge_tile.
 template <class V>
-__global__ void __launch_bounds__(128) k_push_rows(Geo g, const V* __restrict__ z, const DevState* st, P2P pp, int a) {
+__global__ void __launch_bounds__(256) k_push_rows(Geo g, const V* __restrict__ z, const DevState* st, P2P pp, int a) {
     if (st->halt != H_RUN) return;
     const int64_t row = blockIdx.y == 0 ? 0 : g.nyl - 1;
     push_edge_tile<V>(g, pp, a, (int)blockIdx.y, z + row * g.row, *(volatile const int*)&st->epoch);
 }
 
-// P2P transport: wait until the neighbours' pushes of this epoch have landed in the ghost rows of z
-// (a = 0) / z_s (a = 1): flags [a][side][tile], side 0 from rank-1 (wlo), 1 from rank+1 (whi).  A
-// kernel of its own, so that the edge-row stencil launched after it reads ghost rows no write can
-// still be in flight to (its loads may take the read-only path).  One CTA, any width.
-__global__ void __launch_bounds__(256) k_p2p_wait(DevState* st, P2P pp, int a, int wlo, int whi) {
-    if (st->halt != H_RUN) return;
-    const int epoch = *(volatile const int*)&st->epoch;
-    bool bad = false;
-    for (int t = threadIdx.x; t < 2 * pp.tiles; t += blockDim.x) {
-        const int side = t / pp.tiles;
-        if (side == 0 ? !wlo : !whi) continue;
-        if (!wait_flag_sys(pp.hflag + a * 2 * pp.tiles + t, epoch, pp.timeout_ns)) bad = true;
+// The P2P wait of an edge-row stencil CTA (128 columns = flags 2 blockIdx.x, 2 blockIdx.x + 1):
+// the neighbours' pushes of this epoch into the ghost row(s) its row reads.  hw: this rank's halo
+// flags of the array [side][tiles64] (NULL: no wait).  false on timeout.
+struct HWait {
+    const int* f;
+    int tiles64;
+    int wlo, whi;      // rank-1 / rank+1 exist
+    long long timeout_ns;
+};
+__device__ __forceinline__ bool edge_wait(const HWait& hw, int64_t jl, int64_t nyl, int epoch) {
+    bool ok = true;
+    for (int h = 0; h < 2; ++h) {
+        const int t = 2 * (int)blockIdx.x + h;
+        if (t >= hw.tiles64) break;
+        if (hw.wlo && jl == 0) ok = wait_flag_sys(hw.f + t, epoch, hw.timeout_ns) && ok;
+        if (hw.whi && jl == nyl - 1) ok = wait_flag_sys(hw.f + hw.tiles64 + t, epoch, hw.timeout_ns) && ok;
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) st->halt = H_PEER_TIMEOUT;
+    return ok;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1258,6 +1322,100 @@ __global__ void __launch_bounds__(RW, 4) k_stencil(Geo g, Vecs<MODE> vv,
 #pragma unroll
                 for (int a = 0; a < NA; ++a) cur[e][a] = nxt[e][a];
             zup_c = zup_n;
+        }
+    }
+    if (DOTS != 0) write_slots<NQ>(g, vv.slots, acc, MODE == 2 ? 0x7u : 0x0u, jl);
+}
+
+// The stencil (and its dot-product slots) of a few rows — the band-edge rows of latitude bands,
+// after their ghost rows arrived — staged for latency (see k_edge_rows): per chunk of SR_KC levels,
+// 512 threads (4 level lanes x 128 columns) compute y = Ahat z for every (column, level) at once,
+// the 128 column threads then add their terms in level order from shared memory, so each column's
+// partials and the CTA's slot are k_stencil's, operation for operation.  (The 384 extra threads
+// join the CTA sum with zero partials: a sum that starts at +0.0 is never -0.0, so adding +0.0 leaves
+// every bit.)  Ghost rows are read through L2 (ld.global.cg): with the P2P transport this CTA first
+// waits (hw.f != NULL) for the neighbours' pushes of this epoch, which may land while it runs.
+// grid (tiles, rows of rm), SR_THREADS.
+#ifdef EG_SR_THREADS
+constexpr int SR_THREADS = EG_SR_THREADS, SR_KC = 16;
+#else
+constexpr int SR_THREADS = 512, SR_KC = 16;
+#endif
+template <int MODE, int DOTS>
+__global__ void __launch_bounds__(SR_THREADS) k_stencil_rows(Geo g, Vecs<MODE> vv,
+                                                             const typename Prec<MODE>::V* __restrict__ z,
+                                                             typename Prec<MODE>::V* __restrict__ y,
+                                                             const typename Prec<MODE>::V* __restrict__ aux, RowMap rm,
+                                                             HWait hw) {
+    using V = typename Prec<MODE>::V;
+    if (DOTS != 0 && vv.st->halt != H_RUN) return;
+    constexpr int NQ = DOTS == 2 ? 3 : 1;
+    __shared__ V sa[SR_KC][RW], sx[SR_KC][RW];
+    const int64_t jl = rm.lo + (int64_t)blockIdx.y * rm.step, jg = g.j0 + jl;
+    if (hw.f != nullptr) {
+        __shared__ int okw;
+        if (threadIdx.x == 0) okw = edge_wait(hw, jl, g.nyl, *(volatile const int*)&vv.st->epoch);
+        __syncthreads();
+        if (!okw) {
+            if (threadIdx.x == 0) vv.st->halt = H_PEER_TIMEOUT;
+            return;
+        }
+    }
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+    const int c = threadIdx.x % RW, kl = threadIdx.x / RW;
+    constexpr int NL = SR_THREADS / RW;
+    const int i = blockIdx.x * RW + c;
+    const bool act = i < g.nx;
+    const int nx = (int)g.nx, nz = (int)g.nz;
+    const int ii = act ? i : 0;
+    const int64_t rb = jl * g.row;
+    const int iE = (ii + 1 == nx) ? 0 : ii + 1, iW = (ii == 0) ? nx - 1 : ii - 1;
+    const V* zc = z + rb + ii;
+    const V* zE = z + rb + iE;
+    const V* zW = z + rb + iW;
+    const V* zN = (jg < g.ny - 1) ? zc + g.row : zc;
+    const V* zS = (jg > 0) ? zc - g.row : zc;
+    const V* __restrict__ b4 = vv.B4 + 4 * (rb + ii);
+    const V* __restrict__ b2 = vv.B2 + 2 * (rb + ii);
+    V* __restrict__ yo = y + rb + ii;
+    for (int k0 = 0; k0 < nz; k0 += SR_KC) {
+        if (act) {
+            for (int k = k0 + kl; k < k0 + SR_KC && k < nz; k += NL) {
+                const int o = k * nx;
+                const VecN<V, 4> h4 = ldv<4>(b4 + 4 * o);
+                const VecN<V, 2> h2 = ldv<2>(b2 + 2 * o);
+                const V zp = __ldcg(zc + min(k + 1, nz - 1) * nx);  // multiplied by U = 0 on the top level
+                const V zm = k == 0 ? (V)0 : __ldcg(zc + (k - 1) * nx);
+                V a = __ldcg(zc + o);
+                a = fma(h4.v[0], __ldcg(zE + o), a);
+                a = fma(h4.v[1], __ldcg(zW + o), a);
+                a = fma(h4.v[2], __ldcg(zN + o), a);
+                a = fma(h4.v[3], __ldcg(zS + o), a);
+                a = fma(h2.v[0], zp, a);
+                a = fma(h2.v[1], zm, a);
+                yo[o] = a;
+                sa[k - k0][c] = a;
+                if (DOTS) sx[k - k0][c] = aux[rb + ii + o];
+            }
+        }
+        if (DOTS != 0) {
+            __syncthreads();
+            if (threadIdx.x < RW && act) {
+                for (int k = k0; k < k0 + SR_KC && k < nz; ++k) {
+                    const V a = sa[k - k0][c];
+                    if (DOTS == 1) {
+                        acc_dot<MODE>(acc[0], sx[k - k0][c], a);
+                    } else {
+                        const V sv = sx[k - k0][c];
+                        acc_dot<MODE>(acc[0], a, sv);
+                        acc_dot<MODE>(acc[1], a, a);
+                        acc_dot<MODE>(acc[2], sv, sv);
+                    }
+                }
+            }
+            __syncthreads();
         }
     }
     if (DOTS != 0) write_slots<NQ>(g, vv.slots, acc, MODE == 2 ? 0x7u : 0x0u, jl);
