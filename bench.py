@@ -428,6 +428,8 @@ def run_ours(args, prob, ws, rank, local):
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
+                     "peak_note": "the measured copy bandwidth (1:1 read:write); a read-dominated kernel "
+                                  "(the stencils read 8 bytes per byte written) can exceed it: frac > 1",
                      "alg_bytes_per_launch": kbytes},
         "iteration_roofline": {"alg_bytes_per_point": B_ALG[args.precision],
                                "achieved_GBps": B_ALG[args.precision] * n * value / 1e9,

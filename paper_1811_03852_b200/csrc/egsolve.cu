@@ -85,8 +85,9 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t fe
     // P2P transport (latitude bands): gather buffers [2][8][3][2] epoch-stamped words and the
     // ghost-row flags [z, z_s][side][64-column tiles] — written by the other ranks through peer memory
     L->off_p2p = o;   o = align_up(o + kP2PGall + 4 * (size_t)((g->nx + 63) / 64) * sizeof(int), A);
-    // latitude bands, fused schedule: k_edge_rows' scratch rows [z, z_s][row 0, row nyl-1][row]
-    L->off_edge = o;  o = align_up(o + 4 * row * L->vsz, A);
+    // latitude bands: k_edge_rows' scratch rows [z, z_s][row 0, row nyl-1][row] (fused schedule),
+    // then k_edge_stencil's arrival counters [2 rows][tiles]
+    L->off_edge = o;  o = align_up(o + 4 * row * L->vsz + 2 * (size_t)L->tiles * sizeof(int), A);
     L->off_state = o; o = align_up(o + sizeof(DevState), A);
     L->base_total = o;
     // EG_FEATURE_TRISOR: colour-split (E,W,N,S), (U,D) and f for the red-black tri-SOR sweeps
@@ -641,8 +642,8 @@ int p2p_push_join(eg_solver* s) {
 
 // stencil of the interior rows (edge = false: the 5-kernel schedule while the ghost rows travel) or
 // of the band-edge rows after their ghost rows arrived (the phase kernel / the interior launch left
-// them out: k_stencil_rows, which with the P2P transport first waits for the neighbours' pushes of
-// array a: 0 = z, 1 = z_s), same arithmetic and reduction slots as the full launch
+// them out: k_edge_stencil, which with the P2P transport first waits for the neighbours'
+// pushes of array a: 0 = z, 1 = z_s), same arithmetic and reduction slots as the full launch
 template <int MODE, int DOTS>
 int stencil_rows(eg_solver* s, const typename Prec<MODE>::V* z, typename Prec<MODE>::V* y,
                  const typename Prec<MODE>::V* aux, bool edge, int a = 0) {
@@ -653,17 +654,14 @@ int stencil_rows(eg_solver* s, const typename Prec<MODE>::V* z, typename Prec<MO
     if (edge) return EG_OK;
 #endif
     Vecs<MODE> v = vecs<MODE>(s, s->x64);
-#ifdef EG_DEBUG_OLD_EDGE_STENCIL
-    if (false) {
-#else
     if (edge) {
-#endif
         HWait hw{nullptr, 0, 0, 0, 0};
         if (s->pp.on)
             hw = HWait{s->pp.hflag + a * 2 * s->pp.tiles, s->pp.tiles, s->rank > 0, s->rank < s->nranks - 1,
                        s->pp.timeout_ns};
-        k_stencil_rows<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n), SR_THREADS, 0, s->st>>>(s->geo, v, z, y, aux,
-                                                                                                     rm, hw);
+        k_edge_stencil<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n, (unsigned)((s->grid.nz + 3) / 4)), 512,
+                                     es_smem_bytes<MODE>(), s->st>>>(s->geo, v, z, y, aux, rm, hw,
+                                                                     (int*)(s->ws + s->L.off_edge + 4 * s->L.row * s->L.vsz));
     } else {
         k_stencil<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n), RW, 0, s->st>>>(s->geo, v, z, y, aux, rm);
     }
@@ -1470,6 +1468,8 @@ int set_thomas_smem(eg_solver* s) {
     CK(cudaFuncSetAttribute(k_sor_half<MODE, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
     CK(cudaFuncSetAttribute(k_sor_half<MODE, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
     CK(cudaFuncSetAttribute(k_sor_half<MODE, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_th));
+    CK(cudaFuncSetAttribute(k_edge_stencil<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)es_smem_bytes<MODE>()));
+    CK(cudaFuncSetAttribute(k_edge_stencil<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)es_smem_bytes<MODE>()));
     int rc = set_thomas_smem_c<MODE, 1>(s);
     if (!rc) rc = set_thomas_smem_c<MODE, 2>(s);
     if constexpr (MODE != 0) {
@@ -1794,6 +1794,9 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
         return rc;
     }
     int rc = prec == EG_FP64 ? set_thomas_smem<0>(s) : prec == EG_MIXED ? set_thomas_smem<1>(s) : set_thomas_smem<2>(s);
+    // k_edge_stencil's arrival counters start at 0 (each launch leaves them at 0)
+    if (rc == EG_OK && cudaMemsetAsync(s->ws + L.off_edge + 4 * L.row * L.vsz, 0, 2 * (size_t)L.tiles * sizeof(int), s->st) != cudaSuccess)
+        rc = fail(s, EG_ERR_CUDA, "edge-stencil counters");
     if (rc == EG_OK && s->use_tm64) {
         for (const void* f : {(const void*)k_thomas_tm64<0>, (const void*)k_thomas_tm64<1>, (const void*)k_thomas_tm64<2>})
             if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, TM64_SMEM) != cudaSuccess)

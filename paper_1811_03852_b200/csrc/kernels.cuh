@@ -912,7 +912,8 @@ __global__ void __launch_bounds__(128, 2) k_thomas_tm64(Geo g, Vecs<0> vv, const
 // kernels, operation for operation (bitwise equal results).
 constexpr int ER_COLS = 64;       // columns per CTA of the edge-row kernels (one P2P flag each)
 constexpr int ER_THREADS = 512;   // 8 level lanes x 64 columns
-inline size_t er_smem_bytes(int64_t nz) { return (size_t)3 * nz * ER_COLS * sizeof(float); }
+constexpr int ER_MAXL = 16;       // levels per lane: nz <= 128 (the fused schedule's limit)
+inline size_t er_smem_bytes(int64_t nz) { return (size_t)5 * nz * ER_COLS * sizeof(float); }
 
 // P2P transport (pp.on): this CTA's ER_COLS columns of the band's edge row go straight into the
 // neighbour's ghost row through peer memory (side 0: local row 0 -> rank-1's ghost row nyl; side 1:
@@ -963,9 +964,11 @@ __global__ void __launch_bounds__(ER_THREADS) k_edge_rows(Geo g, Vecs<MODE> vv, 
         alpha = (float)st->alpha_v;
     }
     const int nx = (int)g.nx, nz = (int)g.nz;
-    float* F = ersm;                      // f, then y, then z   [nz][64]
-    float* U = ersm + nz * ER_COLS;       // U, then c'
+    float* F = ersm;                      // f, then z   [nz][64]
+    float* U = ersm + nz * ER_COLS;
     float* D = U + nz * ER_COLS;
+    float* C = D + nz * ER_COLS;          // c'
+    float* Y = C + nz * ER_COLS;          // y
     const int c = threadIdx.x % ER_COLS, kl = threadIdx.x / ER_COLS;
     constexpr int NL = ER_THREADS / ER_COLS;
     const int i_raw = blockIdx.x * ER_COLS + c;
@@ -979,19 +982,34 @@ __global__ void __launch_bounds__(ER_THREADS) k_edge_rows(Geo g, Vecs<MODE> vv, 
     const float* __restrict__ Vv = (KIND == 1 && fresh ? vv.r : vv.v) + base;
     if (KIND == 1 && fresh) beta = 0.f;
     const float* __restrict__ UD = vv.B2 + 2 * base;
-    for (int k = kl; k < nz; k += NL) {
-        const int64_t o = (int64_t)k * nx;
-        float f;
-        if (KIND == 1) f = fmaf(beta, fmaf(-omega, Vv[o], Pp[o]), A0[o]);
-        else f = fmaf(-alpha, Vv[o], A0[o]);
-        const VecN<float, 2> ud = ldv<2>(UD + 2 * o);
-        F[k * ER_COLS + c] = f;
-        U[k * ER_COLS + c] = ud.v[0];
-        D[k * ER_COLS + c] = ud.v[1];
+    {  // all of this thread's levels (<= ER_MAXL) loaded before any is used: one round of latency
+        float a_[ER_MAXL], p_[ER_MAXL], v_[ER_MAXL];
+        VecN<float, 2> ud_[ER_MAXL];
+#pragma unroll
+        for (int e = 0; e < ER_MAXL; ++e) {
+            const int64_t o = (int64_t)min(kl + e * NL, nz - 1) * nx;
+            a_[e] = A0[o];
+            v_[e] = Vv[o];
+            p_[e] = KIND == 1 ? Pp[o] : 0.f;
+            ud_[e] = ldv<2>(UD + 2 * o);
+        }
+#pragma unroll
+        for (int e = 0; e < ER_MAXL; ++e) {
+            const int k = kl + e * NL;
+            if (k < nz) {
+                float f;
+                if (KIND == 1) f = fmaf(beta, fmaf(-omega, v_[e], p_[e]), a_[e]);
+                else f = fmaf(-alpha, v_[e], a_[e]);
+                F[k * ER_COLS + c] = f;
+                U[k * ER_COLS + c] = ud_[e].v[0];
+                D[k * ER_COLS + c] = ud_[e].v[1];
+            }
+        }
     }
     __syncthreads();
     if (threadIdx.x < ER_COLS) {
         float cprev = 0.f, yprev = 0.f;
+#pragma unroll 8
         for (int k = 0; k < nz; ++k) {
             const float u = U[k * ER_COLS + c], d = D[k * ER_COLS + c], f = F[k * ER_COLS + c];
             float cc, y;
@@ -1003,14 +1021,16 @@ __global__ void __launch_bounds__(ER_THREADS) k_edge_rows(Geo g, Vecs<MODE> vv, 
                 cc = u * inv;
                 y = fmaf(-d, yprev, f) * inv;
             }
-            U[k * ER_COLS + c] = cc;
-            F[k * ER_COLS + c] = y;
+            C[k * ER_COLS + c] = cc;
+            Y[k * ER_COLS + c] = y;
             cprev = cc;
             yprev = y;
         }
         float zn = yprev;
+        F[(nz - 1) * ER_COLS + c] = zn;
+#pragma unroll 8
         for (int k = nz - 2; k >= 0; --k) {
-            zn = fmaf(-U[k * ER_COLS + c], zn, F[k * ER_COLS + c]);
+            zn = fmaf(-C[k * ER_COLS + c], zn, Y[k * ER_COLS + c]);
             F[k * ER_COLS + c] = zn;
         }
     }
@@ -1328,97 +1348,121 @@ __global__ void __launch_bounds__(RW, 4) k_stencil(Geo g, Vecs<MODE> vv,
 }
 
 // The stencil (and its dot-product slots) of a few rows — the band-edge rows of latitude bands,
-// after their ghost rows arrived — staged for latency (see k_edge_rows): per chunk of SR_KC levels,
-// 512 threads (4 level lanes x 128 columns) compute y = Ahat z for every (column, level) at once,
-// the 128 column threads then add their terms in level order from shared memory, so each column's
-// partials and the CTA's slot are k_stencil's, operation for operation.  (The 384 extra threads
-// join the CTA sum with zero partials: a sum that starts at +0.0 is never -0.0, so adding +0.0 leaves
-// every bit.)  Ghost rows are read through L2 (ld.global.cg): with the P2P transport this CTA first
-// waits (hw.f != NULL) for the neighbours' pushes of this epoch, which may land while it runs.
-// grid (tiles, rows of rm), SR_THREADS.
-#ifdef EG_SR_THREADS
-constexpr int SR_THREADS = EG_SR_THREADS, SR_KC = 16;
-#else
-constexpr int SR_THREADS = 512, SR_KC = 16;
-#endif
+// after their ghost rows arrived.  Two rows are too few for k_stencil's column walk (nz dependent
+// rounds of loads in 24 CTAs), so one latency-short kernel, k_edge_stencil:
+//  * every CTA computes y = Ahat z at 4 levels of 128 columns of one row, one point per thread
+//    (grid (tiles, rows, ceil(nz / 4))): a single round of loads.  With the P2P transport it first
+//    waits (hw.f != NULL) for the neighbours' pushes of this epoch, which may land while the grid
+//    runs, so z is read through L2 (ld.global.cg);
+//  * the last CTA to finish a (tile, row) — an arrival counter per (row, tile) in ctr, reset by it —
+//    loads y and aux of every level of its 128 columns into shared memory (one round, L2) and its
+//    first 128 threads add their column's terms in level order, then the CTA's slot: k_stencil's
+//    sums operation for operation (the other 384 threads join the CTA sum with zero partials: a sum
+//    that starts at +0.0 is never -0.0, so adding +0.0 leaves every bit).
+// Bitwise equal to k_stencil's y and slots.  Dynamic smem: es_smem_bytes.
+constexpr int ES_KC = 64;  // levels staged per round of the dot pass
+template <int MODE>
+inline size_t es_smem_bytes() { return (size_t)2 * ES_KC * RW * sizeof(typename Prec<MODE>::V); }
 template <int MODE, int DOTS>
-__global__ void __launch_bounds__(SR_THREADS) k_stencil_rows(Geo g, Vecs<MODE> vv,
-                                                             const typename Prec<MODE>::V* __restrict__ z,
-                                                             typename Prec<MODE>::V* __restrict__ y,
-                                                             const typename Prec<MODE>::V* __restrict__ aux, RowMap rm,
-                                                             HWait hw) {
+__global__ void __launch_bounds__(512) k_edge_stencil(Geo g, Vecs<MODE> vv, const typename Prec<MODE>::V* __restrict__ z,
+                                                      typename Prec<MODE>::V* __restrict__ y,
+                                                      const typename Prec<MODE>::V* __restrict__ aux, RowMap rm, HWait hw,
+                                                      int* __restrict__ ctr) {
     using V = typename Prec<MODE>::V;
-    if (DOTS != 0 && vv.st->halt != H_RUN) return;
-    constexpr int NQ = DOTS == 2 ? 3 : 1;
-    __shared__ V sa[SR_KC][RW], sx[SR_KC][RW];
+    extern __shared__ __align__(16) unsigned char essm[];
+    if (vv.st->halt != H_RUN) return;
     const int64_t jl = rm.lo + (int64_t)blockIdx.y * rm.step, jg = g.j0 + jl;
+    __shared__ int flag;
     if (hw.f != nullptr) {
-        __shared__ int okw;
-        if (threadIdx.x == 0) okw = edge_wait(hw, jl, g.nyl, *(volatile const int*)&vv.st->epoch);
+        if (threadIdx.x == 0) flag = edge_wait(hw, jl, g.nyl, *(volatile const int*)&vv.st->epoch);
         __syncthreads();
-        if (!okw) {
+        if (!flag) {
             if (threadIdx.x == 0) vv.st->halt = H_PEER_TIMEOUT;
             return;
         }
+        __syncthreads();
     }
+    const int c = threadIdx.x % RW;
+    const int i = blockIdx.x * RW + c;
+    const int nx = (int)g.nx, nz = (int)g.nz;
+    const int64_t rb = jl * g.row;
+    {
+        const int k = (int)blockIdx.z * 4 + (int)threadIdx.x / RW;
+        if (i < nx && k < nz) {
+            const int iE = (i + 1 == nx) ? 0 : i + 1, iW = (i == 0) ? nx - 1 : i - 1;
+            const V* zc = z + rb + i;
+            const V* zN = (jg < g.ny - 1) ? zc + g.row : zc;
+            const V* zS = (jg > 0) ? zc - g.row : zc;
+            const int o = k * nx;
+            const VecN<V, 4> h4 = ldv<4>(vv.B4 + 4 * (rb + i + o));
+            const VecN<V, 2> h2 = ldv<2>(vv.B2 + 2 * (rb + i + o));
+            const V zp = __ldcg(zc + min(k + 1, nz - 1) * nx);  // multiplied by U = 0 on the top level
+            const V zm = k == 0 ? (V)0 : __ldcg(zc + (k - 1) * nx);
+            V a = __ldcg(zc + o);
+            a = fma(h4.v[0], __ldcg(z + rb + iE + o), a);
+            a = fma(h4.v[1], __ldcg(z + rb + iW + o), a);
+            a = fma(h4.v[2], __ldcg(zN + o), a);
+            a = fma(h4.v[3], __ldcg(zS + o), a);
+            a = fma(h2.v[0], zp, a);
+            a = fma(h2.v[1], zm, a);
+            y[rb + i + o] = a;
+        }
+    }
+    if (DOTS == 0) return;
+    // the last CTA of this (tile, row) to arrive sums the column terms
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this CTA's y before its arrival
+        int* cp = ctr + blockIdx.y * gridDim.x + blockIdx.x;
+        flag = atomicAdd(cp, 1) == (int)gridDim.z - 1;
+        if (flag) *cp = 0;  // every CTA of the (tile, row) has arrived: ready for the next launch
+    }
+    __syncthreads();
+    if (!flag) return;
+    __threadfence();
+    constexpr int NQ = DOTS == 2 ? 3 : 1;
+    V* sy = reinterpret_cast<V*>(essm);
+    V* sx = sy + ES_KC * RW;
     double acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-    const int c = threadIdx.x % RW, kl = threadIdx.x / RW;
-    constexpr int NL = SR_THREADS / RW;
-    const int i = blockIdx.x * RW + c;
-    const bool act = i < g.nx;
-    const int nx = (int)g.nx, nz = (int)g.nz;
-    const int ii = act ? i : 0;
-    const int64_t rb = jl * g.row;
-    const int iE = (ii + 1 == nx) ? 0 : ii + 1, iW = (ii == 0) ? nx - 1 : ii - 1;
-    const V* zc = z + rb + ii;
-    const V* zE = z + rb + iE;
-    const V* zW = z + rb + iW;
-    const V* zN = (jg < g.ny - 1) ? zc + g.row : zc;
-    const V* zS = (jg > 0) ? zc - g.row : zc;
-    const V* __restrict__ b4 = vv.B4 + 4 * (rb + ii);
-    const V* __restrict__ b2 = vv.B2 + 2 * (rb + ii);
-    V* __restrict__ yo = y + rb + ii;
-    for (int k0 = 0; k0 < nz; k0 += SR_KC) {
-        if (act) {
-            for (int k = k0 + kl; k < k0 + SR_KC && k < nz; k += NL) {
-                const int o = k * nx;
-                const VecN<V, 4> h4 = ldv<4>(b4 + 4 * o);
-                const VecN<V, 2> h2 = ldv<2>(b2 + 2 * o);
-                const V zp = __ldcg(zc + min(k + 1, nz - 1) * nx);  // multiplied by U = 0 on the top level
-                const V zm = k == 0 ? (V)0 : __ldcg(zc + (k - 1) * nx);
-                V a = __ldcg(zc + o);
-                a = fma(h4.v[0], __ldcg(zE + o), a);
-                a = fma(h4.v[1], __ldcg(zW + o), a);
-                a = fma(h4.v[2], __ldcg(zN + o), a);
-                a = fma(h4.v[3], __ldcg(zS + o), a);
-                a = fma(h2.v[0], zp, a);
-                a = fma(h2.v[1], zm, a);
-                yo[o] = a;
-                sa[k - k0][c] = a;
-                if (DOTS) sx[k - k0][c] = aux[rb + ii + o];
+    constexpr int PER = ES_KC * RW / 512;  // elements per thread per round
+    for (int k0 = 0; k0 < nz; k0 += ES_KC) {
+        const int kn = min(ES_KC, nz - k0);
+        V ty[PER], tx[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {  // all loads of the round first: [level][column], coalesced
+            const int e = threadIdx.x + u * 512, kk = e / RW, ii = blockIdx.x * RW + e % RW;
+            if (kk < kn && ii < nx) {
+                const int64_t q = rb + ii + (int64_t)(k0 + kk) * nx;
+                ty[u] = __ldcg(y + q);
+                tx[u] = aux[q];
             }
         }
-        if (DOTS != 0) {
-            __syncthreads();
-            if (threadIdx.x < RW && act) {
-                for (int k = k0; k < k0 + SR_KC && k < nz; ++k) {
-                    const V a = sa[k - k0][c];
-                    if (DOTS == 1) {
-                        acc_dot<MODE>(acc[0], sx[k - k0][c], a);
-                    } else {
-                        const V sv = sx[k - k0][c];
-                        acc_dot<MODE>(acc[0], a, sv);
-                        acc_dot<MODE>(acc[1], a, a);
-                        acc_dot<MODE>(acc[2], sv, sv);
-                    }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int e = threadIdx.x + u * 512, kk = e / RW, ii = blockIdx.x * RW + e % RW;
+            if (kk < kn && ii < nx) {
+                sy[e] = ty[u];
+                sx[e] = tx[u];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < RW && i < nx) {
+            for (int kk = 0; kk < kn; ++kk) {
+                const V a = sy[kk * RW + c], sv = sx[kk * RW + c];
+                if (DOTS == 1) {
+                    acc_dot<MODE>(acc[0], sv, a);
+                } else {
+                    acc_dot<MODE>(acc[0], a, sv);
+                    acc_dot<MODE>(acc[1], a, a);
+                    acc_dot<MODE>(acc[2], sv, sv);
                 }
             }
-            __syncthreads();
         }
+        __syncthreads();
     }
-    if (DOTS != 0) write_slots<NQ>(g, vv.slots, acc, MODE == 2 ? 0x7u : 0x0u, jl);
+    write_slots<NQ>(g, vv.slots, acc, MODE == 2 ? 0x7u : 0x0u, jl);
 }
 
 // ---------------------------------------------------------------------------------------------

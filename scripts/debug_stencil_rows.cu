@@ -1,4 +1,4 @@
-// A/B of k_stencil_rows against k_stencil on the same random inputs (debug harness, one GPU):
+// A/B of the band-edge stencil (k_edge_stencil) against k_stencil on the same random inputs (debug harness, one GPU):
 // y and the reduction slots of the given rows must be bitwise equal, per precision mode.
 #include <cstdio>
 #include <cstdlib>
@@ -57,7 +57,10 @@ int run(int nx, int nyl, int nz) {
     vv.slots = s1;
     k_stencil<MODE, DOTS><<<dim3(g.tiles, nr), RW>>>(g, vv, z + row, y1, a, rm);
     vv.slots = s2;
-    k_stencil_rows<MODE, DOTS><<<dim3(g.tiles, nr), SR_THREADS>>>(g, vv, z + row, y2, a, rm, HWait{nullptr, 0, 0, 0, 0});
+    int* ctr; cudaMalloc(&ctr, 2 * g.tiles * 4); cudaMemset(ctr, 0, 2 * g.tiles * 4);
+    cudaFuncSetAttribute(k_edge_stencil<MODE, DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)es_smem_bytes<MODE>());
+    k_edge_stencil<MODE, DOTS><<<dim3(g.tiles, nr, (nz + 3) / 4), 512, es_smem_bytes<MODE>()>>>(g, vv, z + row, y2, a, rm,
+                                                                                              HWait{nullptr, 0, 0, 0, 0}, ctr);
     double* s3; cudaMalloc(&s3, 3 * nyl * g.tiles * 8); cudaMemset(s3, 0, 3 * nyl * g.tiles * 8);
     vv.slots = s3;
     k_naive<MODE, DOTS><<<dim3(g.tiles, nr), RW>>>(g, vv, y1, a, rm);
@@ -77,7 +80,7 @@ int run(int nx, int nyl, int nz) {
         if (q1[q] != q2[q]) { if (bs < 4) printf("   slot %zu: %.17g vs %.17g\n", q, q1[q], q2[q]); ++bs; }
     int b13 = 0, b23 = 0;
     for (size_t q = 0; q < q1.size(); ++q) { b13 += q1[q] != q3[q]; b23 += q2[q] != q3[q]; }
-    printf("   vs naive: k_stencil %d, k_stencil_rows %d\n", b13, b23);
+    printf("   vs naive: k_stencil %d, edge kernels %d\n", b13, b23);
     printf("MODE %d DOTS %d %dx%dx%d: y mismatches %d, slot mismatches %d (%s)\n", MODE, DOTS, nx, nyl, nz, by, bs,
            cudaGetErrorString(cudaGetLastError()));
     return by + bs;
