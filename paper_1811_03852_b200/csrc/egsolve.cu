@@ -568,7 +568,7 @@ int p2p_reset_flags(eg_solver* s) {
 // ghost row.  Otherwise it runs on s->st.
 // row0 / last_row: the band's row 0 and row nyl-1 as sent (last_row = NULL: row nyl-1 of row0's array)
 int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz, bool async = false,
-         void* last_row = nullptr) {
+         void* last_row = nullptr, bool cst_ordered = false) {
     if (s->nranks == 1) return EG_OK;
     const size_t rowb = (size_t)s->L.row * esz;
     ncclDataType_t ty = esz == 8 ? ncclDouble : ncclFloat;
@@ -581,7 +581,7 @@ int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz, b
         G->last[s->rank] = last;
         if (!lb_barrier(G)) return lb_fail(s);
         // every rank's edge rows are enqueued on the shared stream before this point
-        if (async) {
+        if (async && !cst_ordered) {
             CK(cudaEventRecord(s->ev_edge, s->st));
             CK(cudaStreamWaitEvent(xs, s->ev_edge, 0));
         }
@@ -592,7 +592,7 @@ int halo(eg_solver* s, void* row0, void* ghost_lo, void* ghost_hi, size_t esz, b
         if (!lb_barrier(G)) return lb_fail(s);
         return EG_OK;
     }
-    if (async) {
+    if (async && !cst_ordered) {
         CK(cudaEventRecord(s->ev_edge, s->st));
         CK(cudaStreamWaitEvent(xs, s->ev_edge, 0));
     }
@@ -751,18 +751,21 @@ int halo_start(eg_solver* s, double* z, int a) { return halo_start_t<double>(s, 
 // (which writes s, z_s, t and reads r, v: nothing k_edge_rows reads).  z: on s->st ahead of phase A,
 // which updates p in place and rewrites v, the inputs of k_edge_rows' p update.  Profiled solves
 // keep everything on s->st, where the CUDA events are (and so does the loopback copy transport).
+// z_s on the communication stream?  (Loopback copies: the copies read the neighbours' scratch
+// rows, ordered after their k_edge_rows only if those ran on the one shared stream.)
+bool edge_on_cst(const eg_solver* s, int kind) { return !(s->profiling || kind == 1 || (s->lb && !s->pp.on)); }
+
+// z_s: iteration_fused records ev_edge right after the finaliser and launches phase B BEFORE this
+// (so that the cooperative phase kernel takes its SMs first and k_edge_rows fills the spare ones,
+// instead of holding SMs the cooperative launch then has to wait for)
 template <int MODE, int KIND>
 int edge_exchange(eg_solver* s, Vecs<MODE>& v, typename Prec<MODE>::V* z) {
     using V = typename Prec<MODE>::V;
     const dim3 gedge((unsigned)((s->grid.nx + ER_COLS - 1) / ER_COLS), 2u);
     V* scratch = (V*)(s->ws + s->L.off_edge) + (size_t)(KIND - 1) * 2 * s->L.row;
-    // (loopback copies: the copies read the neighbours' scratch rows, ordered after their
-    // k_edge_rows only if those ran on the one shared stream)
-    cudaStream_t xs = (s->profiling || KIND == 1 || (s->lb && !s->pp.on)) ? s->st : s->cst;
-    if (xs != s->st) {
-        CK(cudaEventRecord(s->ev_edge, s->st));  // after the finaliser that set beta / omega / alpha
-        CK(cudaStreamWaitEvent(xs, s->ev_edge, 0));
-    }
+    const bool on_cst = edge_on_cst(s, KIND);
+    cudaStream_t xs = on_cst ? s->cst : s->st;
+    if (on_cst) CK(cudaStreamWaitEvent(xs, s->ev_edge, 0));  // ev_edge: after the finaliser that set alpha
     {
         ProfScope ps(s, KID_EDGE, 0.0);
         k_edge_rows<MODE, KIND><<<gedge, ER_THREADS, er_smem_bytes(s->grid.nz), xs>>>(s->geo, v, (float*)scratch, s->pp);
@@ -773,10 +776,12 @@ int edge_exchange(eg_solver* s, Vecs<MODE>& v, typename Prec<MODE>::V* z) {
         if (!s->profiling) CK(cudaEventRecord(s->ev_halo, xs));
         return p2p_push_join(s);
     }
-    // (from s->st: halo() orders the exchange on s->cst after k_edge_rows itself)
+    // (from s->st: halo() orders the exchange on s->cst after k_edge_rows itself; on s->cst it
+    // follows k_edge_rows there and must not wait for the phase kernel already on s->st)
     const size_t rowb = (size_t)s->L.row * sizeof(V);
     unsigned char* zr = (unsigned char*)z;
-    if ((rc = halo(s, scratch, zr - rowb, zr + (size_t)s->L.nyl * rowb, sizeof(V), !s->profiling, scratch + s->L.row)))
+    if ((rc = halo(s, scratch, zr - rowb, zr + (size_t)s->L.nyl * rowb, sizeof(V), !s->profiling, scratch + s->L.row,
+                   on_cst)))
         return rc;
     return EG_OK;
 }
@@ -875,12 +880,15 @@ int iteration_fused(eg_solver* s, void* x_it) {
         }
 #endif
         if ((rc = finalize<MODE, W_A>(s, 0))) return rc;
-        if (s->nranks > 1 && (rc = edge_exchange<MODE, 2>(s, v, v.zs))) return rc;
+        const bool zs_beside = s->nranks > 1 && edge_on_cst(s, 2);
+        if (zs_beside) CK(cudaEventRecord(s->ev_edge, s->st));  // z_s edge rows: after this finaliser
+        else if (s->nranks > 1 && (rc = edge_exchange<MODE, 2>(s, v, v.zs))) return rc;
         {
             ProfScope ps(s, KID_PHASE_B);
             CK(launch_ex(true, s->pdl, k_march<MODE, 2>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
                            s->maps));
         }
+        if (zs_beside && (rc = edge_exchange<MODE, 2>(s, v, v.zs))) return rc;
         if (s->nranks > 1) {
             if ((rc = edge_join(s, 1, true))) return rc;
             if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true, 1))) return rc;
