@@ -85,9 +85,10 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t fe
     // P2P transport (latitude bands): gather buffers [2][8][3][2] epoch-stamped words and the
     // ghost-row flags [z, z_s][side][64-column tiles] — written by the other ranks through peer memory
     L->off_p2p = o;   o = align_up(o + kP2PGall + 4 * (size_t)((g->nx + 63) / 64) * sizeof(int), A);
-    // latitude bands: k_edge_rows' scratch rows [z, z_s][row 0, row nyl-1][row] (fused schedule),
-    // then k_edge_stencil's arrival counters [2 rows][tiles]
-    L->off_edge = o;  o = align_up(o + 4 * row * L->vsz + 2 * (size_t)L->tiles * sizeof(int), A);
+    // latitude bands: k_edge_rows' scratch rows [z, z_s][row 0, row nyl-1][row] and the band-edge
+    // copies of p and v [p, v][row 0, row nyl-1][row] (fused schedule), then k_edge_stencil's arrival
+    // counters [2 rows][tiles]
+    L->off_edge = o;  o = align_up(o + 8 * row * L->vsz + 2 * (size_t)L->tiles * sizeof(int), A);
     L->off_state = o; o = align_up(o + sizeof(DevState), A);
     L->base_total = o;
     // EG_FEATURE_TRISOR: colour-split (E,W,N,S), (U,D) and f for the red-black tri-SOR sweeps
@@ -646,7 +647,7 @@ int p2p_push_join(eg_solver* s) {
 // pushes of array a: 0 = z, 1 = z_s), same arithmetic and reduction slots as the full launch
 template <int MODE, int DOTS>
 int stencil_rows(eg_solver* s, const typename Prec<MODE>::V* z, typename Prec<MODE>::V* y,
-                 const typename Prec<MODE>::V* aux, bool edge, int a = 0) {
+                 const typename Prec<MODE>::V* aux, bool edge, int a = 0, bool copy_v = false) {
     RowMap rm;
     const int n = edge ? edge_rows(s, &rm) : interior_rows(s, &rm);
     if (n == 0) return EG_OK;
@@ -655,13 +656,16 @@ int stencil_rows(eg_solver* s, const typename Prec<MODE>::V* z, typename Prec<MO
 #endif
     Vecs<MODE> v = vecs<MODE>(s, s->x64);
     if (edge) {
+        // (fused schedule, phase A: v of the edge rows also into their band-edge copies for k_edge_rows)
+        typename Prec<MODE>::V* ycopy =
+            copy_v ? (typename Prec<MODE>::V*)(s->ws + s->L.off_edge) + 6 * s->L.row : nullptr;
         HWait hw{nullptr, 0, 0, 0, 0};
         if (s->pp.on)
             hw = HWait{s->pp.hflag + a * 2 * s->pp.tiles, s->pp.tiles, s->rank > 0, s->rank < s->nranks - 1,
                        s->pp.timeout_ns};
         k_edge_stencil<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n, (unsigned)((s->grid.nz + 3) / 4)), 512,
                                      es_smem_bytes<MODE>(), s->st>>>(s->geo, v, z, y, aux, rm, hw,
-                                                                     (int*)(s->ws + s->L.off_edge + 4 * s->L.row * s->L.vsz));
+                                                                     (int*)(s->ws + s->L.off_edge + 8 * s->L.row * s->L.vsz), ycopy);
     } else {
         k_stencil<MODE, DOTS><<<dim3((unsigned)s->L.tiles, (unsigned)n), RW, 0, s->st>>>(s->geo, v, z, y, aux, rm);
     }
@@ -751,13 +755,14 @@ int halo_start(eg_solver* s, double* z, int a) { return halo_start_t<double>(s, 
 // (which writes s, z_s, t and reads r, v: nothing k_edge_rows reads).  z: on s->st ahead of phase A,
 // which updates p in place and rewrites v, the inputs of k_edge_rows' p update.  Profiled solves
 // keep everything on s->st, where the CUDA events are (and so does the loopback copy transport).
-// z_s on the communication stream?  (Loopback copies: the copies read the neighbours' scratch
-// rows, ordered after their k_edge_rows only if those ran on the one shared stream.)
-bool edge_on_cst(const eg_solver* s, int kind) { return !(s->profiling || kind == 1 || (s->lb && !s->pp.on)); }
+// the edge rows on the communication stream?  (Loopback copies: the copies read the neighbours'
+// scratch rows, ordered after their k_edge_rows only if those ran on the one shared stream.)
+bool edge_on_cst(const eg_solver* s, int kind) { (void)kind; return !(s->profiling || (s->lb && !s->pp.on)); }
 
-// z_s: iteration_fused records ev_edge right after the finaliser and launches phase B BEFORE this
-// (so that the cooperative phase kernel takes its SMs first and k_edge_rows fills the spare ones,
-// instead of holding SMs the cooperative launch then has to wait for)
+// On s->cst, iteration_fused records ev_edge right after the finaliser and launches the phase
+// kernel BEFORE this (so that the cooperative phase kernel takes its SMs first and k_edge_rows fills
+// the spare ones, instead of holding SMs the cooperative launch then has to wait for).  z (KIND 1)
+// reads p and v of the edge rows from their band-edge copies (pv_edge), which phase A does not touch.
 template <int MODE, int KIND>
 int edge_exchange(eg_solver* s, Vecs<MODE>& v, typename Prec<MODE>::V* z) {
     using V = typename Prec<MODE>::V;
@@ -768,7 +773,8 @@ int edge_exchange(eg_solver* s, Vecs<MODE>& v, typename Prec<MODE>::V* z) {
     if (on_cst) CK(cudaStreamWaitEvent(xs, s->ev_edge, 0));  // ev_edge: after the finaliser that set alpha
     {
         ProfScope ps(s, KID_EDGE, 0.0);
-        k_edge_rows<MODE, KIND><<<gedge, ER_THREADS, er_smem_bytes(s->grid.nz), xs>>>(s->geo, v, (float*)scratch, s->pp);
+        k_edge_rows<MODE, KIND><<<gedge, ER_THREADS, er_smem_bytes(s->grid.nz), xs>>>(
+            s->geo, v, (float*)scratch, s->pp, KIND == 1 ? (float*)(s->ws + s->L.off_edge) + 4 * s->L.row : nullptr);
         CK(cudaGetLastError());
     }
     int rc;
@@ -845,7 +851,9 @@ int iteration_fused(eg_solver* s, void* x_it) {
     int rc;
     if constexpr (MODE != 0) {
         const unsigned grid = (unsigned)(s->mg.strips * s->L.tiles);
-        if (s->nranks > 1 && (rc = edge_exchange<MODE, 1>(s, v, v.z))) return rc;
+        const bool z_beside = s->nranks > 1 && edge_on_cst(s, 1);
+        if (z_beside) CK(cudaEventRecord(s->ev_edge, s->st));  // z edge rows: after the last finaliser
+        else if (s->nranks > 1 && (rc = edge_exchange<MODE, 1>(s, v, v.z))) return rc;
 #ifdef MA_VERIFY
         const int64_t n = s->L.n;
         if (g_vfy.n != n) return fail(s, EG_ERR_CUDA, "MA_VERIFY buffers not allocated for this size");
@@ -862,9 +870,10 @@ int iteration_fused(eg_solver* s, void* x_it) {
             CK(launch_ex(true, s->pdl, k_march<MODE, 1>, grid, MA_THREADS, s->smem_march, s->st, s->geo, v, s->mg, s->ready_flags,
                            s->maps));
         }
+        if (z_beside && (rc = edge_exchange<MODE, 1>(s, v, v.z))) return rc;
         if (s->nranks > 1) {  // the band-edge rows' stencil, once their ghost rows are in
             if ((rc = edge_join(s, 0, true))) return rc;
-            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true, 0))) return rc;
+            if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true, 0, true))) return rc;
         }
 #ifdef MA_VERIFY
         {
@@ -1803,7 +1812,7 @@ int eg_solver_create_ex(const eg_grid* grid, const eg_dist* dist, const double* 
     }
     int rc = prec == EG_FP64 ? set_thomas_smem<0>(s) : prec == EG_MIXED ? set_thomas_smem<1>(s) : set_thomas_smem<2>(s);
     // k_edge_stencil's arrival counters start at 0 (each launch leaves them at 0)
-    if (rc == EG_OK && cudaMemsetAsync(s->ws + L.off_edge + 4 * L.row * L.vsz, 0, 2 * (size_t)L.tiles * sizeof(int), s->st) != cudaSuccess)
+    if (rc == EG_OK && cudaMemsetAsync(s->ws + L.off_edge + 8 * L.row * L.vsz, 0, 2 * (size_t)L.tiles * sizeof(int), s->st) != cudaSuccess)
         rc = fail(s, EG_ERR_CUDA, "edge-stencil counters");
     if (rc == EG_OK && s->use_tm64) {
         for (const void* f : {(const void*)k_thomas_tm64<0>, (const void*)k_thomas_tm64<1>, (const void*)k_thomas_tm64<2>})

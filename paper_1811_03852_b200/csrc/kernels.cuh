@@ -949,7 +949,8 @@ __device__ __forceinline__ void push_edge_tile(const Geo& g, const P2P& pp, int 
 // the elimination and back substitution there, 512 threads store.
 // grid (ceil(nx/64), 2): blockIdx.y 0 -> local row 0, 1 -> local row nyl-1.  smem er_smem_bytes.
 template <int MODE, int KIND>
-__global__ void __launch_bounds__(ER_THREADS) k_edge_rows(Geo g, Vecs<MODE> vv, float* __restrict__ zout, P2P pp) {
+__global__ void __launch_bounds__(ER_THREADS) k_edge_rows(Geo g, Vecs<MODE> vv, float* __restrict__ zout, P2P pp,
+                                                          float* pv_edge) {
     static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
     extern __shared__ __align__(16) float ersm[];
     const DevState* st = vv.st;
@@ -977,9 +978,14 @@ __global__ void __launch_bounds__(ER_THREADS) k_edge_rows(Geo g, Vecs<MODE> vv, 
     const int64_t row = blockIdx.y == 0 ? 0 : g.nyl - 1;
     const int64_t base = row * g.row + i;
     const float* __restrict__ A0 = vv.r + base;
-    // p = v = 0 after a (re)start: read r in their place with beta = 0 (as thomas_tm_tile)
-    const float* __restrict__ Pp = (KIND == 1 && fresh ? vv.r : vv.p) + base;
-    const float* __restrict__ Vv = (KIND == 1 && fresh ? vv.r : vv.v) + base;
+    // p = v = 0 after a (re)start: read r in their place with beta = 0 (as thomas_tm_tile).
+    // z (KIND 1) with pv_edge: p and v of the edge rows come from the band-edge copies [p, v][2][row]
+    // (this kernel's own p of the last iteration, the edge-row stencil's v), not from p / v, which
+    // the phase kernel running beside it rewrites; the new p goes back to the copy
+    const int64_t eb = (int64_t)blockIdx.y * g.row + i;
+    const float* Pp = KIND == 1 && fresh ? vv.r + base : (KIND == 1 && pv_edge ? pv_edge + eb : vv.p + base);
+    const float* Vv = KIND == 1 && fresh ? vv.r + base
+                      : (KIND == 1 && pv_edge ? pv_edge + 2 * g.row + eb : vv.v + base);
     if (KIND == 1 && fresh) beta = 0.f;
     const float* __restrict__ UD = vv.B2 + 2 * base;
     {  // all of this thread's levels (<= ER_MAXL) loaded before any is used: one round of latency
@@ -1000,6 +1006,7 @@ __global__ void __launch_bounds__(ER_THREADS) k_edge_rows(Geo g, Vecs<MODE> vv, 
                 float f;
                 if (KIND == 1) f = fmaf(beta, fmaf(-omega, v_[e], p_[e]), a_[e]);
                 else f = fmaf(-alpha, v_[e], a_[e]);
+                if (KIND == 1 && pv_edge && act) pv_edge[eb + (int64_t)k * nx] = f;  // p of this row, for the next one
                 F[k * ER_COLS + c] = f;
                 U[k * ER_COLS + c] = ud_[e].v[0];
                 D[k * ER_COLS + c] = ud_[e].v[1];
@@ -1367,7 +1374,7 @@ template <int MODE, int DOTS>
 __global__ void __launch_bounds__(512) k_edge_stencil(Geo g, Vecs<MODE> vv, const typename Prec<MODE>::V* __restrict__ z,
                                                       typename Prec<MODE>::V* __restrict__ y,
                                                       const typename Prec<MODE>::V* __restrict__ aux, RowMap rm, HWait hw,
-                                                      int* __restrict__ ctr) {
+                                                      int* __restrict__ ctr, typename Prec<MODE>::V* ycopy) {
     using V = typename Prec<MODE>::V;
     extern __shared__ __align__(16) unsigned char essm[];
     if (vv.st->halt != H_RUN) return;
@@ -1406,6 +1413,12 @@ __global__ void __launch_bounds__(512) k_edge_stencil(Geo g, Vecs<MODE> vv, cons
             a = fma(h2.v[0], zp, a);
             a = fma(h2.v[1], zm, a);
             y[rb + i + o] = a;
+#ifndef EG_MUTATE_NO_VCOPY  // mutation check of the band-edge copies (scripts/build_variant.sh)
+            if (ycopy) {  // v of the band-edge rows for k_edge_rows (slot 0: row 0, slot 1: row nyl-1)
+                if (jl == 0) ycopy[i + o] = a;
+                if (jl == g.nyl - 1) ycopy[g.row + i + o] = a;
+            }
+#endif
         }
     }
     if (DOTS == 0) return;
