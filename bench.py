@@ -264,6 +264,7 @@ def run_ours(args, prob, ws, rank, local):
         x = torch.empty(nloc, dtype=torch.float64, device=dev)
         s = egs.Solver((prob.nx, prob.ny, prob.nz), bands, args.precision, group=group, stream=stream,
                        batch=True)
+    transport = s.transport  # latitude bands: "p2p" (NVLink peer memory) or "nccl"; one GPU: "none"
 
     def barrier():
         if ws > 1:
@@ -424,7 +425,7 @@ def run_ours(args, prob, ws, rank, local):
         "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[args.precision], "data": "synthetic",
-        "config": config_dict(args, prob, ws),
+        "config": dict(config_dict(args, prob, ws), transport=transport),
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
