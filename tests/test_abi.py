@@ -110,3 +110,18 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "oracle.h" not in txt and "liboracle" not in txt
+
+
+def test_transport_codes_match_the_header(egs):
+    """eg_solver_transport's EG_TRANSPORT_* codes (include/egsolve.h) are the names the binding's
+    Solver.transport reports, and a NULL handle is an argument error."""
+    src = open(os.path.join(ROOT, "include", "egsolve.h")).read()
+    codes = {int(v): k for k, v in re.findall(r"#define EG_TRANSPORT_([A-Z0-9_]+)\s+(\d+)", src)}
+    assert codes == {0: "NONE", 1: "NCCL", 2: "P2P", 3: "LOOPBACK", 4: "LOOPBACK_P2P"}
+    assert {k: v.lower().replace("_", "-") for k, v in codes.items()} == egs.Solver.TRANSPORTS
+    assert egs.lib().eg_solver_transport(None) < 0
+    # the IPC test hooks reject NULL arguments without touching the GPU
+    rec = ctypes.create_string_buffer(80)
+    assert egs.lib().eg_debug_ipc_export(None, rec) == 1
+    p, o = ctypes.c_void_p(), ctypes.c_void_p()
+    assert egs.lib().eg_debug_ipc_open(None, ctypes.byref(p), ctypes.byref(o)) == 1
