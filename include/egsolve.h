@@ -211,8 +211,10 @@ int eg_solve_batch(eg_solver* s, int count, const double* const* b, double* cons
                    const double* const bands[7], const eg_solve_params* params, double* history,
                    eg_solve_info* info, int* done);
 
-/* Release the NCCL communicator (or the loopback-group membership), streams, events and graphs
- * (not the caller's workspace).  NULL is a no-op. */
+/* Release the NCCL communicator (or the loopback-group membership), the peer mappings of the P2P
+ * transport, streams, events and graphs (not the caller's workspace).  With latitude bands the
+ * other ranks write into this rank's workspace during solves: destroy a handle (and free its
+ * workspace) only once every rank's last collective call on it has returned.  NULL is a no-op. */
 void eg_solver_destroy(eg_solver* s);
 
 /* Human-readable detail of the last error on this handle ("" if none).  Valid until the next call. */
