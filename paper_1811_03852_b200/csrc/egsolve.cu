@@ -188,6 +188,7 @@ struct eg_solver {
     int nsm = 148;
     size_t smem_march = 0;
     int64_t epoch_base = 1;     // first epoch of the next solve (flags are reset before 2^30)
+    int gseq = 0;               // DevState.gseq carried from solve to solve (P2P gather buffers)
     int device = 0;             // the CUDA device the handle was created on
     int precond = EG_PRECOND_TRIDIAG;  // NEXT-1: EG_PRECOND_TRISOR selects red-black tri-SOR
     void* split = nullptr;             // colour-split B4 | B2 | f for tri-SOR (NULL: not available)
@@ -1274,6 +1275,7 @@ int solve_impl(eg_solver* s, const double* b, const double* x0, const eg_solve_p
     }
     h->epoch = (int)s->epoch_base;
     s->epoch_base += reserve;
+    h->gseq = s->gseq;  // the P2P gather buffers alternate with it across solves
     k_copy_words<<<1, 256, 0, s->st>>>((const uint32_t*)s->hstate_dev, (uint32_t*)s->dstate, (int)(sizeof(DevState) / 4));
     CK(cudaGetLastError());
 
@@ -2123,6 +2125,7 @@ int eg_solve(eg_solver* s, const double* b, const double* x0, const eg_solve_par
     // every finaliser launch bumps the epoch, including launches of a replayed chunk past a halt: the
     // next solve starts past the last epoch this one used (the host mirror is read after the last one)
     s->epoch_base = std::max<int64_t>(s->epoch_base, (int64_t)s->hstate->epoch + 1);
+    s->gseq = s->hstate->gseq;
     if (rc != EG_OK && info) info->status = rc;
     return rc;
 }

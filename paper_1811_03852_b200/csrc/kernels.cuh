@@ -1854,13 +1854,13 @@ __device__ __forceinline__ void x_snapshot(DevState* st) {
 // one-kernel finaliser: one CTA per (local) reduction group, the last CTA to finish runs the logic.
 // One GPU: all G groups are local.  Latitude bands with the P2P transport (pp.on, NCCL ranks):
 // every CTA also pushes its group's sums to every rank (p2p_push_group) and the last CTA waits for
-// all G groups' words of this epoch (p2p_gather) before the logic — the all-gather inside the
+// all G groups' words of this reduction (p2p_gather) before the logic — the all-gather inside the
 // finaliser, one launch per reduction as on one GPU.
 template <int WHICH> __device__ __forceinline__ bool fin_no_sums(const DevState* st);
 template <int WHICH>
-__device__ __forceinline__ void p2p_push_group(const Geo& g, const P2P& pp, const double* gsum, int gl, int epoch);
+__device__ __forceinline__ void p2p_push_group(const Geo& g, const P2P& pp, const double* gsum, int gl, int seq);
 template <int WHICH>
-__device__ __forceinline__ bool p2p_gather(const Geo& g, const P2P& pp, int epoch, double* gs);
+__device__ __forceinline__ bool p2p_gather(const Geo& g, const P2P& pp, int seq, double* gs);
 
 template <int MODE, int WHICH>
 __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __restrict__ slots, DevState* st,
@@ -1869,12 +1869,13 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __rest
     const uint32_t r32 = fin_r32<MODE>(WHICH);
     pdl_wait();
     pdl_launch_dependents();  // the next kernel may launch (and wait) while this small grid runs
-    // halt / sexit / epoch are read once, before this CTA's arrival: only the last CTA to arrive
-    // (after every CTA has read them) writes the state, so every CTA takes the same branch and
-    // stamps its pushes with the same epoch
+    // halt / sexit / epoch / gseq are read once, before this CTA's arrival: only the last CTA to
+    // arrive (after every CTA has read them) writes the state, so every CTA takes the same branch
+    // and stamps its pushes alike
     const int halt0 = *(volatile const int*)&st->halt;
     const int sexit0 = *(volatile const int*)&st->sexit;
     const int epoch = *(volatile const int*)&st->epoch;
+    const int gseq = *(volatile const int*)&st->gseq;
     if (WHICH != W_START && WHICH != W_VERIFY && halt0 != H_RUN) {  // (then nobody writes but this)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             st->epoch = epoch + 1;  // every finaliser launch bumps the epoch (stamps the next phase launch)
@@ -1888,7 +1889,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __rest
     __shared__ int last;
     __shared__ double gs[8 * 3];
     __syncthreads();
-    if (pp.on && sums) p2p_push_group<WHICH>(g, pp, gsum, blockIdx.x, epoch);
+    if (pp.on && sums) p2p_push_group<WHICH>(g, pp, gsum, blockIdx.x, gseq);
     if (threadIdx.x == 0) {
         __threadfence();  // this group's sums before the arrival
         last = atomicAdd(&st->fin_ctr, 1) == (int)gridDim.x - 1;
@@ -1896,11 +1897,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __rest
     __syncthreads();
     if (!last) return;
     bool ok = true;
-    if (pp.on && sums) ok = p2p_gather<WHICH>(g, pp, epoch, gs);
+    if (pp.on && sums) ok = p2p_gather<WHICH>(g, pp, gseq, gs);
     if (threadIdx.x == 0) {
         __threadfence();
         st->fin_ctr = 0;
         st->epoch = epoch + 1;
+        if (sums) st->gseq = gseq + 1;
         if (!ok) {
             st->halt = H_PEER_TIMEOUT;
         } else {
@@ -1911,10 +1913,14 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin(Geo g, const double* __rest
 }
 
 // The P2P all-gather of the group sums (pp.on): every fp64 sum travels as two 64-bit words
-// (epoch << 32 | one 32-bit half) into every rank's gather buffer (its own included) at
-// [epoch & 1][global group][q][half].  No fence: an aligned 64-bit store is single-copy atomic, so
-// a word whose epoch matches holds this epoch's half.  Two buffers: a rank can run at most one
-// reduction ahead of a slower one (DESIGN.md §7 P2P).
+// ((seq + 1) << 32 | one 32-bit half) into every rank's gather buffer (its own included) at
+// [seq & 1][global group][q][half], seq = DevState.gseq, the number of summing finalisers so far
+// (the same on every rank, kept across solves).  No fence: an aligned 64-bit store is single-copy
+// atomic, so a word whose stamp matches holds this reduction's half.  Two buffers, alternating
+// strictly: a rank can run at most one reduction ahead of a slower one, because its next needs the
+// slower rank's push of the current one, which that rank makes after consuming the previous one
+// (DESIGN.md §7 P2P).  (A stamp per pushing reduction, not the epoch: halted finalisers bump the
+// epoch without pushing, so epochs of consecutive pushes can share a parity.)
 template <int WHICH>
 __device__ __forceinline__ bool fin_no_sums(const DevState* st) {  // k_fin_groups' early exits
     return (WHICH != W_START && WHICH != W_VERIFY && st->halt != H_RUN) || (WHICH == W_C && st->sexit);
@@ -1922,35 +1928,36 @@ __device__ __forceinline__ bool fin_no_sums(const DevState* st) {  // k_fin_grou
 constexpr int P2P_GWORDS = 8 * 3 * 2;  // words per parity buffer: [group][q][half]
 // after fin_group_par + __syncthreads: this CTA's group (local index gl) to every rank
 template <int WHICH>
-__device__ __forceinline__ void p2p_push_group(const Geo& g, const P2P& pp, const double* gsum, int gl, int epoch) {
+__device__ __forceinline__ void p2p_push_group(const Geo& g, const P2P& pp, const double* gsum, int gl, int seq) {
     constexpr int NQ = fin_nq(WHICH);
     const int t = threadIdx.x;
     if (t < pp.nranks * NQ * 2) {  // one word per thread: rank r, sum q, half h
         const int r = t / (NQ * 2), q = (t >> 1) % NQ, h = t & 1;
-        const unsigned e = (unsigned)epoch + (pp.fault ? 1u : 0u);  // fault injection: a wrong stamp
+        const unsigned stamp = (unsigned)seq + 1u + (pp.fault ? 2u : 0u);  // fault injection: a wrong stamp
         const unsigned long long bits =
             (unsigned long long)__double_as_longlong(((volatile const double*)gsum)[gl * NQ + q]);
         const unsigned half = h ? (unsigned)(bits >> 32) : (unsigned)bits;
-        st_relaxed_sys_u64(pp.gall[r] + (e & 1u) * P2P_GWORDS + ((g.g_lo + gl) * 3 + q) * 2 + h,
-                           ((unsigned long long)e << 32) | half);
+        st_relaxed_sys_u64(pp.gall[r] + ((unsigned)seq & 1u) * P2P_GWORDS + ((g.g_lo + gl) * 3 + q) * 2 + h,
+                           ((unsigned long long)stamp << 32) | half);
     }
 }
-// all G groups' sums of this epoch from this rank's gather buffer into gs[G * NQ] (shared), the
+// all G groups' sums of reduction seq from this rank's gather buffer into gs[G * NQ] (shared), the
 // words polled by the CTA's threads in parallel; false if one did not arrive within the timeout.
 // Called by every thread of the CTA.
 template <int WHICH>
-__device__ __forceinline__ bool p2p_gather(const Geo& g, const P2P& pp, int epoch, double* gs) {
+__device__ __forceinline__ bool p2p_gather(const Geo& g, const P2P& pp, int seq, double* gs) {
     constexpr int NQ = fin_nq(WHICH);
     __shared__ unsigned gw[P2P_GWORDS];
-    const unsigned long long* b = pp.gall[pp.rank] + (unsigned)(epoch & 1) * P2P_GWORDS;
+    const unsigned long long* b = pp.gall[pp.rank] + ((unsigned)seq & 1u) * P2P_GWORDS;
+    const unsigned stamp = (unsigned)seq + 1u;
     bool bad = false;
     for (int w = threadIdx.x; w < g.G * NQ * 2; w += blockDim.x) {
         const int gi = w / (NQ * 2), rem = w % (NQ * 2);
         const unsigned long long* src = b + (gi * 3 + (rem >> 1)) * 2 + (rem & 1);
         unsigned long long v = ld_relaxed_sys_u64(src);
-        if ((unsigned)(v >> 32) != (unsigned)epoch) {
+        if ((unsigned)(v >> 32) != stamp) {
             const unsigned long long t0 = globaltimer_ns();
-            while ((unsigned)((v = ld_relaxed_sys_u64(src)) >> 32) != (unsigned)epoch) {
+            while ((unsigned)((v = ld_relaxed_sys_u64(src)) >> 32) != stamp) {
                 __nanosleep(100);
                 if ((long long)(globaltimer_ns() - t0) > pp.timeout_ns) { bad = true; break; }
             }
@@ -1978,7 +1985,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_fin_groups(Geo g, const double*
     fin_group_par<NQ>(g, slots, r32, blockIdx.x, gsum);
     if (pp.on) {
         __syncthreads();
-        p2p_push_group<WHICH>(g, pp, gsum, blockIdx.x, *(volatile const int*)&st->epoch);
+        p2p_push_group<WHICH>(g, pp, gsum, blockIdx.x, *(volatile const int*)&st->gseq);
     }
 }
 
@@ -1986,10 +1993,13 @@ template <int MODE, int WHICH>
 __global__ void k_fin_logic(Geo g, const double* __restrict__ gall, DevState* st, int first, P2P pp) {
     __shared__ double gs[8 * 3];
     const int epoch = *(volatile const int*)&st->epoch;
-    const bool p2p = pp.on && !fin_no_sums<WHICH>(st);
-    const bool ok = p2p ? p2p_gather<WHICH>(g, pp, epoch, gs) : true;
+    const int gseq = *(volatile const int*)&st->gseq;
+    const bool sums = !fin_no_sums<WHICH>(st);
+    const bool p2p = pp.on && sums;
+    const bool ok = p2p ? p2p_gather<WHICH>(g, pp, gseq, gs) : true;
     if (threadIdx.x == 0) {
         st->epoch = epoch + 1;
+        if (sums) st->gseq = gseq + 1;
         if (!ok) {
             st->halt = H_PEER_TIMEOUT;
         } else {
