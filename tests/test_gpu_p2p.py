@@ -152,3 +152,20 @@ def test_cuda_ipc_of_a_caching_allocator_slice():
     torch.cuda.synchronize()
     assert torch.equal(view.cpu(), torch.arange(n, dtype=torch.float64) * -2.0)
     assert bool((blk[:n + 37] == 7.25).all()) and bool((blk[2 * n + 37:] == 7.25).all())  # only the slice
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_p2p_split_update_knob_bitwise(split, monkeypatch):
+    """EG_SPLIT_UPDATE forces the update's x half onto the side stream (default off with P2P, on
+    with copies): either way the bands reproduce the single-GPU solve bitwise."""
+    prob = CASES[1]
+    monkeypatch.setenv("EG_FUSE", "1")
+    ref = Bands(prob, "mixed", 1)
+    x1, i1, h1 = ref.solve(tol=1e-6, maxit=30, restart_every=4)
+    monkeypatch.setenv("EG_SPLIT_UPDATE", split)
+    for p2p in (True, False):
+        run = _bands(prob, "mixed", 4, p2p, monkeypatch)
+        xP, iP, hP = run.solve(tol=1e-6, maxit=30, restart_every=4)
+        assert all(_same_info(i, i1[0]) for i in iP) and np.array_equal(xP, x1), (split, p2p)
+        run.close()
+    ref.close()
