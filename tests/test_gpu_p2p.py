@@ -169,3 +169,19 @@ def test_p2p_split_update_knob_bitwise(split, monkeypatch):
         assert all(_same_info(i, i1[0]) for i in iP) and np.array_equal(xP, x1), (split, p2p)
         run.close()
     ref.close()
+
+
+def test_p2p_with_programmatic_dependent_launch_bitwise(monkeypatch):
+    """EG_PDL=1 (phase kernels, update and one-kernel finalisers may launch before their predecessor
+    finished and wait on it in-kernel) on 4 bands: bitwise the default."""
+    prob = CASES[0]
+    monkeypatch.setenv("EG_FUSE", "1")
+    base = _bands(prob, "mixed", 4, True, monkeypatch)
+    x0, i0, h0 = base.solve(tol=1e-6, maxit=40, restart_every=5)
+    base.close()
+    monkeypatch.setenv("EG_PDL", "1")
+    run = _bands(prob, "mixed", 4, True, monkeypatch)
+    x1, i1, h1 = run.solve(tol=1e-6, maxit=40, restart_every=5)
+    run.close()
+    assert all(_same_info(a, b) for a, b in zip(i1, i0)) and np.array_equal(x1, x0)
+    assert all(np.array_equal(a, b) for a, b in zip(h1, h0))
