@@ -185,3 +185,37 @@ def test_p2p_with_programmatic_dependent_launch_bitwise(monkeypatch):
     run.close()
     assert all(_same_info(a, b) for a, b in zip(i1, i0)) and np.array_equal(x1, x0)
     assert all(np.array_equal(a, b) for a, b in zip(h1, h0))
+
+
+def test_random_band_shapes_bitwise():
+    """Seeded random grids (ragged tiles, odd nx, 1-row bands, nz from 1 to 80), random precision,
+    schedule and P: the P2P bands reproduce the single-GPU solve bitwise (x, history, info)."""
+    import os
+    rng = np.random.default_rng(1811)
+    for case in range(16):
+        nx = int(rng.integers(3, 300))
+        ny = int(rng.integers(8, 41))
+        nz = int(rng.integers(1, 73))
+        mode = ["mixed", "fp64", "fp32"][case % 3]
+        fuse = case % 2 == 0
+        if fuse:  # the fused phase kernels need nx % 4 == 0 (16-byte TMA strides)
+            nx = max(4, nx - nx % 4)
+        P = int(rng.choice([2, 4, 8]))
+        prob = gen.Problem(nx, ny, nz, seed=100 + case)
+        os.environ["EG_FUSE" if fuse else "EG_NO_FUSE"] = "1"
+        try:
+            ref = Bands(prob, mode, 1)
+            run = Bands(prob, mode, P)
+        finally:
+            os.environ.pop("EG_FUSE", None)
+            os.environ.pop("EG_NO_FUSE", None)
+        assert all(q.transport == "loopback-p2p" for q in run.s)
+        kw = dict(tol=1e-6, maxit=25, restart_every=4)
+        x1, i1, h1 = ref.solve(**kw)
+        xP, iP, hP = run.solve(**kw)
+        tag = (nx, ny, nz, mode, fuse, P)
+        assert all(_same_info(i, i1[0]) for i in iP), tag
+        assert np.array_equal(xP, x1), tag
+        assert all(np.array_equal(h, h1[0]) for h in hP), tag
+        ref.close()
+        run.close()
