@@ -738,7 +738,7 @@ VfyBufs g_vfy{};
 #endif
 
 // the ghost-row exchange of z (a = 0) / z_s (a = 1) after the Thomas kernel wrote all rows: a push
-// kernel (P2P) or the overlapped NCCL / loopback exchange (joined by halo_join)
+// kernel (P2P) or the overlapped NCCL / loopback exchange (joined by edge_join)
 template <class V>
 int halo_start_t(eg_solver* s, V* z, int a) {
     if (!s->pp.on) return halo_ghosted(s, z, true);
@@ -751,12 +751,12 @@ int halo_start(eg_solver* s, double* z, int a) { return halo_start_t<double>(s, 
 
 // Fused schedule, latitude bands: z (KIND 1) / z_s (KIND 2) of the band's edge rows, k_edge_rows
 // into the scratch rows, then either its own pushes into the neighbours' ghost rows (P2P) or the
-// NCCL / loopback exchange of the scratch rows on s->cst (ev_halo marks the end), beside the phase
-// kernel that s->st launches next.  z_s: k_edge_rows itself runs on s->cst too, beside phase B
-// (which writes s, z_s, t and reads r, v: nothing k_edge_rows reads).  z: on s->st ahead of phase A,
-// which updates p in place and rewrites v, the inputs of k_edge_rows' p update.  Profiled solves
-// keep everything on s->st, where the CUDA events are (and so does the loopback copy transport).
-// the edge rows on the communication stream?  (Loopback copies: the copies read the neighbours'
+// NCCL / loopback exchange of the scratch rows, all on s->cst (ev_halo marks the end) beside the
+// phase kernel.  Phase B writes s, z_s, t and reads r, v: nothing k_edge_rows<2> reads; phase A
+// rewrites p and v, so k_edge_rows<1> reads their band-edge copies instead.  Profiled solves keep
+// everything on s->st ahead of the phase kernel, where the CUDA events are (and so does the
+// loopback copy transport).
+// The edge rows on the communication stream?  (Loopback copies: the copies read the neighbours'
 // scratch rows, ordered after their k_edge_rows only if those ran on the one shared stream.)
 bool edge_on_cst(const eg_solver* s, int kind) { (void)kind; return !(s->profiling || (s->lb && !s->pp.on)); }
 
