@@ -82,9 +82,10 @@ bool make_layout(const eg_grid* g, int64_t nyl, int mode, Layout* L, uint32_t fe
     // FP64 phase kernels: 4 warp sums per (row, 128-column slot) (march64.cuh)
     L->off_hslots = o; o = align_up(o + (mode == EG_FP64 ? 3 * 4 * (size_t)nyl * L->tiles * 8 : 0), A);
     L->off_gsum = o;  o = align_up(o + 2 * 8 * 3 * 8, A);
-    // P2P transport (latitude bands): gather buffers [2][8][3][2] epoch-stamped words and the
-    // ghost-row flags [z, z_s][side][64-column tiles] — written by the other ranks through peer memory
-    L->off_p2p = o;   o = align_up(o + kP2PGall + 4 * (size_t)((g->nx + 63) / 64) * sizeof(int), A);
+    // P2P transport (latitude bands): gather buffers [2][8][3][2] stamped words, the ghost-row
+    // flags [z, z_s][side][64-column tiles] and the tri-SOR halo flags [2][side][tiles] — written by
+    // the other ranks through peer memory — and this rank's tri-SOR halo counter
+    L->off_p2p = o;   o = align_up(o + kP2PGall + (8 * (size_t)((g->nx + 63) / 64) + 4) * sizeof(int), A);
     // latitude bands: k_edge_rows' scratch rows [z, z_s][row 0, row nyl-1][row] and the band-edge
     // copies of p and v [p, v][row 0, row nyl-1][row] (fused schedule), then k_edge_stencil's arrival
     // counters [2 rows][tiles]
@@ -123,6 +124,7 @@ struct LoopGroup {
     std::vector<const unsigned char*> first, last;  // posted edge rows
     std::vector<const double*> gsum;                // posted group sums
     std::vector<unsigned char*> ws;                 // the ranks' workspaces (P2P transport)
+    std::vector<int> split;                         // the ranks have the colour-split tri-SOR region
 };
 constexpr int kMaxIt = 1 << 26;  // epochs (8 per iteration at most) stay far below 2^31
 constexpr char kLoopMagic[8] = {'E', 'G', 'L', 'O', 'O', 'P', 'B', 'K'};
@@ -396,7 +398,7 @@ int lb_fail(eg_solver* s) {
 // ---- P2P transport: the peer table ----
 // base[r]: rank r's workspace as this process addresses it.  Every rank's layout follows from the
 // grid, the precision and its band (valid_dist's group-aligned split), so only the bases travel.
-void p2p_table(eg_solver* s, unsigned char* const* base) {
+void p2p_table(eg_solver* s, unsigned char* const* base, int split_all) {
     P2P& pp = s->pp;
     pp = P2P{};
     pp.rank = s->rank;
@@ -418,16 +420,27 @@ void p2p_table(eg_solver* s, unsigned char* const* base) {
         Layout Lr;
         layout_of(r, &Lr);
         pp.gall[r] = (unsigned long long*)(base[r] + Lr.off_p2p);
+        int* hfl = (int*)(base[r] + Lr.off_p2p + kP2PGall);
+        // the colour-split x (tri-SOR sweeps), row 0 at split + 7 n + row (off_split = base_total
+        // whatever the features; every rank has the region, or none: split_all)
+        unsigned char* xs0 = base[r] + Lr.off_split + (size_t)(7 * Lr.n + Lr.row) * Lr.vsz;
         if (r == s->rank - 1) {  // our row 0 -> its ghost row nyl
-            pp.fdst_lo = (int*)(base[r] + Lr.off_p2p + kP2PGall);
+            pp.fdst_lo = hfl;
+            pp.tdst_lo = hfl + 4 * pp.tiles;
             for (int a = 0; a < 2; ++a) pp.dst_lo[a] = zext_of(r, Lr, a) + (size_t)(Lr.row + Lr.n) * Lr.vsz;
+            pp.dst_lo_x = s->split ? (void*)(xs0 + (size_t)Lr.n * Lr.vsz) : nullptr;
         }
         if (r == s->rank + 1) {  // our row nyl-1 -> its ghost row -1
-            pp.fdst_hi = (int*)(base[r] + Lr.off_p2p + kP2PGall);
+            pp.fdst_hi = hfl;
+            pp.tdst_hi = hfl + 4 * pp.tiles;
             for (int a = 0; a < 2; ++a) pp.dst_hi[a] = zext_of(r, Lr, a);
+            pp.dst_hi_x = s->split ? (void*)(xs0 - (size_t)Lr.row * Lr.vsz) : nullptr;
         }
     }
     pp.hflag = (const int*)(s->ws + s->L.off_p2p + kP2PGall);
+    pp.tflag = pp.hflag + 4 * pp.tiles;
+    pp.tcount = (int*)(s->ws + s->L.off_p2p + kP2PGall) + 8 * pp.tiles;
+    pp.tsor = split_all;
     pp.on = 1;
 }
 
@@ -478,9 +491,10 @@ int p2p_setup_nccl(eg_solver* s) {
     const int P = s->nranks;
     std::vector<unsigned char*> base(P, nullptr);
     base[s->rank] = s->ws;
-    int ok = 1;
+    int ok = 1, split_same = 1;
     if (P > 1) {
-        const Rec mine = ipc_export(s->ws);
+        Rec mine = ipc_export(s->ws);
+        mine.pad = s->split ? 1 : 0;  // has the colour-split tri-SOR region
         std::vector<Rec> all(P);
         Rec* d = nullptr;
         CK(cudaMalloc(&d, sizeof(Rec) * (P + 1)));
@@ -491,6 +505,7 @@ int p2p_setup_nccl(eg_solver* s) {
                             cudaMemcpy(all.data(), d, sizeof(Rec) * P, cudaMemcpyDeviceToHost) != cudaSuccess))
             rc = EG_ERR_CUDA;
         for (int r = 0; rc == EG_OK && r < P; ++r) {
+            if (all[r].pad != mine.pad) split_same = 0;
             if (!all[r].ok) { ok = 0; continue; }
             if (r == s->rank || !ok) continue;
             void* p = nullptr;
@@ -515,7 +530,8 @@ int p2p_setup_nccl(eg_solver* s) {
     }
     CK(cudaMemsetAsync(s->ws + s->L.off_p2p, 0, s->L.off_state - s->L.off_p2p, s->st));
     CK(cudaStreamSynchronize(s->st));
-    p2p_table(s, base.data());
+    // (split-ness differs between ranks: the tri-SOR halos stay on NCCL; ranks agree, all saw the records)
+    p2p_table(s, base.data(), split_same);
     // every rank has cleared its flags before any rank's first push (which comes after this barrier)
     int* one = nullptr;
     CK(cudaMalloc(&one, sizeof(int)));
@@ -530,9 +546,12 @@ int p2p_setup_nccl(eg_solver* s) {
 int p2p_setup_loop(eg_solver* s) {
     LoopGroup* G = s->lb;
     G->ws[s->rank] = s->ws;
+    G->split[s->rank] = s->split ? 1 : 0;
     CK(cudaMemsetAsync(s->ws + s->L.off_p2p, 0, s->L.off_state - s->L.off_p2p, s->st));
     if (!lb_barrier(G)) return lb_fail(s);  // every rank's clear is enqueued before any push
-    p2p_table(s, G->ws.data());
+    int same = 1;
+    for (int r = 0; r < s->nranks; ++r) same &= G->split[r] == G->split[s->rank];
+    p2p_table(s, G->ws.data(), same);
     return EG_OK;
 }
 
@@ -939,6 +958,23 @@ int iteration_fused(eg_solver* s, void* x_it) {
     return EG_OK;
 }
 
+// the halo after a tri-SOR half-sweep of the ghosted array arr (which: 0 z, 1 z_s, 2 colour-split
+// x): the P2P push + wait (k_push_sweep / k_wait_sweep; loopback: a barrier between them) or the
+// NCCL / loopback exchange.  in_solve: the sweep kernels skip halted iterations (so do these).
+int sweep_halo(eg_solver* s, void* arr, int which, bool in_solve) {
+    if (s->nranks == 1) return EG_OK;
+    if (!(s->pp.on && s->pp.tsor)) return halo_ghosted(s, arr);
+    const dim3 gp((unsigned)((s->grid.nx + ER_COLS - 1) / ER_COLS), 2u);
+    if (s->L.vsz == 8) k_push_sweep<double><<<gp, 256, 0, s->st>>>(s->geo, (const double*)arr, s->dstate, s->pp, which, in_solve);
+    else k_push_sweep<float><<<gp, 256, 0, s->st>>>(s->geo, (const float*)arr, s->dstate, s->pp, which, in_solve);
+    CK(cudaGetLastError());
+    int rc;
+    if ((rc = p2p_push_join(s))) return rc;
+    k_wait_sweep<<<1, 256, 0, s->st>>>(s->dstate, s->pp, in_solve, s->rank > 0, s->rank < s->nranks - 1);
+    CK(cudaGetLastError());
+    return EG_OK;
+}
+
 // the colour-split band copies of the tri-SOR sweeps for the current operator (set_operator writes
 // them itself once tri-SOR is selected; otherwise this pass derives them).  Called before an
 // iteration graph is captured, so that the one-time pass is never part of the replayed graph.
@@ -1023,7 +1059,8 @@ int apply_trisor(eg_solver* s, Vecs<MODE>& v, const typename Prec<MODE>::V* fin,
                 }
                 CK(cudaGetLastError());
             }
-            if ((rc = halo_ghosted(s, xs_half ? (void*)xsr : (void*)z))) return rc;
+            if ((rc = sweep_halo(s, xs_half ? (void*)xsr : (void*)z, xs_half ? 2 : (z == v.zs ? 1 : 0), KIND != 0)))
+                return rc;
         }
     return EG_OK;
 }
@@ -2249,6 +2286,7 @@ int eg_loopback_id(int nranks, char out[128]) {
     G->last.assign(nranks, nullptr);
     G->gsum.assign(nranks, nullptr);
     G->ws.assign(nranks, nullptr);
+    G->split.assign(nranks, 0);
     memset(out, 0, 128);
     memcpy(out, kLoopMagic, sizeof kLoopMagic);
     memcpy(out + 8, &G, sizeof G);

@@ -1060,6 +1060,56 @@ __global__ void __launch_bounds__(256) k_push_rows(Geo g, const V* __restrict__ 
     push_edge_tile<V>(g, pp, a, (int)blockIdx.y, z + row * g.row, *(volatile const int*)&st->epoch);
 }
 
+// P2P transport, tri-SOR (NEXT-1): the halo after every red-black half-sweep.  k_push_sweep pushes
+// rows 0 / nyl-1 of the array the half-sweep wrote (which: 0 z, 1 z_s, 2 the colour-split x) into
+// the neighbours' ghost rows and stamps their flags [seq & 1][side][tile] with seq + 1; k_wait_sweep
+// waits for the neighbours' stamps of the same seq, then advances this rank's counter (*tcount,
+// every rank the same sequence of half-sweeps).  Two flag buffers: a rank's push seq + 2 needs its
+// wait seq + 1, i.e. the neighbour's push seq + 1, made after that neighbour's wait seq.  The ghost
+// data itself is single-buffered: a push overwrites the neighbour's ghost row while that
+// neighbour's next half-sweep may read it, but that half-sweep reads only the other colour, whose
+// values the push rewrites unchanged (a half-sweep updates one colour).  check_halt: inside a
+// solve (KIND != 0) the sweeps of a halted iteration return early, and so do both kernels.
+template <class V>
+__global__ void __launch_bounds__(256) k_push_sweep(Geo g, const V* __restrict__ arr, const DevState* st, P2P pp, int which,
+                                                    int check_halt) {
+    if (check_halt && st->halt != H_RUN) return;
+    V* dst = (V*)(blockIdx.y == 0 ? (which == 2 ? pp.dst_lo_x : pp.dst_lo[which])
+                                   : (which == 2 ? pp.dst_hi_x : pp.dst_hi[which]));
+    int* fl = blockIdx.y == 0 ? pp.tdst_lo : pp.tdst_hi;
+    if (dst == nullptr || fl == nullptr) return;
+    const int seq = *(volatile const int*)pp.tcount;
+    const int64_t row = blockIdx.y == 0 ? 0 : g.nyl - 1;
+    const V* src = arr + row * g.row;
+    const int c = threadIdx.x % ER_COLS, kl = threadIdx.x / ER_COLS, nl = blockDim.x / ER_COLS;
+    const int i = blockIdx.x * ER_COLS + c;
+#ifndef EG_MUTATE_NO_SWEEP_PUSH  // mutation check of the tri-SOR P2P test (scripts/build_variant.sh)
+    if (i < g.nx)
+        for (int k = kl; k < (int)g.nz; k += nl) dst[(int64_t)k * g.nx + i] = src[(int64_t)k * g.nx + i];
+#endif
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        // our row 0 is rank-1's ghost row nyl (its side 1), our row nyl-1 rank+1's ghost row -1
+        st_release_sys(fl + ((seq & 1) * 2 + (blockIdx.y == 0 ? 1 : 0)) * pp.tiles + blockIdx.x, seq + 1);
+    }
+}
+__global__ void __launch_bounds__(256) k_wait_sweep(DevState* st, P2P pp, int check_halt, int wlo, int whi) {
+    if (check_halt && st->halt != H_RUN) return;
+    const int seq = *(volatile const int*)pp.tcount;
+    bool bad = false;
+    for (int t = threadIdx.x; t < 2 * pp.tiles; t += blockDim.x) {
+        const int side = t / pp.tiles;
+        if (side == 0 ? !wlo : !whi) continue;
+        if (!wait_flag_sys(pp.tflag + (seq & 1) * 2 * pp.tiles + t, seq + 1, pp.timeout_ns)) bad = true;
+    }
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        *pp.tcount = seq + 1;
+        if (bad) st->halt = H_PEER_TIMEOUT;
+    }
+}
+
 // The P2P wait of an edge-row stencil CTA (128 columns = flags 2 blockIdx.x, 2 blockIdx.x + 1):
 // the neighbours' pushes of this epoch into the ghost row(s) its row reads.  hw: this rank's halo
 // flags of the array [side][tiles64] (NULL: no wait).  false on timeout.

@@ -19,18 +19,22 @@ cfg = args[args.index("--config") + 1] if "--config" in args else "C3"
 P = int(args[args.index("--P") + 1]) if "--P" in args else 4
 reps = int(args[args.index("--reps") + 1]) if "--reps" in args else 6
 mode = args[args.index("--mode") + 1] if "--mode" in args else "mixed"
+trisor = "--trisor" in args  # the tri-SOR preconditioner (P2P half-sweep halos)
 prob = gen.CONFIGS[cfg]
 bands, bh = gen.host(prob)
 g = (prob.nx, prob.ny, prob.nz)
 row = prob.nx * prob.nz
-ref = egs.Solver(g, torch.from_numpy(bands).cuda(), mode)
+ref = egs.Solver(g, torch.from_numpy(bands).cuda(), mode, trisor=trisor)
 uid = egs.loopback_id(P)
 sv = []
 for r in range(P):
     j0, j1 = egs.band_rows(prob.ny, r, P)
     sv.append((egs.Solver(g, torch.from_numpy(np.ascontiguousarray(bands[:, j0 * row:j1 * row])).cuda(), mode,
-                          dist=(r, P, uid)), slice(j0 * row, j1 * row)))
-print(cfg, P, mode, sv[0][0].transport, flush=True)
+                          dist=(r, P, uid), trisor=trisor), slice(j0 * row, j1 * row)))
+if trisor:
+    for q in [ref] + [v[0] for v in sv]:
+        q.set_preconditioner("trisor", sweeps=3, omega=1.5)
+print(cfg, P, mode, "tri-SOR" if trisor else "T^-1", sv[0][0].transport, flush=True)
 rng = np.random.default_rng(7)
 bad = 0
 for rep in range(reps):
