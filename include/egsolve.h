@@ -250,10 +250,11 @@ int eg_loopback_id(int nranks, char out[128]);
  * that a peer never satisfies ends the solve with EG_ERR_NCCL after EG_P2P_TIMEOUT_MS (default
  * 60000) instead of hanging.  The loopback test transport uses the same P2P kernels on one GPU
  * (EG_TRANSPORT_LOOPBACK_P2P, built at the first solve) or host-barrier copies (EG_P2P=0,
- * EG_TRANSPORT_LOOPBACK).  Results are bitwise identical under every transport.  The tri-SOR
- * preconditioner's halo after each red-black half-sweep goes the same way (a push kernel and a
- * wait kernel; it needs every rank created with the same features).  The restart / verification
- * ghost rows of x and eg_apply_operator keep the NCCL exchange. */
+ * EG_TRANSPORT_LOOPBACK).  Results are bitwise identical under every transport.  The other halos
+ * go the same way, as a push kernel and a wait kernel: the tri-SOR preconditioner's after each
+ * red-black half-sweep (it needs every rank created with the same features), the ghost rows of x
+ * before a restart / the verification, and the input of eg_apply_operator.  After create, NCCL
+ * then carries nothing (loopback: from the first solve on). */
 #define EG_TRANSPORT_NONE 0          /* one GPU, no exchange                               */
 #define EG_TRANSPORT_NCCL 1
 #define EG_TRANSPORT_P2P 2

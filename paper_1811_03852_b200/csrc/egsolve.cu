@@ -429,12 +429,14 @@ void p2p_table(eg_solver* s, unsigned char* const* base, int split_all) {
             pp.tdst_lo = hfl + 4 * pp.tiles;
             for (int a = 0; a < 2; ++a) pp.dst_lo[a] = zext_of(r, Lr, a) + (size_t)(Lr.row + Lr.n) * Lr.vsz;
             pp.dst_lo_x = s->split ? (void*)(xs0 + (size_t)Lr.n * Lr.vsz) : nullptr;
+            pp.dst_lo_xg = base[r] + Lr.off_xg + (size_t)Lr.row * 8;  // its ghost row nyl of x
         }
         if (r == s->rank + 1) {  // our row nyl-1 -> its ghost row -1
             pp.fdst_hi = hfl;
             pp.tdst_hi = hfl + 4 * pp.tiles;
             for (int a = 0; a < 2; ++a) pp.dst_hi[a] = zext_of(r, Lr, a);
             pp.dst_hi_x = s->split ? (void*)(xs0 - (size_t)Lr.row * Lr.vsz) : nullptr;
+            pp.dst_hi_xg = base[r] + Lr.off_xg;  // its ghost row -1 of x
         }
     }
     pp.hflag = (const int*)(s->ws + s->L.off_p2p + kP2PGall);
@@ -961,11 +963,15 @@ int iteration_fused(eg_solver* s, void* x_it) {
 // the halo after a tri-SOR half-sweep of the ghosted array arr (which: 0 z, 1 z_s, 2 colour-split
 // x): the P2P push + wait (k_push_sweep / k_wait_sweep; loopback: a barrier between them) or the
 // NCCL / loopback exchange.  in_solve: the sweep kernels skip halted iterations (so do these).
-int sweep_halo(eg_solver* s, void* arr, int which, bool in_solve) {
+int sweep_halo(eg_solver* s, void* arr, int which, bool in_solve, size_t esz = 0) {
     if (s->nranks == 1) return EG_OK;
-    if (!(s->pp.on && s->pp.tsor)) return halo_ghosted(s, arr);
+    if (!(s->pp.on && (s->pp.tsor || which != 2))) {
+        if (which != 3) return halo_ghosted(s, arr);
+        return halo(s, arr, s->xg, (unsigned char*)s->xg + s->L.row * 8, esz);
+    }
+    if (esz == 0) esz = s->L.vsz;
     const dim3 gp((unsigned)((s->grid.nx + ER_COLS - 1) / ER_COLS), 2u);
-    if (s->L.vsz == 8) k_push_sweep<double><<<gp, 256, 0, s->st>>>(s->geo, (const double*)arr, s->dstate, s->pp, which, in_solve);
+    if (esz == 8) k_push_sweep<double><<<gp, 256, 0, s->st>>>(s->geo, (const double*)arr, s->dstate, s->pp, which, in_solve);
     else k_push_sweep<float><<<gp, 256, 0, s->st>>>(s->geo, (const float*)arr, s->dstate, s->pp, which, in_solve);
     CK(cudaGetLastError());
     int rc;
@@ -1166,7 +1172,7 @@ int start(eg_solver* s, void* x_it, const double* b, int entry, int xzero, const
     int rc;
     if (!xzero && s->nranks > 1) {  // fp64 (X) ghost rows of x
         X* x = (X*)x_it;
-        if ((rc = halo(s, x, s->xg, (unsigned char*)s->xg + s->L.row * 8, sizeof(X)))) return rc;
+        if ((rc = sweep_halo(s, x, 3, false, sizeof(X)))) return rc;
     }
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     s->next_fresh = true;
@@ -1195,7 +1201,7 @@ int verify(eg_solver* s, void* x_it) {
     int rc;
     if (s->nranks > 1) {
         X* x = (X*)x_it;
-        if ((rc = halo(s, x, s->xg, (unsigned char*)s->xg + s->L.row * 8, sizeof(X)))) return rc;
+        if ((rc = sweep_halo(s, x, 3, false, sizeof(X)))) return rc;
     }
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     {
@@ -1466,7 +1472,7 @@ int apply_impl(eg_solver* s, const void* x, void* y) {
     int rc;
     if (s->nranks > 1) {  // stage into the ghosted buffer and exchange halo rows
         CK(cudaMemcpyAsync(v.z, x, s->L.n * sizeof(V), cudaMemcpyDeviceToDevice, s->st));
-        if ((rc = halo_ghosted(s, v.z))) return rc;
+        if ((rc = sweep_halo(s, v.z, 0, false))) return rc;
         zin = v.z;
     }
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);

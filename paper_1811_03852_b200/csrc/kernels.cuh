@@ -1060,8 +1060,10 @@ __global__ void __launch_bounds__(256) k_push_rows(Geo g, const V* __restrict__ 
     push_edge_tile<V>(g, pp, a, (int)blockIdx.y, z + row * g.row, *(volatile const int*)&st->epoch);
 }
 
-// P2P transport, tri-SOR (NEXT-1): the halo after every red-black half-sweep.  k_push_sweep pushes
-// rows 0 / nyl-1 of the array the half-sweep wrote (which: 0 z, 1 z_s, 2 the colour-split x) into
+// P2P transport, tri-SOR (NEXT-1): the halo after every red-black half-sweep (and the sequenced
+// halos outside the iteration: x before a restart / the verification, the input of
+// eg_apply_operator).  k_push_sweep pushes rows 0 / nyl-1 of an array (which: 0 z, 1 z_s, 2 the
+// colour-split x, 3 the ghost rows of x) into
 // the neighbours' ghost rows and stamps their flags [seq & 1][side][tile] with seq + 1; k_wait_sweep
 // waits for the neighbours' stamps of the same seq, then advances this rank's counter (*tcount,
 // every rank the same sequence of half-sweeps).  Two flag buffers: a rank's push seq + 2 needs its
@@ -1074,8 +1076,8 @@ template <class V>
 __global__ void __launch_bounds__(256) k_push_sweep(Geo g, const V* __restrict__ arr, const DevState* st, P2P pp, int which,
                                                     int check_halt) {
     if (check_halt && st->halt != H_RUN) return;
-    V* dst = (V*)(blockIdx.y == 0 ? (which == 2 ? pp.dst_lo_x : pp.dst_lo[which])
-                                   : (which == 2 ? pp.dst_hi_x : pp.dst_hi[which]));
+    V* dst = (V*)(blockIdx.y == 0 ? (which == 3 ? pp.dst_lo_xg : which == 2 ? pp.dst_lo_x : pp.dst_lo[which])
+                                   : (which == 3 ? pp.dst_hi_xg : which == 2 ? pp.dst_hi_x : pp.dst_hi[which]));
     int* fl = blockIdx.y == 0 ? pp.tdst_lo : pp.tdst_hi;
     if (dst == nullptr || fl == nullptr) return;
     const int seq = *(volatile const int*)pp.tcount;

@@ -225,7 +225,8 @@ def test_random_band_shapes_bitwise():
 def test_p2p_trisor_halos_bitwise(mode, monkeypatch):
     """The tri-SOR preconditioner (NEXT-1) on bands: the halo after every red-black half-sweep by
     P2P pushes + waits (k_push_sweep / k_wait_sweep) equals the copy transport and the single-GPU
-    solve bitwise, for solves and for eg_precondition after a solve (the counter persists)."""
+    solve bitwise, for solves (with restarts: the x ghost rows go the same way) and for
+    eg_precondition / eg_apply_operator after a solve (the counter persists)."""
     prob = gen.Problem(96, 24, 13, seed=17)  # nx even: red-black tri-SOR
     ref = Bands(prob, mode, 1, trisor=True)
     for q in ref.s:
@@ -234,6 +235,7 @@ def test_p2p_trisor_halos_bitwise(mode, monkeypatch):
     dt = torch.float64 if mode == "fp64" else torch.float32
     xin = torch.from_numpy(np.random.default_rng(5).standard_normal(prob.n)).to(dt).cuda()
     z1 = ref.call("precondition", xin)
+    y1 = ref.call("apply", xin)
     for P in (2, 4, 8):
         for p2p in (True, False):
             run = _bands(prob, mode, P, p2p, monkeypatch, trisor=True)
@@ -244,5 +246,6 @@ def test_p2p_trisor_halos_bitwise(mode, monkeypatch):
                 assert all(_same_info(i, i1[0]) for i in iP) and np.array_equal(xP, x1), (P, p2p)
                 assert all(np.array_equal(h, h1[0]) for h in hP), (P, p2p)
             assert torch.equal(run.call("precondition", xin), z1), (P, p2p)
+            assert torch.equal(run.call("apply", xin), y1), (P, p2p)  # the input's halo after solves: P2P too
             run.close()
     ref.close()
