@@ -54,8 +54,8 @@ int main(int argc, char** argv) {
         printf("%-44s %8.2f us per launch (%s)\n", name, 1000.f * ms / 400, cudaGetErrorString(cudaGetLastError()));
     };
     printf("band %d x %d x %d (fp32 V)\n", nx, nyl, nz);
-    timeit("k_edge_rows<1> (z, staged)", [&] { k_edge_rows<MODE, 1><<<ge, ER_THREADS, ers>>>(g, vv, scratch, pp); });
-    timeit("k_edge_rows<2> (z_s, staged)", [&] { k_edge_rows<MODE, 2><<<ge, ER_THREADS, ers>>>(g, vv, scratch, pp); });
+    timeit("k_edge_rows<1> (z, staged)", [&] { k_edge_rows<MODE, 1><<<ge, ER_THREADS, ers>>>(g, vv, scratch, pp, nullptr); });
+    timeit("k_edge_rows<2> (z_s, staged)", [&] { k_edge_rows<MODE, 2><<<ge, ER_THREADS, ers>>>(g, vv, scratch, pp, nullptr); });
     timeit("k_stencil<1> on the 2 edge rows (column walk)",
            [&] { k_stencil<MODE, 1><<<dim3(g.tiles, 2), RW>>>(g, vv, vv.z, vv.v, vv.rh, rm); });
     int* ctr = (int*)alloc(2 * g.tiles * 4);
@@ -64,16 +64,16 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(k_edge_stencil<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ess);
     cudaFuncSetAttribute(k_edge_stencil<MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ess);
     timeit("k_edge_stencil<1>", [&] {
-        k_edge_stencil<MODE, 1><<<dim3(g.tiles, 2, (nz + 3) / 4), 512, ess>>>(g, vv, vv.z, vv.v, vv.rh, rm, HWait{nullptr, 0, 0, 0, 0}, ctr);
+        k_edge_stencil<MODE, 1><<<dim3(g.tiles, 2, (nz + 3) / 4), 512, ess>>>(g, vv, vv.z, vv.v, vv.rh, rm, HWait{nullptr, 0, 0, 0, 0}, ctr, nullptr);
     });
     timeit("k_edge_stencil<0> (points only)", [&] {
-        k_edge_stencil<MODE, 0><<<dim3(g.tiles, 2, (nz + 3) / 4), 512, ess>>>(g, vv, vv.z, vv.v, vv.rh, rm, HWait{nullptr, 0, 0, 0, 0}, ctr);
+        k_edge_stencil<MODE, 0><<<dim3(g.tiles, 2, (nz + 3) / 4), 512, ess>>>(g, vv, vv.z, vv.v, vv.rh, rm, HWait{nullptr, 0, 0, 0, 0}, ctr, nullptr);
     });
     timeit("k_stencil<2> on the 2 edge rows (column walk)",
            [&] { k_stencil<MODE, 2><<<dim3(g.tiles, 2), RW>>>(g, vv, vv.zs = vv.z, vv.t, vv.s, rm); });
     timeit("k_edge_stencil<2>", [&] {
-        k_edge_stencil<MODE, 2><<<dim3(g.tiles, 2, (nz + 3) / 4), 512, ess>>>(g, vv, vv.z, vv.t, vv.s, rm, HWait{nullptr, 0, 0, 0, 0}, ctr);
+        k_edge_stencil<MODE, 2><<<dim3(g.tiles, 2, (nz + 3) / 4), 512, ess>>>(g, vv, vv.z, vv.t, vv.s, rm, HWait{nullptr, 0, 0, 0, 0}, ctr, nullptr);
     });
-    timeit("k_copy-like empty kernel (1 CTA, launch floor)", [&] { k_edge_stencil<MODE, 0><<<dim3(1, 1, 1), 32, ess>>>(g, vv, vv.z, vv.v, vv.rh, RowMap{0, 0}, HWait{nullptr, 0, 0, 0, 0}, ctr); });
+    timeit("k_copy-like empty kernel (1 CTA, launch floor)", [&] { k_edge_stencil<MODE, 0><<<dim3(1, 1, 1), 32, ess>>>(g, vv, vv.z, vv.v, vv.rh, RowMap{0, 0}, HWait{nullptr, 0, 0, 0, 0}, ctr, nullptr); });
     return 0;
 }

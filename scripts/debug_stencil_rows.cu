@@ -60,7 +60,7 @@ int run(int nx, int nyl, int nz) {
     int* ctr; cudaMalloc(&ctr, 2 * g.tiles * 4); cudaMemset(ctr, 0, 2 * g.tiles * 4);
     cudaFuncSetAttribute(k_edge_stencil<MODE, DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)es_smem_bytes<MODE>());
     k_edge_stencil<MODE, DOTS><<<dim3(g.tiles, nr, (nz + 3) / 4), 512, es_smem_bytes<MODE>()>>>(g, vv, z + row, y2, a, rm,
-                                                                                              HWait{nullptr, 0, 0, 0, 0}, ctr);
+                                                                                              HWait{nullptr, 0, 0, 0, 0}, ctr, nullptr);
     double* s3; cudaMalloc(&s3, 3 * nyl * g.tiles * 8); cudaMemset(s3, 0, 3 * nyl * g.tiles * 8);
     vv.slots = s3;
     k_naive<MODE, DOTS><<<dim3(g.tiles, nr), RW>>>(g, vv, y1, a, rm);
