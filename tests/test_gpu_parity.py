@@ -654,3 +654,34 @@ def test_programmatic_dependent_launch_bitwise(mode, monkeypatch):
         x1, i1, h1 = s1.solve(bt, **kw)
         x2, i2, h2 = s2.solve(bt, **kw)
         assert i1.iters == i2.iters and np.array_equal(h1, h2) and torch.equal(x1, x2)
+
+
+_RNG_T = np.random.default_rng(1853)
+RANDOM_TRISOR = [gen.Problem(2 * int(_RNG_T.integers(2, 150)), int(_RNG_T.integers(1, 40)), int(_RNG_T.integers(1, 90)),
+                             seed=200 + k) for k in range(8)]  # nx even: red-black tri-SOR
+
+
+@pytest.mark.parametrize("k", range(len(RANDOM_TRISOR)))
+def test_random_trisor_parity(k):
+    """NEXT-1 on seeded random shapes (nz up to 89: both the TMA sweeps and k_sor_half): the
+    tri-SOR sweeps against the oracle's Eq. 7 sweeps, natural and colour-split arrays bitwise equal,
+    and a tri-SOR solve that converges with the oracle's solution."""
+    prob = RANDOM_TRISOR[k]
+    mode = MODES[k % 3]
+    sweeps, omega = (3, 1.5) if k % 2 == 0 else (2, 1.2)
+    s, bands, b = _make(prob, mode)
+    s.set_preconditioner("trisor", sweeps=sweeps, omega=omega)
+    g = (prob.nx, prob.ny, prob.nz)
+    ahat, diag = oracle.scale(g, bands, mode)
+    f = np.random.default_rng(k).standard_normal(prob.n).astype(_vnp(mode))
+    z = s.precondition(torch.from_numpy(f).cuda())
+    zo = oracle.trisor(g, "fp64", ahat, f.astype(np.float64), sweeps=sweeps, omega=omega)
+    assert _rel(z.cpu().numpy().astype(np.float64), zo) <= (1e-12 if mode == "fp64" else 1e-5), (prob, mode)
+    st = egs.Solver(g, torch.from_numpy(bands).cuda(), mode, trisor=True)
+    st.set_preconditioner("trisor", sweeps=sweeps, omega=omega)
+    assert torch.equal(st.precondition(torch.from_numpy(f).cuda()), z), (prob, mode)
+    tol = 1e-4
+    xo, ho, io = oracle.solve(g, mode, ahat, diag, b, tol=tol, maxit=200)
+    xg, info, h = st.solve(torch.from_numpy(b).cuda(), tol=tol, maxit=200)
+    assert info.converged and info.true_R < tol, (prob, mode, info)
+    assert _rel(xg.cpu().numpy(), xo) <= 50 * tol, (prob, mode)
