@@ -1107,14 +1107,14 @@ int iteration(eg_solver* s, void* x_it) {
     {
         ProfScope ps(s, KID_THOMAS_P);
         if constexpr (MODE != 0) {
-            if (s->use_tm) k_thomas_tm<MODE, 1><<<gtm, 128, s->smem_tm, s->st>>>(s->geo, v, nullptr, v.z);
-            else if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
-            else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+            if (s->use_tm) CK(launch_ex(false, s->pdl, k_thomas_tm<MODE, 1>, dim3(gtm), dim3(128), s->smem_tm, s->st, s->geo, v, nullptr, v.z));
+            else if (s->cpt == 2) CK(launch_ex(false, s->pdl, k_thomas<MODE, 1, 2>, dim3(gt), dim3(tth), s->smem_th, s->st, s->geo, v, nullptr, v.z));
+            else CK(launch_ex(false, s->pdl, k_thomas<MODE, 1, 1>, dim3(gt), dim3(tth), s->smem_th, s->st, s->geo, v, nullptr, v.z));
         } else {
-            if (s->th_tma64) k_thomas_tma64<1><<<s->nsm, T6_THREADS, T6_SMEM, s->st>>>(s->geo, v, v.z, s->thmaps64);
-            else if (s->use_tm64) k_thomas_tm64<1><<<gtm, 128, TM64_SMEM, s->st>>>(s->geo, v, nullptr, v.z);
-            else if (s->cpt == 2) k_thomas<MODE, 1, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
-            else k_thomas<MODE, 1, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.z);
+            if (s->th_tma64) CK(launch_ex(false, s->pdl, k_thomas_tma64<1>, dim3(s->nsm), dim3(T6_THREADS), T6_SMEM, s->st, s->geo, v, v.z, s->thmaps64));
+            else if (s->use_tm64) CK(launch_ex(false, s->pdl, k_thomas_tm64<1>, dim3(gtm), dim3(128), TM64_SMEM, s->st, s->geo, v, nullptr, v.z));
+            else if (s->cpt == 2) CK(launch_ex(false, s->pdl, k_thomas<MODE, 1, 2>, dim3(gt), dim3(tth), s->smem_th, s->st, s->geo, v, nullptr, v.z));
+            else CK(launch_ex(false, s->pdl, k_thomas<MODE, 1, 1>, dim3(gt), dim3(tth), s->smem_th, s->st, s->geo, v, nullptr, v.z));
         }
         CK(cudaGetLastError());
     }
@@ -1126,7 +1126,7 @@ int iteration(eg_solver* s, void* x_it) {
             if ((rc = edge_join(s, 0, !s->pp.on))) return rc;
             if ((rc = stencil_rows<MODE, 1>(s, v.z, v.v, v.rh, true, 0))) return rc;
         } else {
-            k_stencil<MODE, 1><<<gr, RW, 0, s->st>>>(s->geo, v, v.z, v.v, v.rh, ALL_ROWS);
+            CK(launch_ex(false, s->pdl, k_stencil<MODE, 1>, dim3(gr), dim3(RW), 0, s->st, s->geo, v, v.z, v.v, v.rh, ALL_ROWS));
             CK(cudaGetLastError());
         }
     }
@@ -1134,15 +1134,15 @@ int iteration(eg_solver* s, void* x_it) {
     {
         ProfScope ps(s, KID_THOMAS_S);
         if constexpr (MODE != 0) {
-            if (s->use_tm) k_thomas_tm<MODE, 2><<<gtm, 128, s->smem_tm, s->st>>>(s->geo, v, nullptr, v.zs);
-            else if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
-            else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+            if (s->use_tm) CK(launch_ex(false, s->pdl, k_thomas_tm<MODE, 2>, dim3(gtm), dim3(128), s->smem_tm, s->st, s->geo, v, nullptr, v.zs));
+            else if (s->cpt == 2) CK(launch_ex(false, s->pdl, k_thomas<MODE, 2, 2>, dim3(gt), dim3(tth), s->smem_th, s->st, s->geo, v, nullptr, v.zs));
+            else CK(launch_ex(false, s->pdl, k_thomas<MODE, 2, 1>, dim3(gt), dim3(tth), s->smem_th, s->st, s->geo, v, nullptr, v.zs));
         } else {
             // (the TMA-fed kernel is slower for this lighter solve, 3.68 vs 3.40 ms at C5: one CTA per SM
             // cannot hide the FP64 recurrence the 2-CTA TMEM kernel overlaps)
-            if (s->use_tm64) k_thomas_tm64<2><<<gtm, 128, TM64_SMEM, s->st>>>(s->geo, v, nullptr, v.zs);
-            else if (s->cpt == 2) k_thomas<MODE, 2, 2><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
-            else k_thomas<MODE, 2, 1><<<gt, tth, s->smem_th, s->st>>>(s->geo, v, nullptr, v.zs);
+            if (s->use_tm64) CK(launch_ex(false, s->pdl, k_thomas_tm64<2>, dim3(gtm), dim3(128), TM64_SMEM, s->st, s->geo, v, nullptr, v.zs));
+            else if (s->cpt == 2) CK(launch_ex(false, s->pdl, k_thomas<MODE, 2, 2>, dim3(gt), dim3(tth), s->smem_th, s->st, s->geo, v, nullptr, v.zs));
+            else CK(launch_ex(false, s->pdl, k_thomas<MODE, 2, 1>, dim3(gt), dim3(tth), s->smem_th, s->st, s->geo, v, nullptr, v.zs));
         }
         CK(cudaGetLastError());
     }
@@ -1154,7 +1154,7 @@ int iteration(eg_solver* s, void* x_it) {
             if ((rc = edge_join(s, 1, !s->pp.on))) return rc;
             if ((rc = stencil_rows<MODE, 2>(s, v.zs, v.t, v.s, true, 1))) return rc;
         } else {
-            k_stencil<MODE, 2><<<gr, RW, 0, s->st>>>(s->geo, v, v.zs, v.t, v.s, ALL_ROWS);
+            CK(launch_ex(false, s->pdl, k_stencil<MODE, 2>, dim3(gr), dim3(RW), 0, s->st, s->geo, v, v.zs, v.t, v.s, ALL_ROWS));
             CK(cudaGetLastError());
         }
     }

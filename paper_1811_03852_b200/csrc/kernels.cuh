@@ -71,6 +71,12 @@ __device__ __forceinline__ void stv(T* p, const VecN<T, N>& a) { *reinterpret_ca
 // before it reads anything that kernel writes, and lets its own dependents launch early.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// first thing of a kernel the iteration may launch programmatically (EG_PDL): wait for the previous
+// kernel's completion (a no-op for a normal launch), then let the next one launch and wait likewise
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_launch_dependents();
+}
 
 // L2 prefetch of a future level (no register cost): the register batches then see L2 latency
 __device__ __forceinline__ void pf_l2(const void* p) {
@@ -453,6 +459,7 @@ template <int MODE, int KIND, int CPT>
 __global__ void __launch_bounds__(128) k_thomas(Geo g, Vecs<MODE> vv,
                                                 const typename Prec<MODE>::V* __restrict__ fin,
                                                 typename Prec<MODE>::V* __restrict__ zout) {
+    pdl_enter();  // (EG_PDL: the iteration may launch this kernel programmatically)
     using V = typename Prec<MODE>::V;
     // levels per batch; the next batch is in flight while the current one is eliminated.  Occupancy
     // is bounded by the shared-memory factors (3 CTAs / SM), not registers, so batches are deep.
@@ -739,6 +746,7 @@ __device__ __forceinline__ void thomas_tm_tile(const Geo& g, const Vecs<MODE>& v
 template <int MODE, int KIND>
 __global__ void __launch_bounds__(128, 4) k_thomas_tm(Geo g, Vecs<MODE> vv, const float* __restrict__ fin,
                                                       float* __restrict__ zout) {
+    pdl_enter();  // (EG_PDL: the iteration may launch this kernel programmatically)
     static_assert(sizeof(typename Prec<MODE>::V) == 4, "fp32 working precision only");
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ uint32_t tm_base;
@@ -775,6 +783,7 @@ constexpr int TM64_SMEM = 80 * 1024;  // >= nz * 128 * 8 (nz <= 80); > 228 KB / 
 template <int KIND>
 __global__ void __launch_bounds__(128, 2) k_thomas_tm64(Geo g, Vecs<0> vv, const double* __restrict__ fin,
                                                         double* __restrict__ zout) {
+    pdl_enter();  // (EG_PDL: the iteration may launch this kernel programmatically)
     using V = double;
     constexpr int KB = 4;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -1314,6 +1323,7 @@ __global__ void __launch_bounds__(RW, 4) k_stencil(Geo g, Vecs<MODE> vv,
                                                 const typename Prec<MODE>::V* __restrict__ z,
                                                 typename Prec<MODE>::V* __restrict__ y,
                                                 const typename Prec<MODE>::V* __restrict__ aux, RowMap rm) {
+    pdl_enter();  // (EG_PDL: the iteration may launch this kernel programmatically)
     using V = typename Prec<MODE>::V;
     if (DOTS != 0 && vv.st->halt != H_RUN) return;
     constexpr int NQ = DOTS == 2 ? 3 : 1;
@@ -1550,7 +1560,7 @@ __global__ void __launch_bounds__(RW) k_update(Geo g, Vecs<MODE> vv) {
     using VC = VecN<V, CPT>;
     using XC = VecN<X, CPT>;
     const DevState* st = vv.st;
-    pdl_wait();
+    pdl_enter();
     if (PART == 2 ? st->xs_run == 0 : st->halt != H_RUN) return;
     const bool sexit = (PART == 2 ? st->xs_sexit : st->sexit) != 0;
     const bool xz = (PART == 2 ? st->xs_xzero : st->xzero) != 0;  // x = 0 (not stored): first update after x0 = 0

@@ -490,6 +490,7 @@ struct ThomasMaps64 {
 template <int KIND>
 __global__ void __launch_bounds__(T6_THREADS, 1) k_thomas_tma64(Geo g, Vecs<0> vv, double* __restrict__ zout,
                                                                  const __grid_constant__ ThomasMaps64 maps) {
+    pdl_enter();  // (EG_PDL: the iteration may launch this kernel programmatically)
     using V = double;
     extern __shared__ __align__(128) unsigned char smtma[];
     __shared__ __align__(8) uint64_t full[T6_STAGES], empty[T6_STAGES];

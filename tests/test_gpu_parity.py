@@ -639,14 +639,16 @@ def test_random_shapes_parity(k, monkeypatch):
     assert _rel(xg.cpu().numpy(), xo) <= 10 * tol
 
 
-@pytest.mark.parametrize("mode", ["mixed", "fp32"])
-def test_programmatic_dependent_launch_bitwise(mode, monkeypatch):
-    """EG_PDL=1 (programmatic dependent launches in the fused iteration) changes no result."""
+@pytest.mark.parametrize("mode", ["mixed", "fp32", "fp64"])
+@pytest.mark.parametrize("sched", ["EG_FUSE", "EG_NO_FUSE"])
+def test_programmatic_dependent_launch_bitwise(mode, sched, monkeypatch):
+    """EG_PDL=1 (programmatic dependent launches of the iteration's kernels, fused or 5-kernel
+    schedule) changes no result."""
     prob = gen.Problem(256, 40, 30, seed=33)
     bands, b = gen.host(prob)
     g = (prob.nx, prob.ny, prob.nz)
     bd, bt = torch.from_numpy(bands).cuda(), torch.from_numpy(b).cuda()
-    monkeypatch.setenv("EG_FUSE", "1")
+    monkeypatch.setenv(sched, "1")
     s1 = egs.Solver(g, bd, mode)
     monkeypatch.setenv("EG_PDL", "1")
     s2 = egs.Solver(g, bd, mode)
