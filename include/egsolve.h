@@ -250,11 +250,12 @@ int eg_loopback_id(int nranks, char out[128]);
  * that a peer never satisfies ends the solve with EG_ERR_NCCL after EG_P2P_TIMEOUT_MS (default
  * 60000) instead of hanging.  The loopback test transport uses the same P2P kernels on one GPU
  * (EG_TRANSPORT_LOOPBACK_P2P, built at the first solve) or host-barrier copies (EG_P2P=0,
- * EG_TRANSPORT_LOOPBACK).  Results are bitwise identical under every transport.  The other halos
- * go the same way, as a push kernel and a wait kernel: the tri-SOR preconditioner's after each
- * red-black half-sweep (it needs every rank created with the same features), the ghost rows of x
- * before a restart / the verification, and the input of eg_apply_operator.  After create, NCCL
- * then carries nothing (loopback: from the first solve on). */
+ * EG_TRANSPORT_LOOPBACK).  Results are bitwise identical under every transport.  The tri-SOR
+ * preconditioner's halo after each red-black half-sweep (it needs every rank created with the
+ * same features) and the ghost rows of x before a restart / the verification go the same way, as
+ * a push kernel and a wait kernel.  eg_apply_operator keeps the NCCL / copy exchange, which the
+ * receiver writes itself: consecutive applies have no global sum between them that would keep a
+ * pushing neighbour from overwriting a ghost row not yet read. */
 #define EG_TRANSPORT_NONE 0          /* one GPU, no exchange                               */
 #define EG_TRANSPORT_NCCL 1
 #define EG_TRANSPORT_P2P 2

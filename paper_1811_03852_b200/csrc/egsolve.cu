@@ -1470,10 +1470,15 @@ int apply_impl(eg_solver* s, const void* x, void* y) {
     using V = typename Prec<MODE>::V;
     const V* zin = (const V*)x;
     int rc;
-    if (s->nranks > 1) {  // stage into the ghosted buffer and exchange halo rows
-        CK(cudaMemcpyAsync(v.z, x, s->L.n * sizeof(V), cudaMemcpyDeviceToDevice, s->st));
-        if ((rc = sweep_halo(s, v.z, 0, false))) return rc;
-        zin = v.z;
+    if (s->nranks > 1) {  // stage into a ghosted buffer and exchange halo rows
+        // (NCCL / loopback copies, written by the receiver itself, even with the P2P transport: two
+        // applies in a row have no global sum between them, so a pushing neighbour could overwrite a
+        // ghost row this rank's stencil has not read yet.  z_s, not z: a tri-SOR eg_precondition
+        // pushes into z and could likewise overtake this stencil; the pushes into z_s all come
+        // inside a solve, after a global sum this rank takes part in only after its apply.)
+        CK(cudaMemcpyAsync(v.zs, x, s->L.n * sizeof(V), cudaMemcpyDeviceToDevice, s->st));
+        if ((rc = halo_ghosted(s, v.zs))) return rc;
+        zin = v.zs;
     }
     const dim3 gr((unsigned)s->L.tiles, (unsigned)s->L.nyl);
     ProfScope ps(s, KID_APPLY);

@@ -226,7 +226,7 @@ def test_p2p_trisor_halos_bitwise(mode, monkeypatch):
     """The tri-SOR preconditioner (NEXT-1) on bands: the halo after every red-black half-sweep by
     P2P pushes + waits (k_push_sweep / k_wait_sweep) equals the copy transport and the single-GPU
     solve bitwise, for solves (with restarts: the x ghost rows go the same way) and for
-    eg_precondition / eg_apply_operator after a solve (the counter persists)."""
+    eg_precondition after a solve (the counter persists), with eg_apply_operator in between."""
     prob = gen.Problem(96, 24, 13, seed=17)  # nx even: red-black tri-SOR
     ref = Bands(prob, mode, 1, trisor=True)
     for q in ref.s:
@@ -246,6 +246,6 @@ def test_p2p_trisor_halos_bitwise(mode, monkeypatch):
                 assert all(_same_info(i, i1[0]) for i in iP) and np.array_equal(xP, x1), (P, p2p)
                 assert all(np.array_equal(h, h1[0]) for h in hP), (P, p2p)
             assert torch.equal(run.call("precondition", xin), z1), (P, p2p)
-            assert torch.equal(run.call("apply", xin), y1), (P, p2p)  # the input's halo after solves: P2P too
+            assert torch.equal(run.call("apply", xin), y1), (P, p2p)  # (its halo: NCCL / copies, on z_s)
             run.close()
     ref.close()
